@@ -1,0 +1,375 @@
+#!/usr/bin/env python3
+"""bench.py -- space-time multigrid V-cycle throughput on B200.
+
+Workload (BASELINE.json configs[1], the single-B200 case the metric is quoted
+on): 2D heat equation on the unit square, Q1 on a uniform 128x128 grid (127^2
+interior nodes), T = 1, N_t = 256, DG p_t = 1, FP64; f i.i.d. uniform[-1,1]
+per space-time dof and u0 i.i.d. uniform[-1,1] per interior node (seed 42,
+counter-based generator); zero initial guess; V(1,1) cycles
+with damped block Jacobi (omega_t = 1/2, exact block solves), mu-driven
+coarsening; stop at ||r_k|| <= 1e-8 ||r_0||.
+
+One step = one full solve to 1e-8 (basis transforms included) on inputs
+resident in HBM.  value = fine DoF x V-cycles / s, summed over ranks.
+e2e = the same through stmg_solve_host with pinned HOST buffers (H2D of f and
+u, D2H of u inside the timed region).  --impl reference times the CPU oracle
+(the reference algorithm restated in C++/OpenMP; the reference itself cannot
+be built here) on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "C1": dict(p_t=1, dim=1, space_level=5, time_level=6, t_final=1.0, random_u0=False,
+               desc="configs[0]: 1D heat, Q1 h=1/64 (63 nodes), N_t=64, p_t=1"),
+    "C2": dict(p_t=1, dim=2, space_level=6, time_level=8, t_final=1.0, random_u0=True,
+               desc="configs[1]: 2D heat, Q1 128x128 grid (127^2 interior), N_t=256, p_t=1, random u0"),
+    "C3": dict(p_t=2, dim=2, space_level=7, time_level=12, t_final=1.0, random_u0=False,
+               desc="configs[2]: 2D heat, Q1 256x256 grid (255^2 interior), N_t=4096, p_t=2"),
+    "C4": dict(p_t=1, dim=3, space_level=5, time_level=10, t_final=1.0, random_u0=False,
+               desc="configs[3]: 3D heat, Q1 64^3 grid (63^3 interior), N_t=1024, p_t=1"),
+    "C5": dict(p_t=1, dim=2, space_level=8, time_level=11, t_final=1.0, random_u0=False,
+               desc="configs[4] G=1: 2D heat, Q1 512x512 grid (511^2 interior), N_t=2048, p_t=1"),
+}
+METRIC = "space-time DoF*V-cycles/s (full solve to 1e-8 residual reduction)"
+UNIT = "DoF*V-cycles/s"
+EPS = 1e-8
+SEED = 42
+L2_FLUSH_BYTES = 512 << 20
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(self.NAMES, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local, dist
+
+
+def allreduce_max(dist, local, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(dist, local, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(dist, local):
+    if dist is not None:
+        import torch
+        torch.cuda.synchronize(local)
+        dist.barrier()
+
+
+def oracle_inputs(cfg):
+    from oracle import oracle as O
+    h = O.Hierarchy(cfg["p_t"], cfg["dim"], cfg["space_level"], cfg["time_level"], cfg["t_final"])
+    return h, O.make_inputs(h, SEED, random_u0=cfg["random_u0"])
+
+
+def cpu_reference_cycles(cfg, cycles: int, warm: int = 0):
+    """Time `cycles` V(1,1) cycles of the oracle (+ stop-test residual and norm
+    each cycle, mg.cpp:150-160) on all host cores.  Returns (s_per_cycle, n0)."""
+    from oracle import oracle as O
+    h, f = oracle_inputs(cfg)
+    u = np.zeros_like(f)
+    n0 = f.size
+    times = []
+    for k in range(warm + cycles):
+        t0 = time.perf_counter()
+        u = h.mg_cycle(0, u, f, 1, 1, 1, 0.5)
+        r = h.residual(0, u, f)
+        h.norm(0, r)
+        dt = time.perf_counter() - t0
+        if k >= warm:
+            times.append(dt)
+    return times, n0
+
+
+def run_reference(args, cfgname):
+    world, rank, local, dist = dist_setup()
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[cfgname]
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    times, n0 = cpu_reference_cycles(cfg, args.steps, args.warmup)
+    per = sum(times) / len(times)
+    value = n0 / per
+    sample = (f"{args.steps} V(1,1) cycles (+ stop-test residual/norm) of {cfgname} from a zero guess, "
+              f"{args.warmup} untimed; one step = one cycle")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded splitmix64 uniform[-1,1])",
+        "config": {"workload": cfg["desc"], "dofs": n0, "cycle": "V(1,1) omega_t=0.5 exact blocks"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference (Eigen3) cannot be built here; CPU oracle = C++/OpenMP restatement "
+                "of the reference algorithm (oracle/)",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def traffic_from_profiles(kernel_tag: str):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get(kernel_tag)
+    except Exception:
+        return None
+
+
+def run_ours(args, cfgname):
+    world, rank, local, dist = dist_setup()
+    from paper_1411_0519_b200 import stmg
+    from paper_1411_0519_b200 import _capi as A
+    cfg = CONFIGS[cfgname]
+    h = stmg.Hierarchy(cfg["p_t"], cfg["dim"], cfg["space_level"], cfg["time_level"],
+                       cfg["t_final"], device=local)
+    n0 = h.size(0)
+    f = h.vector(0)
+    h.fill_uniform(f, SEED, 0)
+    if cfg["random_u0"]:
+        L0 = h.levels[0]
+        u0 = stmg.BlockVector(h, L0["n_x"], (L0["n_x"],))
+        h.fill_uniform(u0, SEED, 1)
+        h.fold_u0(f, u0)
+        del u0
+    u = h.vector(0)
+    ccfg = stmg.CycleConfig(nu1=1, nu2=1, gamma=1, omega_t=0.5)
+    import ctypes as C
+    flush = C.c_void_p()
+    A.check(A.lib().stmg_device_alloc(h._ctx, L2_FLUSH_BYTES, C.byref(flush)))
+
+    def one_step():
+        A.check(A.lib().stmg_memset_zero(h._ctx, u.ptr, n0 * 8))
+        A.check(A.lib().stmg_memset_zero(h._ctx, flush, L2_FLUSH_BYTES))  # evict L2
+        h.synchronize()
+        return h.solve(f, u, ccfg, EPS)
+
+    for _ in range(args.warmup):
+        one_step()
+    h.profile(True)
+    h.profile_reset()
+    launches0 = h.launch_count()
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier(dist, local)
+    h.synchronize()
+    t_wall0 = time.perf_counter()
+    dev_s, iters = [], []
+    for _ in range(args.steps):
+        rep = one_step()
+        if not rep.converged:
+            raise RuntimeError("solve did not converge")
+        dev_s.append(rep.device_time_seconds)
+        iters.append(rep.iterations)
+    h.synchronize()
+    barrier(dist, local)
+    t_wall = time.perf_counter() - t_wall0
+    clk = clocks.stop()
+    launches = h.launch_count() - launches0
+    prof = {k: h.profile_read(k) for k in (0, 1, 2)}
+    h.profile(False)
+
+    total_dev = allreduce_max(dist, local, sum(dev_s))
+    work = allreduce_sum(dist, local, float(n0 * sum(iters)))
+    value = work / total_dev
+    ms_per_step = 1e3 * total_dev / args.steps
+
+    # end to end through the C ABI with pinned host buffers
+    hf = C.c_void_p()
+    hu = C.c_void_p()
+    A.check(A.lib().stmg_host_alloc(h._ctx, n0 * 8, C.byref(hf)))
+    A.check(A.lib().stmg_host_alloc(h._ctx, n0 * 8, C.byref(hu)))
+    hf_np = np.ctypeslib.as_array((C.c_double * n0).from_address(hf.value))
+    hu_np = np.ctypeslib.as_array((C.c_double * n0).from_address(hu.value))
+    A.check(A.lib().stmg_download(h._ctx, hf.value, f.ptr, n0 * 8))
+    e2e_s, e2e_it = [], []
+    for k in range(args.warmup + args.steps):
+        hu_np[:] = 0.0
+        A.check(A.lib().stmg_memset_zero(h._ctx, flush, L2_FLUSH_BYTES))
+        h.synchronize()
+        barrier(dist, local)
+        rep = h.solve_host(hf_np, hu_np, ccfg, EPS)
+        if k >= args.warmup:
+            e2e_s.append(rep.wall_time_seconds)
+            e2e_it.append(rep.iterations)
+    e2e_total = allreduce_max(dist, local, sum(e2e_s))
+    e2e_work = allreduce_sum(dist, local, float(n0 * sum(e2e_it)))
+    A.lib().stmg_host_free(h._ctx, hf)
+    A.lib().stmg_host_free(h._ctx, hu)
+
+    peak, peak_kind = peaks()
+    ms0, n0l, b0 = prof[0]
+    ms1, n1l, b1 = prof[1]
+    dom = 0 if ms0 >= ms1 else 1
+    ms, nl, b = prof[dom]
+    avg_s = (ms / nl) * 1e-3 if nl else float("nan")
+    achieved = b / avg_s / 1e9 if nl else None
+    names = {0: "k_down (level 0: pre-smooth + residual + restrict)",
+             1: "k_up (level 0: prolong + correct + post-smooth + residual norm)"}
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak if achieved else None,
+            "traffic": traffic_from_profiles("k_down" if dom == 0 else "k_up"),
+            "kernel": names[dom], "peak_kind": peak_kind,
+            "algorithmic_bytes_per_launch": b, "avg_launch_ms": avg_s * 1e3,
+            "step_share": (ms0 + ms1) / (1e3 * sum(dev_s)) if dev_s else None,
+            "other_kernel": {"name": names[1 - dom],
+                             "achieved_gbs": (prof[1 - dom][2] / (prof[1 - dom][0] / prof[1 - dom][1] * 1e-3) / 1e9)
+                             if prof[1 - dom][1] else None},
+            "transform_pass_ms_per_solve": prof[2][0] / max(len(dev_s), 1)}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded splitmix64 uniform[-1,1], f and u0)",
+        "config": {"workload": cfg["desc"], "dofs": n0, "levels": len(h.levels),
+                   "cycle": "V(1,1), omega_t=0.5, exact DG block solves, mu-driven coarsening",
+                   "eps": EPS, "step": "one full solve to 1e-8 incl. sine-basis transforms",
+                   "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB memset); vector {n0 * 8 / 1e6:.0f} MB",
+                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "path": "spectral fused V-cycle (CUDA graph)"},
+        "iterations": iters[0], "time_to_1e-8_ms": ms_per_step,
+        "wall_ms_per_step_incl_flush": 1e3 * t_wall / args.steps,
+        "e2e": {"value": e2e_work / e2e_total, "unit": UNIT,
+                "h2d_bytes_per_step": 2 * n0 * 8, "d2h_bytes_per_step": n0 * 8,
+                "ms_per_step": 1e3 * e2e_total / args.steps},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        times, n0c = cpu_reference_cycles(cfg, args.cpu_cycles)
+        per = sum(times) / len(times)
+        line["cpu_baseline"] = {
+            "value": n0c / per, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{args.cpu_cycles} V(1,1) cycles (+ stop-test residual/norm) of {cfgname} "
+                      f"from a zero guess on the CPU oracle, OpenMP over time steps"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-cycles", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args, args.config)
+    return run_ours(args, args.config)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,180 @@
+/*
+ * stmg_b200.h -- C ABI of the B200-native space-time multigrid library.
+ *
+ * Drop-in boundary for the reference's hot path (arXiv 1411.0519 space-time
+ * multigrid, /root/reference/proj).  The reference has no FFI: its boundary is
+ * the C++ header API of the static library `stmg`.  Each entry point below
+ * names the reference function it replaces (file:line, relative to
+ * /root/reference/proj).  A C++ shim with the reference's own signatures is in
+ * include/stmg_b200.hpp.
+ *
+ * Conventions
+ *  - Every function returns an int status: STMG_OK (0), STMG_EINVAL (1, the
+ *    reference's std::invalid_argument), STMG_ERUNTIME (2, std::runtime_error,
+ *    CUDA or NCCL failures).  stmg_last_error() returns the message of the last
+ *    failure on the calling thread.
+ *  - Vectors are DEVICE pointers (double, FP64) in the reference BlockVector
+ *    layout (block_vector.hpp:12-29): flat index (n*n_loc + l)*n_x + r with
+ *    r = (iz*n1 + iy)*n1 + ix.  Only stmg_solve_host takes host pointers.
+ *  - All compute calls are stream-ordered on the context's stream; only
+ *    stmg_norm, stmg_solve*, stmg_download and stmg_synchronize synchronise.
+ *  - The context is not thread-safe (one driver thread, like the reference).
+ *  - There is no CPU fallback: without a CUDA device stmg_create fails.
+ */
+#ifndef STMG_B200_H
+#define STMG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STMG_OK 0
+#define STMG_EINVAL 1
+#define STMG_ERUNTIME 2
+
+/* Coarsening policy (mg.hpp:47, CoarseningPolicy). */
+#define STMG_POLICY_MU_DRIVEN 0
+#define STMG_POLICY_ALWAYS_SEMI 1
+#define STMG_POLICY_PREFER_FULL 2
+
+/* Coarsening mode of a level (mg.hpp:12, Coarsening). */
+#define STMG_COARSEN_NONE 0
+#define STMG_COARSEN_SEMI 1
+#define STMG_COARSEN_FULL 2
+
+/* Cycle execution path. */
+#define STMG_PATH_SPECTRAL 0 /* fused V-cycle on sine coefficients (default) */
+#define STMG_PATH_PHYSICAL 1 /* reference call structure on nodal values */
+
+typedef struct stmg_ctx stmg_ctx;
+
+/* HierarchyParams (mg.hpp:49-58) + build_two_grid's mode (mg.hpp:81). */
+typedef struct {
+  int p_t;          /* DG degree in time, 0..3 on the GPU path */
+  int dim;          /* 1, 2 or 3 */
+  int space_level;  /* finest space level L: n1 = 2^(L+1)-1 nodes per axis */
+  int time_level;   /* finest n_t = 2^time_level */
+  double t_final;   /* T; tau = T / n_t on the finest level */
+  double mu_star;   /* full-coarsening threshold; <= 0 -> lfa::critical_mu(p_t) */
+  int policy;       /* STMG_POLICY_* */
+  int two_grid;     /* 0: full ladder; STMG_COARSEN_SEMI/FULL: build_two_grid */
+  int device;       /* CUDA device ordinal */
+} stmg_hierarchy_params;
+
+/* CycleConfig + SmootherConfig (mg.hpp:66-71, smoother.hpp:15-24). */
+typedef struct {
+  int nu1;          /* pre-smoothing sweeps */
+  int nu2;          /* post-smoothing sweeps */
+  int gamma;        /* 1 = V-cycle */
+  double omega_t;   /* block-Jacobi damping */
+  int path;         /* STMG_PATH_* */
+} stmg_cycle_config;
+
+/* SolveReport (mg.hpp:83-89). */
+typedef struct {
+  int iterations;
+  int converged;
+  double wall_time_seconds;   /* host wall clock of the whole call */
+  double device_time_seconds; /* CUDA events around the solve on the ctx stream
+                                 (basis transforms included, host I/O excluded) */
+  double r0;
+  double r_final;
+  uint64_t seed;
+} stmg_solve_report;
+
+/* STLevel summary (mg.hpp:19-36). */
+typedef struct {
+  int64_t n_t, n_x, n_loc, n1;
+  int dim, space_level, coarsen_to_next;
+  double tau, h, mu;
+} stmg_level_info;
+
+const char* stmg_last_error(void);
+
+/* lfa::critical_mu (lfa.cpp:317-328); returns NaN on invalid p_t. */
+double stmg_critical_mu(int p_t);
+/* assemble_dg_block (dg_time.cpp:125-166): row-major (p_t+1)^2 blocks. */
+int stmg_dg_block(int p_t, double tau, double* K, double* M, double* N);
+/* build_time_transfer (transfer.cpp:50-73): row-major R1, R2. */
+int stmg_time_transfer(int p_t, double tau, double* R1, double* R2);
+
+/* build_hierarchy / build_two_grid (mg.cpp:10-94) + device setup. */
+int stmg_create(const stmg_hierarchy_params* params, stmg_ctx** out);
+int stmg_destroy(stmg_ctx* ctx);
+int stmg_num_levels(const stmg_ctx* ctx, int* out);
+int stmg_get_level_info(const stmg_ctx* ctx, int level, stmg_level_info* out);
+/* Number of doubles of a level vector (BlockVector::size). */
+int stmg_level_size(const stmg_ctx* ctx, int level, int64_t* out);
+
+/* Device memory plumbing (plain pointers and sizes). */
+int stmg_device_alloc(stmg_ctx* ctx, size_t bytes, void** dptr);
+int stmg_device_free(stmg_ctx* ctx, void* dptr);
+int stmg_upload(stmg_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes);
+int stmg_download(stmg_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes);
+int stmg_memset_zero(stmg_ctx* ctx, void* dst_dev, size_t bytes);
+/* Page-locked host buffers for the end-to-end path (cudaHostAlloc). */
+int stmg_host_alloc(stmg_ctx* ctx, size_t bytes, void** hptr);
+int stmg_host_free(stmg_ctx* ctx, void* hptr);
+int stmg_synchronize(stmg_ctx* ctx);
+/* Seeded counter-based uniform[-1,1) fill; identical to the
+ * host generator for the same (seed, stream, global offset). */
+int stmg_fill_uniform(stmg_ctx* ctx, double* dst_dev, int64_t n, uint64_t seed,
+                      uint64_t stream, int64_t offset);
+/* f(0,k,:) += psi_k(0) * M_h u0 on the finest level (u0: n_x nodal values). */
+int stmg_fold_u0(stmg_ctx* ctx, double* f_dev, const double* u0_dev);
+
+/* ---- operators: reference entry points (device pointers) ---------------- */
+/* apply (st_system.cpp:44-49): y = L u. */
+int stmg_apply(stmg_ctx* ctx, int level, const double* u, double* y);
+/* residual (st_system.cpp:57-67): r = f - L u. */
+int stmg_residual(stmg_ctx* ctx, int level, const double* u, const double* f,
+                  double* r);
+/* BlockVector::norm (st_system.cpp:8-16); synchronising. */
+int stmg_norm(stmg_ctx* ctx, int level, const double* v, double* out);
+/* BlockSolver::solve on every time step (st_system.cpp:110-116). */
+int stmg_block_solve(stmg_ctx* ctx, int level, const double* b, double* x);
+/* block_jacobi_step, exact blocks (smoother.cpp:96-106): nu sweeps of
+ * u <- u + omega_t A^-1 (f - L u). */
+int stmg_smooth(stmg_ctx* ctx, int level, double* u, const double* f,
+                double omega_t, int nu);
+/* restrict_semi / restrict_full (transfer.cpp:75-85, 138-149).  mode 0 uses
+ * the level's coarsen_to_next. */
+int stmg_restrict(stmg_ctx* ctx, int level, int mode, const double* fine,
+                  double* coarse);
+/* prolong_semi / prolong_full (transfer.cpp:87-96, 151-158). */
+int stmg_prolong(stmg_ctx* ctx, int level, int mode, const double* coarse,
+                 double* fine);
+/* forward_substitution_solve (st_system.cpp:118-130). */
+int stmg_forward_substitution(stmg_ctx* ctx, int level, const double* f,
+                              double* u);
+/* mg_cycle (mg.cpp:96-132): one gamma-cycle from `level` on u in place. */
+int stmg_mg_cycle(stmg_ctx* ctx, int level, double* u, const double* f,
+                  const stmg_cycle_config* cfg);
+/* solve (mg.cpp:134-166): cycles until ||r_k|| <= eps ||r_0|| or max_iter.
+ * history (optional, capacity history_cap) receives ||r_0||, ||r_1||, ... */
+int stmg_solve(stmg_ctx* ctx, const double* f, double* u,
+               const stmg_cycle_config* cfg, double eps, int max_iter,
+               double* history, int history_cap, stmg_solve_report* report);
+/* Same with HOST f and u (pinned or pageable): H2D, solve, D2H. */
+int stmg_solve_host(stmg_ctx* ctx, const double* f_host, double* u_host,
+                    const stmg_cycle_config* cfg, double eps, int max_iter,
+                    double* history, int history_cap, stmg_solve_report* report);
+
+/* ---- live per-kernel timing (CUDA events inside the cycle) --------------- */
+/* Kernel ids: 0 = fused pre-smooth+residual+restrict on the finest level,
+ *             1 = fused prolong+correct+post-smooth+residual-norm (finest),
+ *             2 = basis transform pass, 3 = physical residual. */
+int stmg_profile_enable(stmg_ctx* ctx, int on);
+int stmg_profile_read(stmg_ctx* ctx, int kernel_id, double* total_ms,
+                      int64_t* launches, double* bytes_per_launch);
+int stmg_profile_reset(stmg_ctx* ctx);
+/* Kernel launches issued by the library since creation (all kinds). */
+int stmg_launch_count(const stmg_ctx* ctx, int64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STMG_B200_H */

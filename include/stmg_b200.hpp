@@ -1,0 +1,317 @@
+// stmg_b200.hpp -- C++ shim that re-exposes the reference's stmg:: API
+// (/root/reference/proj/include/stmg/*.hpp) on top of the C ABI in
+// stmg_b200.h.  Header-only; link against libstmg_b200.so.
+//
+// Differences a caller of the reference sees:
+//  * vectors are device-resident (BlockVector owns a GPU allocation); use
+//    from_host()/to_host() to move data (the reference's Eigen storage has no
+//    equivalent here, so no Eigen dependency);
+//  * an STOperator is (hierarchy, level) instead of raw dg/space pointers;
+//  * errors map to the same exception types: std::invalid_argument for bad
+//    arguments, std::runtime_error for CUDA/runtime failures.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "stmg_b200.h"
+
+namespace stmg {
+
+inline void check(int rc) {
+  if (rc == STMG_OK) return;
+  if (rc == STMG_EINVAL) throw std::invalid_argument(stmg_last_error());
+  throw std::runtime_error(stmg_last_error());
+}
+
+enum class Coarsening { none = STMG_COARSEN_NONE, semi = STMG_COARSEN_SEMI, full = STMG_COARSEN_FULL };
+enum class CoarseningPolicy {
+  mu_driven = STMG_POLICY_MU_DRIVEN,
+  always_semi = STMG_POLICY_ALWAYS_SEMI,
+  prefer_full = STMG_POLICY_PREFER_FULL
+};
+enum class BlockSolverKind { exact, spatial_vcycle };
+
+// dg_time.hpp:19-26 (row-major blocks instead of Eigen matrices)
+struct DGTimeBlock {
+  int p_t = 0;
+  double tau = 1.0;
+  std::vector<double> K, M, N;
+  int n_loc() const { return p_t + 1; }
+};
+
+inline DGTimeBlock assemble_dg_block(int p_t, double tau) {
+  DGTimeBlock b;
+  b.p_t = p_t;
+  b.tau = tau;
+  const int n = p_t + 1 > 0 ? p_t + 1 : 1;
+  b.K.resize(n * n);
+  b.M.resize(n * n);
+  b.N.resize(n * n);
+  check(stmg_dg_block(p_t, tau, b.K.data(), b.M.data(), b.N.data()));
+  return b;
+}
+
+// transfer.hpp:17-20
+struct TimeTransfer {
+  std::vector<double> R1, R2;
+};
+
+inline TimeTransfer build_time_transfer(int p_t, double tau) {
+  TimeTransfer t;
+  const int n = p_t + 1 > 0 ? p_t + 1 : 1;
+  t.R1.resize(n * n);
+  t.R2.resize(n * n);
+  check(stmg_time_transfer(p_t, tau, t.R1.data(), t.R2.data()));
+  return t;
+}
+
+namespace lfa {
+inline double critical_mu(int p_t) {
+  const double v = stmg_critical_mu(p_t);
+  if (v != v) throw std::invalid_argument(stmg_last_error());
+  return v;
+}
+}  // namespace lfa
+
+// mg.hpp:49-58
+struct HierarchyParams {
+  int p_t = 0;
+  int dim = 1;
+  int space_level = 4;
+  int time_level = 4;
+  double t_final = 1.0;
+  double mu_star = 0.3;
+  CoarseningPolicy policy = CoarseningPolicy::mu_driven;
+  BlockSolverKind block_solver = BlockSolverKind::exact;
+  int device = 0;
+};
+
+// smoother.hpp:15-24
+struct SmootherConfig {
+  double omega_t = 0.5;
+  int nu = 1;
+  BlockSolverKind block_solver = BlockSolverKind::exact;
+};
+
+// mg.hpp:66-71
+struct CycleConfig {
+  int nu1 = 2;
+  int nu2 = 2;
+  int gamma = 1;
+  SmootherConfig smoother;
+  int path = STMG_PATH_SPECTRAL;
+};
+
+// mg.hpp:83-89
+struct SolveReport {
+  int iterations = 0;
+  std::vector<double> residual_history;
+  bool converged = false;
+  double wall_time_seconds = 0.0;
+  double device_time_seconds = 0.0;
+  std::uint64_t seed = 0;
+};
+
+class STHierarchy;
+
+// st_system.hpp:18-26: a level of a hierarchy.
+struct STOperator {
+  stmg_ctx* ctx = nullptr;
+  int level = 0;
+};
+
+struct STLevel {
+  stmg_level_info info{};
+  STOperator op_{};
+  STOperator op() const { return op_; }
+  Coarsening coarsen_to_next() const { return Coarsening(info.coarsen_to_next); }
+};
+
+class STHierarchy {
+ public:
+  STHierarchy() = default;
+  explicit STHierarchy(const stmg_hierarchy_params& p) {
+    stmg_ctx* c = nullptr;
+    check(stmg_create(&p, &c));
+    ctx_.reset(c, [](stmg_ctx* x) { stmg_destroy(x); });
+    int n = 0;
+    check(stmg_num_levels(c, &n));
+    levels.resize(n);
+    for (int i = 0; i < n; ++i) {
+      check(stmg_get_level_info(c, i, &levels[i].info));
+      levels[i].op_ = {c, i};
+    }
+  }
+  std::vector<STLevel> levels;  // [0] = finest
+  stmg_ctx* ctx() const { return ctx_.get(); }
+  const STLevel& finest() const { return levels.front(); }
+
+ private:
+  std::shared_ptr<stmg_ctx> ctx_;
+};
+
+inline stmg_hierarchy_params to_c(const HierarchyParams& p, int two_grid) {
+  if (p.block_solver != BlockSolverKind::exact)
+    throw std::invalid_argument("only exact block solves are available on the B200 path");
+  stmg_hierarchy_params c{};
+  c.p_t = p.p_t;
+  c.dim = p.dim;
+  c.space_level = p.space_level;
+  c.time_level = p.time_level;
+  c.t_final = p.t_final;
+  c.mu_star = p.mu_star;
+  c.policy = int(p.policy);
+  c.two_grid = two_grid;
+  c.device = p.device;
+  return c;
+}
+
+// mg.hpp:64 / mg.hpp:81
+inline STHierarchy build_hierarchy(const HierarchyParams& p) { return STHierarchy(to_c(p, 0)); }
+inline STHierarchy build_two_grid(const HierarchyParams& p, Coarsening mode) {
+  if (mode == Coarsening::none) throw std::invalid_argument("two-grid needs semi or full mode");
+  return STHierarchy(to_c(p, int(mode)));
+}
+
+// block_vector.hpp:12-57, device-resident.
+class BlockVector {
+ public:
+  BlockVector() = default;
+  BlockVector(stmg_ctx* ctx, std::int64_t n_t, std::int64_t n_x, std::int64_t n_loc)
+      : ctx_(ctx), n_t_(n_t), n_x_(n_x), n_loc_(n_loc) {
+    void* p = nullptr;
+    check(stmg_device_alloc(ctx, size_t(size()) * sizeof(double), &p));
+    check(stmg_memset_zero(ctx, p, size_t(size()) * sizeof(double)));
+    data_.reset(static_cast<double*>(p), [ctx](double* q) { stmg_device_free(ctx, q); });
+  }
+  static BlockVector for_level(const STOperator& op) {
+    stmg_level_info li{};
+    check(stmg_get_level_info(op.ctx, op.level, &li));
+    return BlockVector(op.ctx, li.n_t, li.n_x, li.n_loc);
+  }
+  std::int64_t n_t() const { return n_t_; }
+  std::int64_t n_x() const { return n_x_; }
+  std::int64_t n_loc() const { return n_loc_; }
+  std::int64_t size() const { return n_t_ * n_x_ * n_loc_; }
+  double* data() { return data_.get(); }
+  const double* data() const { return data_.get(); }
+  stmg_ctx* ctx() const { return ctx_; }
+  void from_host(const std::vector<double>& v) {
+    if (std::int64_t(v.size()) != size()) throw std::invalid_argument("space-time vector shape mismatch");
+    check(stmg_upload(ctx_, data(), v.data(), v.size() * sizeof(double)));
+    check(stmg_synchronize(ctx_));
+  }
+  std::vector<double> to_host() const {
+    std::vector<double> v(static_cast<size_t>(size()));
+    check(stmg_download(ctx_, v.data(), data(), v.size() * sizeof(double)));
+    return v;
+  }
+  void setZero() { check(stmg_memset_zero(ctx_, data(), size_t(size()) * sizeof(double))); }
+
+ private:
+  stmg_ctx* ctx_ = nullptr;
+  std::int64_t n_t_ = 0, n_x_ = 0, n_loc_ = 0;
+  std::shared_ptr<double> data_;
+};
+
+inline BlockVector make_vector(const STOperator& op) { return BlockVector::for_level(op); }
+
+// st_system.hpp:31-47
+inline void apply(const STOperator& op, const BlockVector& u, BlockVector& y) {
+  check(stmg_apply(op.ctx, op.level, u.data(), y.data()));
+}
+inline void residual(const STOperator& op, const BlockVector& u, const BlockVector& f, BlockVector& r) {
+  check(stmg_residual(op.ctx, op.level, u.data(), f.data(), r.data()));
+}
+inline double norm(const STOperator& op, const BlockVector& v) {
+  double out = 0.0;
+  check(stmg_norm(op.ctx, op.level, v.data(), &out));
+  return out;
+}
+// st_system.hpp:70-72
+inline BlockVector forward_substitution_solve(const STOperator& op, const BlockVector& f) {
+  BlockVector u = make_vector(op);
+  check(stmg_forward_substitution(op.ctx, op.level, f.data(), u.data()));
+  return u;
+}
+// smoother.hpp:68-70 (exact block solves)
+inline void block_jacobi_step(const STOperator& op, BlockVector& u, const BlockVector& f,
+                              const SmootherConfig& cfg) {
+  if (cfg.block_solver != BlockSolverKind::exact)
+    throw std::invalid_argument("only exact block solves are available on the B200 path");
+  check(stmg_smooth(op.ctx, op.level, u.data(), f.data(), cfg.omega_t, cfg.nu));
+}
+
+namespace detail {
+inline BlockVector coarse_like(const STOperator& op, int mode) {
+  stmg_level_info li{};
+  check(stmg_get_level_info(op.ctx, op.level, &li));
+  std::int64_t n1 = mode == STMG_COARSEN_SEMI ? li.n1 : (li.n1 - 1) / 2;
+  std::int64_t nx = 1;
+  for (int a = 0; a < li.dim; ++a) nx *= n1;
+  return BlockVector(op.ctx, li.n_t / 2, nx, li.n_loc);
+}
+}  // namespace detail
+
+// transfer.hpp:27-44
+inline BlockVector restrict_semi(const STOperator& op, const BlockVector& fine) {
+  BlockVector c = detail::coarse_like(op, STMG_COARSEN_SEMI);
+  check(stmg_restrict(op.ctx, op.level, STMG_COARSEN_SEMI, fine.data(), c.data()));
+  return c;
+}
+inline BlockVector restrict_full(const STOperator& op, const BlockVector& fine) {
+  BlockVector c = detail::coarse_like(op, STMG_COARSEN_FULL);
+  check(stmg_restrict(op.ctx, op.level, STMG_COARSEN_FULL, fine.data(), c.data()));
+  return c;
+}
+inline BlockVector prolong_semi(const STOperator& op, const BlockVector& coarse) {
+  BlockVector f = make_vector(op);
+  check(stmg_prolong(op.ctx, op.level, STMG_COARSEN_SEMI, coarse.data(), f.data()));
+  return f;
+}
+inline BlockVector prolong_full(const STOperator& op, const BlockVector& coarse) {
+  BlockVector f = make_vector(op);
+  check(stmg_prolong(op.ctx, op.level, STMG_COARSEN_FULL, coarse.data(), f.data()));
+  return f;
+}
+
+inline stmg_cycle_config to_c(const CycleConfig& c) {
+  if (c.smoother.block_solver != BlockSolverKind::exact)
+    throw std::invalid_argument("only exact block solves are available on the B200 path");
+  return stmg_cycle_config{c.nu1, c.nu2, c.gamma, c.smoother.omega_t, c.path};
+}
+
+// mg.hpp:75-76
+inline void mg_cycle(const STHierarchy& h, std::size_t level, BlockVector& u, const BlockVector& f,
+                     const CycleConfig& cfg) {
+  const stmg_cycle_config c = to_c(cfg);
+  check(stmg_mg_cycle(h.ctx(), int(level), u.data(), f.data(), &c));
+}
+
+// mg.hpp:92-94
+inline SolveReport solve(const STHierarchy& h, const BlockVector& f, BlockVector& u,
+                         const CycleConfig& cfg, double eps_mg, int max_iter = 250) {
+  const stmg_cycle_config c = to_c(cfg);
+  std::vector<double> hist(size_t(max_iter > 0 ? max_iter : 0) + 1);
+  stmg_solve_report r{};
+  check(stmg_solve(h.ctx(), f.data(), u.data(), &c, eps_mg, max_iter, hist.data(), int(hist.size()), &r));
+  SolveReport out;
+  out.iterations = r.iterations;
+  out.converged = r.converged != 0;
+  out.residual_history.assign(hist.begin(), hist.begin() + r.iterations + 1);
+  out.wall_time_seconds = r.wall_time_seconds;
+  out.device_time_seconds = r.device_time_seconds;
+  out.seed = r.seed;
+  return out;
+}
+
+// mg.hpp:98 (counter-based generator of SURVEY.md 8(d), uniform [-1, 1))
+inline void fill_random(BlockVector& v, std::uint64_t seed, std::uint64_t stream = 0) {
+  check(stmg_fill_uniform(v.ctx(), v.data(), v.size(), seed, stream, 0));
+}
+
+}  // namespace stmg

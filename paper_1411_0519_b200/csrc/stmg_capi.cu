@@ -1,0 +1,998 @@
+// stmg_capi.cu -- context, device memory, cycle driver and the C ABI
+// (include/stmg_b200.h).  Host code; kernels live in stmg_kernels.cu.
+//
+// Solve path (STMG_PATH_SPECTRAL, default): f and u are transformed once to
+// orthonormal sine coefficients (dim passes of the batched DST-I kernel), the
+// V-cycles run as fused per-mode kernels (k_down / k_up, stmg_kernels.cu)
+// captured in a CUDA graph, and u is transformed back at the end.  The
+// iteration is the reference's V-cycle (mg.cpp:96-166) in an orthogonal basis:
+// identical in exact arithmetic, same stop rule on ||r||_2 (the basis is
+// orthonormal, so the norm is the same).
+//
+// Physical path (STMG_PATH_PHYSICAL): the reference call structure on nodal
+// values, one kernel family per reference entry point; used for the operator
+// API and as a second GPU implementation in the parity tests.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/stmg_b200.h"
+#include "stmg_launch.hpp"
+#include "stmg_setup.hpp"
+
+namespace {
+
+using i64 = int64_t;
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what, int line) {
+  if (e != cudaSuccess)
+    throw CudaError(std::string("CUDA error in ") + what + " (stmg_capi.cu:" + std::to_string(line) +
+                    "): " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x, __LINE__)
+
+template <class F>
+int guard(F&& fn) {
+  try {
+    fn();
+    return STMG_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return STMG_EINVAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return STMG_ERUNTIME;
+  }
+}
+
+void require(bool ok, const char* msg) {
+  if (!ok) throw std::invalid_argument(msg);
+}
+
+// Device buffer with `halo` leading slabs (multi-GPU halo exchange lands there).
+struct DevBuf {
+  double* raw = nullptr;
+  double* base = nullptr;
+  i64 count = 0;
+  void alloc(i64 n, i64 halo_elems) {
+    release();
+    CK(cudaMalloc(&raw, size_t(n + halo_elems) * sizeof(double)));
+    CK(cudaMemset(raw, 0, size_t(n + halo_elems) * sizeof(double)));
+    base = raw + halo_elems;
+    count = n;
+  }
+  void release() {
+    if (raw) cudaFree(raw);
+    raw = base = nullptr;
+    count = 0;
+  }
+};
+
+struct Level {
+  stmg::LevelSpec spec;
+  stmg::LevelView view;
+  double* d_tables = nullptr;  // mval | kval | rfac
+  void* d_twiddle = nullptr;
+  // spectral V-cycle buffers (allocated on first solve)
+  DevBuf F, U[2];
+  // physical-path temporaries (allocated on first use)
+  DevBuf R, RC, EC, CORR;
+};
+
+struct ProfSlot {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;  // eager launches
+  size_t used = 0;
+  cudaEvent_t ga = nullptr, gb = nullptr;  // pair recorded inside the cycle graph
+  bool in_graph = false;
+  double total_ms = 0.0;
+  i64 launches = 0;
+  double bytes = 0.0;
+};
+
+}  // namespace
+
+struct stmg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<Level> levels;
+  int p_t = 0, dim = 1;
+  // scratch
+  DevBuf partials;   // norm partial sums
+  double* d_norm = nullptr;
+  double* d_hist = nullptr;
+  int hist_cap = 0;
+  double* h_norm = nullptr;  // pinned
+  DevBuf user_f, user_u;     // for stmg_solve_host
+  // graphs of one spectral V-cycle keyed by (cfg, starting buffer parity)
+  struct GraphKey {
+    int nu1, nu2, gamma, cur0;
+    double omega;
+    bool operator<(const GraphKey& o) const {
+      if (nu1 != o.nu1) return nu1 < o.nu1;
+      if (nu2 != o.nu2) return nu2 < o.nu2;
+      if (gamma != o.gamma) return gamma < o.gamma;
+      if (cur0 != o.cur0) return cur0 < o.cur0;
+      return omega < o.omega;
+    }
+  };
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    int cur0_after = 0;
+    i64 kernels = 0;
+  };
+  std::map<GraphKey, GraphEntry> graphs;
+  std::vector<int> cur;  // current U buffer per level
+  // profiling
+  bool profile = false;
+  ProfSlot prof[4];
+  i64 launches = 0;
+  bool capturing = false;
+  i64 captured_kernels = 0;
+  cudaEvent_t ev_solve[2] = {nullptr, nullptr};
+};
+
+namespace {
+
+// ---------------------------------------------------------------- helpers
+Level& lev(stmg_ctx* c, int level) {
+  require(c != nullptr, "null context");
+  require(level >= 0 && level < int(c->levels.size()), "level index out of range");
+  return c->levels[level];
+}
+
+void count(stmg_ctx* c, i64 k = 1) {
+  if (c->capturing) c->captured_kernels += k;
+  else c->launches += k;
+}
+
+void prof_begin(stmg_ctx* c, int id) {
+  if (!c->profile) return;
+  ProfSlot& s = c->prof[id];
+  if (c->capturing) {
+    CK(cudaEventRecordWithFlags(s.ga, c->stream, cudaEventRecordExternal));
+    return;
+  }
+  if (s.used == s.pool.size()) {
+    std::pair<cudaEvent_t, cudaEvent_t> e;
+    CK(cudaEventCreate(&e.first));
+    CK(cudaEventCreate(&e.second));
+    s.pool.push_back(e);
+  }
+  CK(cudaEventRecord(s.pool[s.used].first, c->stream));
+}
+
+void prof_end(stmg_ctx* c, int id, double bytes) {
+  if (!c->profile) return;
+  ProfSlot& s = c->prof[id];
+  s.bytes = bytes;
+  if (c->capturing) {
+    CK(cudaEventRecordWithFlags(s.gb, c->stream, cudaEventRecordExternal));
+    s.in_graph = true;
+    return;
+  }
+  CK(cudaEventRecord(s.pool[s.used].second, c->stream));
+  ++s.used;
+}
+
+// Collect eager event pairs (after a synchronisation).
+void prof_collect(stmg_ctx* c) {
+  if (!c->profile) return;
+  for (auto& s : c->prof) {
+    for (size_t i = 0; i < s.used; ++i) {
+      float ms = 0.f;
+      CK(cudaEventSynchronize(s.pool[i].second));
+      CK(cudaEventElapsedTime(&ms, s.pool[i].first, s.pool[i].second));
+      s.total_ms += ms;
+      s.launches += 1;
+    }
+    s.used = 0;
+  }
+}
+
+// Collect the pairs recorded by one replay of a cycle graph.
+void prof_collect_graph(stmg_ctx* c) {
+  if (!c->profile) return;
+  for (auto& s : c->prof) {
+    if (!s.in_graph) continue;
+    float ms = 0.f;
+    CK(cudaEventSynchronize(s.gb));
+    CK(cudaEventElapsedTime(&ms, s.ga, s.gb));
+    s.total_ms += ms;
+    s.launches += 1;
+  }
+}
+
+void build_level_tables(Level& L) {
+  const i64 n1 = L.spec.n1();
+  const double h = L.spec.h, N = double(n1 + 1);
+  const i64 G = (n1 + 1) / 2;
+  std::vector<double> tab(3 * n1);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (i64 q = 0; q < n1; ++q) {
+    const long double th = pi * (long double)(q + 1) / (long double)N;
+    const double c = double(std::cos(th));
+    const double s2 = double(std::sin(th / 2));
+    tab[q] = h / 3.0 * (2.0 + c);             // M1 eigenvalue (h/3)(2 + cos)
+    tab[n1 + q] = 4.0 / h * s2 * s2;          // K1 eigenvalue (2/h)(1 - cos)
+    const double c2 = double(std::cos(th / 2));
+    const double f = 2.0 * c2 * c2 / std::sqrt(2.0);  // (1 + cos)/sqrt(2)
+    tab[2 * n1 + q] = q < G - 1 ? f : (q == G - 1 ? 0.0 : -f);
+  }
+  CK(cudaMalloc(&L.d_tables, tab.size() * sizeof(double)));
+  CK(cudaMemcpy(L.d_tables, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+  // twiddles exp(-2 pi i k / (2N)), k < N
+  std::vector<double> tw(2 * (n1 + 1));
+  for (i64 k = 0; k <= n1; ++k) {
+    const long double a = -pi * (long double)k / (long double)N;
+    tw[2 * k] = double(std::cos(a));
+    tw[2 * k + 1] = double(std::sin(a));
+  }
+  CK(cudaMalloc(&L.d_twiddle, tw.size() * sizeof(double)));
+  CK(cudaMemcpy(L.d_twiddle, tw.data(), tw.size() * sizeof(double), cudaMemcpyHostToDevice));
+
+  stmg::LevelView& v = L.view;
+  v.n_t = L.spec.n_t;
+  v.first_global = true;
+  v.sp.dim = L.spec.dim;
+  v.sp.n1 = n1;
+  v.sp.nx = L.spec.nx();
+  v.sp.h = h;
+  v.sp.mval = L.d_tables;
+  v.sp.kval = L.d_tables + n1;
+  v.sp.rfac = L.d_tables + 2 * n1;
+  const int nl = L.spec.p_t + 1;
+  v.tc.nl = nl;
+  const stmg::DGBlock dg = stmg::dg_block(L.spec.p_t, L.spec.tau);
+  std::vector<double> R1, R2;
+  stmg::time_transfer(L.spec.p_t, L.spec.tau, R1, R2);
+  for (int k = 0; k < nl; ++k) {
+    for (int l = 0; l < nl; ++l) {
+      const int i = k * stmg::kMaxNL + l;
+      v.tc.K[i] = dg.K[k * nl + l];
+      v.tc.M[i] = dg.M[k * nl + l];
+      v.tc.N[i] = dg.N[k * nl + l];
+      v.tc.R1[i] = R1[k * nl + l];
+      v.tc.R2[i] = R2[k * nl + l];
+    }
+    v.tc.psi0[k] = (k % 2 == 0) ? 1.0 : -1.0;
+  }
+}
+
+void ensure(DevBuf& b, i64 n, i64 halo = 0) {
+  if (b.count != n) b.alloc(n, halo);
+}
+
+// ----------------------------------------------------- physical operators
+void dst_all(stmg_ctx* c, Level& L, const double* in, double* out, bool accumulate = false,
+             double alpha = 1.0) {
+  const int dim = L.spec.dim;
+  prof_begin(c, 2);
+  for (int a = 0; a < dim; ++a) {
+    const bool last = a + 1 == dim;
+    CK(stmg::launch_dst_axis(L.view, a, a == 0 ? in : out, out, last && accumulate, alpha,
+                             L.d_twiddle, c->stream));
+    count(c);
+  }
+  prof_end(c, 2, 16.0 * double(L.view.size()) * dim);
+}
+
+// Exact block solve on every step: x = A^-1 b (x may equal b).  When
+// accumulate, u += alpha * A^-1 b instead (x is scratch).
+void block_solve(stmg_ctx* c, Level& L, const double* b, double* x, double* acc_into = nullptr,
+                 double alpha = 1.0) {
+  const int dim = L.spec.dim;
+  CK(stmg::launch_dst_axis(L.view, 0, b, x, false, 1.0, L.d_twiddle, c->stream));
+  count(c);
+  for (int a = 1; a < dim; ++a) {
+    CK(stmg::launch_dst_axis(L.view, a, x, x, false, 1.0, L.d_twiddle, c->stream));
+    count(c);
+  }
+  CK(stmg::launch_modal_solve(L.view, x, c->stream));
+  count(c);
+  for (int a = 0; a < dim; ++a) {
+    const bool last = a + 1 == dim;
+    if (last && acc_into) {
+      CK(stmg::launch_dst_axis(L.view, a, x, acc_into, true, alpha, L.d_twiddle, c->stream));
+    } else {
+      CK(stmg::launch_dst_axis(L.view, a, x, x, false, 1.0, L.d_twiddle, c->stream));
+    }
+    count(c);
+  }
+}
+
+void residual(stmg_ctx* c, Level& L, const double* u, const double* f, double* r) {
+  prof_begin(c, 3);
+  CK(stmg::launch_apply(L.view, u, f, r, true, c->stream));
+  prof_end(c, 3, 24.0 * double(L.view.size()));
+  count(c);
+}
+
+void smooth_phys(stmg_ctx* c, int level, double* u, const double* f, double omega, int nu) {
+  Level& L = c->levels[level];
+  ensure(L.R, L.view.size());
+  for (int s = 0; s < nu; ++s) {
+    residual(c, L, u, f, L.R.base);
+    block_solve(c, L, L.R.base, L.R.base, u, omega);
+  }
+}
+
+i64 coarse_n1(const Level& L, int mode) { return mode == 2 ? (L.spec.n1() - 1) / 2 : L.spec.n1(); }
+
+int resolve_mode(const Level& L, int mode) {
+  if (mode == 0) mode = L.spec.coarsen;
+  require(mode == 1 || mode == 2, "level has no coarser level");
+  require(L.spec.n_t % 2 == 0, "restrict_semi requires an even step count");
+  if (mode == 2) require(L.spec.space_level > 0, "cannot coarsen the level-0 space grid");
+  return mode;
+}
+
+void fwdsub_phys(stmg_ctx* c, Level& L, const double* f, double* u) {
+  ensure(L.R, L.view.size());
+  dst_all(c, L, f, L.R.base);
+  CK(stmg::launch_modal_fwdsub(L.view, L.R.base, u, c->stream));
+  count(c);
+  dst_all(c, L, u, u);
+}
+
+void phys_cycle(stmg_ctx* c, int level, double* u, const double* f, const stmg_cycle_config& cfg) {
+  Level& L = c->levels[level];
+  if (level + 1 == int(c->levels.size())) {
+    fwdsub_phys(c, L, f, u);
+    return;
+  }
+  smooth_phys(c, level, u, f, cfg.omega_t, cfg.nu1);
+  ensure(L.R, L.view.size());
+  residual(c, L, u, f, L.R.base);
+  Level& C = c->levels[level + 1];
+  ensure(C.RC, C.view.size());
+  ensure(C.EC, C.view.size());
+  ensure(L.CORR, L.view.size());
+  const int mode = L.spec.coarsen;
+  CK(stmg::launch_restrict(L.view, mode, C.spec.n1(), L.R.base, C.RC.base, c->stream));
+  count(c);
+  CK(cudaMemsetAsync(C.EC.base, 0, size_t(C.view.size()) * sizeof(double), c->stream));
+  for (int g = 0; g < cfg.gamma; ++g) phys_cycle(c, level + 1, C.EC.base, C.RC.base, cfg);
+  CK(stmg::launch_prolong(L.view, mode, C.spec.n1(), C.EC.base, L.CORR.base, c->stream));
+  count(c);
+  CK(stmg::launch_axpy(u, L.CORR.base, 1.0, L.view.size(), c->stream));
+  count(c);
+  smooth_phys(c, level, u, f, cfg.omega_t, cfg.nu2);
+}
+
+double norm_phys(stmg_ctx* c, Level& L, const double* v) {
+  ensure(c->partials, std::max<i64>(L.view.n_t, 1));
+  CK(stmg::launch_step_sumsq(L.view, v, c->partials.base, c->stream));
+  CK(stmg::launch_norm_final(c->partials.base, L.view.n_t, c->d_norm, nullptr, 0, c->stream));
+  count(c, 2);
+  CK(cudaMemcpyAsync(c->h_norm, c->d_norm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return *c->h_norm;
+}
+
+// --------------------------------------------------------- spectral cycle
+void ensure_spectral(stmg_ctx* c, int from_level) {
+  for (int l = from_level; l < int(c->levels.size()); ++l) {
+    Level& L = c->levels[l];
+    const i64 n = L.view.size(), halo = 2 * L.view.slab();
+    ensure(L.F, n, halo);
+    ensure(L.U[0], n, halo);
+    ensure(L.U[1], n, halo);
+  }
+  if (int(c->cur.size()) != int(c->levels.size())) c->cur.assign(c->levels.size(), 0);
+  // partial sums: largest (blocks x chunks) grid of the residual-norm kernels
+  i64 need = 16;
+  for (int l = from_level; l < int(c->levels.size()); ++l) {
+    const Level& L = c->levels[l];
+    const i64 G = (L.spec.n1() + 1) / 2;
+    i64 lanes = 1;
+    for (int a = 0; a < L.spec.dim; ++a) lanes *= 2 * G;
+    const i64 bx = (std::max(lanes, L.spec.nx()) + 127) / 128;
+    const int ch = std::min(stmg::pick_chunk(L.view, true), stmg::pick_chunk(L.view, false));
+    need = std::max<i64>(need, bx * ((L.view.n_t + ch - 1) / ch));
+  }
+  ensure(c->partials, need);
+}
+
+stmg::ModalArgs modal_args(const Level& L, const Level* C, double omega, bool grouped) {
+  stmg::ModalArgs a;
+  a.omega = omega;
+  a.chunk = stmg::pick_chunk(L.view, grouped);
+  a.mode = L.spec.coarsen ? L.spec.coarsen : 1;
+  a.n1c = C ? C->spec.n1() : L.spec.n1();
+  return a;
+}
+
+// Enqueue one gamma-cycle from `level` on the spectral buffers.  zero_guess:
+// the level's iterate is 0 (coarse levels).  want_resid: compute the residual
+// norm partials of the finest result (returns their count via *np).
+void spectral_cycle(stmg_ctx* c, int level, bool zero_guess, const stmg_cycle_config& cfg,
+                    bool want_resid, i64* np) {
+  Level& L = c->levels[level];
+  int& cur = c->cur[level];
+  if (zero_guess) cur = 0;
+  const bool last = level + 1 == int(c->levels.size());
+  if (last) {
+    CK(stmg::launch_modal_fwdsub(L.view, L.F.base, L.U[cur].base, c->stream));
+    count(c);
+    if (want_resid) {
+      stmg::ModalArgs a = modal_args(L, nullptr, cfg.omega_t, false);
+      CK(stmg::launch_resnorm(L.view, a, L.U[cur].base, L.F.base, c->partials.base, c->stream));
+      count(c);
+      *np = a.n_partials;
+    }
+    return;
+  }
+  Level& C = c->levels[level + 1];
+  const int nu1 = std::max(cfg.nu1, 0), nu2 = std::max(cfg.nu2, 0);
+  // pre-smoothing: nu1-1 plain sweeps, the last fused with residual+restriction
+  for (int s = 0; s + 1 < nu1; ++s) {
+    stmg::ModalArgs a = modal_args(L, &C, cfg.omega_t, false);
+    CK(stmg::launch_smooth(L.view, a, zero_guess, L.F.base, L.U[cur].base, L.U[1 - cur].base,
+                           c->stream));
+    count(c);
+    cur ^= 1;
+    zero_guess = false;
+  }
+  {
+    stmg::ModalArgs a = modal_args(L, &C, nu1 > 0 ? cfg.omega_t : 0.0, true);
+    if (level == 0) prof_begin(c, 0);
+    CK(stmg::launch_down(L.view, a, zero_guess, L.F.base, L.U[cur].base, L.U[1 - cur].base,
+                         C.F.base, c->stream));
+    if (level == 0)
+      prof_end(c, 0, 8.0 * double((zero_guess ? 2 : 3) * L.view.size() + C.view.size()));
+    count(c);
+    cur ^= 1;
+  }
+  for (int g = 0; g < std::max(cfg.gamma, 1); ++g)
+    spectral_cycle(c, level + 1, g == 0, cfg, false, nullptr);
+  // prolong + correct + first post-sweep (+ residual norm on the finest level)
+  const bool fuse_resid = want_resid && nu2 <= 1;
+  {
+    stmg::ModalArgs a = modal_args(L, &C, nu2 > 0 ? cfg.omega_t : 0.0, true);
+    if (level == 0) prof_begin(c, 1);
+    CK(stmg::launch_up(L.view, a, C.U[c->cur[level + 1]].base, L.U[cur].base, L.F.base,
+                       L.U[1 - cur].base, fuse_resid ? c->partials.base : nullptr, c->stream));
+    if (level == 0) prof_end(c, 1, 8.0 * double(3 * L.view.size() + C.view.size()));
+    count(c);
+    if (fuse_resid) *np = a.n_partials;
+    cur ^= 1;
+  }
+  for (int s = 1; s < nu2; ++s) {
+    stmg::ModalArgs a = modal_args(L, &C, cfg.omega_t, false);
+    CK(stmg::launch_smooth(L.view, a, false, L.F.base, L.U[cur].base, L.U[1 - cur].base,
+                           c->stream));
+    count(c);
+    cur ^= 1;
+  }
+  if (want_resid && !fuse_resid) {
+    stmg::ModalArgs a = modal_args(L, &C, cfg.omega_t, false);
+    CK(stmg::launch_resnorm(L.view, a, L.U[cur].base, L.F.base, c->partials.base, c->stream));
+    count(c);
+    *np = a.n_partials;
+  }
+}
+
+void check_cfg(const stmg_cycle_config* cfg) {
+  require(cfg != nullptr, "null cycle config");
+  require(cfg->nu1 >= 0 && cfg->nu2 >= 0, "smoothing step counts must be >= 0");
+  require(cfg->gamma >= 1, "gamma must be >= 1");
+  require(cfg->path == STMG_PATH_SPECTRAL || cfg->path == STMG_PATH_PHYSICAL, "unknown cycle path");
+}
+
+void ensure_hist(stmg_ctx* c, int n) {
+  if (c->hist_cap >= n) return;
+  if (c->d_hist) cudaFree(c->d_hist);
+  CK(cudaMalloc(&c->d_hist, size_t(n) * sizeof(double)));
+  c->hist_cap = n;
+}
+
+// Residual norm of the spectral iterate at level 0 (synchronising).
+double spectral_resnorm(stmg_ctx* c, int level) {
+  Level& L = c->levels[level];
+  stmg::ModalArgs a = modal_args(L, nullptr, 0.5, false);
+  CK(stmg::launch_resnorm(L.view, a, L.U[c->cur[level]].base, L.F.base, c->partials.base,
+                          c->stream));
+  CK(stmg::launch_norm_final(c->partials.base, a.n_partials, c->d_norm, nullptr, 0, c->stream));
+  count(c, 2);
+  CK(cudaMemcpyAsync(c->h_norm, c->d_norm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return *c->h_norm;
+}
+
+// One full V-cycle from level 0 + residual norm into d_norm/h_norm, as a
+// captured graph (replayed every iteration).
+stmg_ctx::GraphEntry& cycle_graph(stmg_ctx* c, const stmg_cycle_config& cfg) {
+  stmg_ctx::GraphKey key{cfg.nu1, cfg.nu2, cfg.gamma, c->cur[0], cfg.omega_t};
+  auto it = c->graphs.find(key);
+  if (it != c->graphs.end()) return it->second;
+  const int cur0 = c->cur[0];
+  cudaGraph_t graph;
+  c->capturing = true;
+  c->captured_kernels = 0;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    i64 np = 0;
+    spectral_cycle(c, 0, false, cfg, true, &np);
+    CK(stmg::launch_norm_final(c->partials.base, np, c->d_norm, nullptr, 0, c->stream));
+    count(c);
+    CK(cudaMemcpyAsync(c->h_norm, c->d_norm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  } catch (...) {
+    cudaStreamEndCapture(c->stream, &graph);
+    c->capturing = false;
+    throw;
+  }
+  CK(cudaStreamEndCapture(c->stream, &graph));
+  c->capturing = false;
+  stmg_ctx::GraphEntry e;
+  CK(cudaGraphInstantiate(&e.exec, graph, 0));
+  CK(cudaGraphDestroy(graph));
+  e.cur0_after = c->cur[0];
+  e.kernels = c->captured_kernels;
+  c->cur[0] = cur0;
+  return c->graphs[key] = e;
+}
+
+void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config& cfg, double eps,
+                int max_iter, double* history, int history_cap, stmg_solve_report* rep) {
+  require(eps > 0.0, "eps_mg must be positive");
+  require(f != nullptr && u != nullptr, "null vector");
+  require(max_iter >= 0, "max_iter must be >= 0");
+  Level& L0 = c->levels[0];
+  stmg_solve_report r{};
+  int nh = 0;
+  auto push = [&](double v) {
+    if (history && nh < history_cap) history[nh] = v;
+    ++nh;
+  };
+  CK(cudaStreamSynchronize(c->stream));
+  const auto t0 = std::chrono::steady_clock::now();
+  CK(cudaEventRecord(c->ev_solve[0], c->stream));
+  if (cfg.path == STMG_PATH_PHYSICAL) {
+    ensure(L0.R, L0.view.size());
+    residual(c, L0, u, f, L0.R.base);
+    const double r0 = norm_phys(c, L0, L0.R.base);
+    r.r0 = r.r_final = r0;
+    push(r0);
+    if (r0 == 0.0) r.converged = 1;
+    for (int k = 0; k < max_iter && !r.converged; ++k) {
+      phys_cycle(c, 0, u, f, cfg);
+      residual(c, L0, u, f, L0.R.base);
+      const double rk = norm_phys(c, L0, L0.R.base);
+      push(rk);
+      r.r_final = rk;
+      ++r.iterations;
+      if (rk <= eps * r0) r.converged = 1;
+    }
+  } else {
+    ensure_spectral(c, 0);
+    c->cur[0] = 0;
+    dst_all(c, L0, f, L0.F.base);
+    dst_all(c, L0, u, L0.U[0].base);
+    const double r0 = spectral_resnorm(c, 0);
+    r.r0 = r.r_final = r0;
+    push(r0);
+    if (r0 == 0.0) r.converged = 1;
+    for (int k = 0; k < max_iter && !r.converged; ++k) {
+      stmg_ctx::GraphEntry& g = cycle_graph(c, cfg);
+      CK(cudaGraphLaunch(g.exec, c->stream));
+      c->launches += g.kernels;
+      CK(cudaStreamSynchronize(c->stream));
+      prof_collect_graph(c);
+      c->cur[0] = g.cur0_after;
+      const double rk = *c->h_norm;
+      push(rk);
+      r.r_final = rk;
+      ++r.iterations;
+      if (rk <= eps * r0) r.converged = 1;
+    }
+    dst_all(c, L0, L0.U[c->cur[0]].base, u);
+  }
+  CK(cudaEventRecord(c->ev_solve[1], c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  prof_collect(c);
+  {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev_solve[0], c->ev_solve[1]));
+    r.device_time_seconds = 1e-3 * double(ms);
+  }
+  r.wall_time_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (rep) *rep = r;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+const char* stmg_last_error(void) { return g_err.c_str(); }
+
+double stmg_critical_mu(int p_t) {
+  double v = NAN;
+  guard([&] { v = stmg::critical_mu(p_t); });
+  return v;
+}
+
+int stmg_dg_block(int p_t, double tau, double* K, double* M, double* N) {
+  return guard([&] {
+    require(K && M && N, "null output");
+    const stmg::DGBlock b = stmg::dg_block(p_t, tau);
+    std::memcpy(K, b.K.data(), b.K.size() * sizeof(double));
+    std::memcpy(M, b.M.data(), b.M.size() * sizeof(double));
+    std::memcpy(N, b.N.data(), b.N.size() * sizeof(double));
+  });
+}
+
+int stmg_time_transfer(int p_t, double tau, double* R1, double* R2) {
+  return guard([&] {
+    require(R1 && R2, "null output");
+    std::vector<double> a, b;
+    stmg::time_transfer(p_t, tau, a, b);
+    std::memcpy(R1, a.data(), a.size() * sizeof(double));
+    std::memcpy(R2, b.data(), b.size() * sizeof(double));
+  });
+}
+
+int stmg_create(const stmg_hierarchy_params* p, stmg_ctx** out) {
+  return guard([&] {
+    require(p != nullptr && out != nullptr, "null argument");
+    *out = nullptr;
+    auto specs = stmg::build_ladder(p->p_t, p->dim, p->space_level, p->time_level, p->t_final,
+                                    p->mu_star, p->policy, p->two_grid);
+    if (p->p_t + 1 > stmg::kMaxNL)
+      throw std::invalid_argument("p_t > 3 is not supported on the B200 path");
+    int ndev = 0;
+    const cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+      throw std::runtime_error("no CUDA device available (the B200 library has no CPU fallback)");
+    require(p->device >= 0 && p->device < ndev, "device ordinal out of range");
+    auto c = std::make_unique<stmg_ctx>();
+    c->device = p->device;
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->p_t = p->p_t;
+    c->dim = p->dim;
+    c->levels.resize(specs.size());
+    for (size_t i = 0; i < specs.size(); ++i) {
+      c->levels[i].spec = specs[i];
+      build_level_tables(c->levels[i]);
+    }
+    CK(cudaMalloc(&c->d_norm, sizeof(double)));
+    CK(cudaMallocHost(&c->h_norm, sizeof(double)));
+    CK(cudaEventCreate(&c->ev_solve[0]));
+    CK(cudaEventCreate(&c->ev_solve[1]));
+    for (auto& s : c->prof) {
+      CK(cudaEventCreate(&s.ga));
+      CK(cudaEventCreate(&s.gb));
+    }
+    c->cur.assign(c->levels.size(), 0);
+    *out = c.release();
+  });
+}
+
+int stmg_destroy(stmg_ctx* c) {
+  return guard([&] {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
+    for (auto& L : c->levels) {
+      cudaFree(L.d_tables);
+      cudaFree(L.d_twiddle);
+      for (DevBuf* b : {&L.F, &L.U[0], &L.U[1], &L.R, &L.RC, &L.EC, &L.CORR}) b->release();
+    }
+    c->partials.release();
+    c->user_f.release();
+    c->user_u.release();
+    for (auto& s : c->prof) {
+      for (auto& e : s.pool) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+      }
+      if (s.ga) cudaEventDestroy(s.ga);
+      if (s.gb) cudaEventDestroy(s.gb);
+    }
+    cudaEventDestroy(c->ev_solve[0]);
+    cudaEventDestroy(c->ev_solve[1]);
+    cudaFree(c->d_norm);
+    cudaFree(c->d_hist);
+    cudaFreeHost(c->h_norm);
+    cudaStreamDestroy(c->stream);
+    delete c;
+  });
+}
+
+int stmg_num_levels(const stmg_ctx* c, int* out) {
+  return guard([&] {
+    require(c && out, "null argument");
+    *out = int(c->levels.size());
+  });
+}
+
+int stmg_get_level_info(const stmg_ctx* cc, int level, stmg_level_info* o) {
+  return guard([&] {
+    stmg_ctx* c = const_cast<stmg_ctx*>(cc);
+    require(o != nullptr, "null output");
+    const Level& L = lev(c, level);
+    o->n_t = L.spec.n_t;
+    o->n_x = L.spec.nx();
+    o->n_loc = L.spec.p_t + 1;
+    o->n1 = L.spec.n1();
+    o->dim = L.spec.dim;
+    o->space_level = L.spec.space_level;
+    o->coarsen_to_next = L.spec.coarsen;
+    o->tau = L.spec.tau;
+    o->h = L.spec.h;
+    o->mu = L.spec.mu;
+  });
+}
+
+int stmg_level_size(const stmg_ctx* cc, int level, int64_t* out) {
+  return guard([&] {
+    require(out != nullptr, "null output");
+    *out = lev(const_cast<stmg_ctx*>(cc), level).spec.size();
+  });
+}
+
+int stmg_device_alloc(stmg_ctx* c, size_t bytes, void** dptr) {
+  return guard([&] {
+    require(c && dptr, "null argument");
+    CK(cudaSetDevice(c->device));
+    CK(cudaMalloc(dptr, bytes ? bytes : 8));
+  });
+}
+
+int stmg_device_free(stmg_ctx* c, void* dptr) {
+  return guard([&] {
+    require(c != nullptr, "null context");
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaFree(dptr));
+  });
+}
+
+int stmg_upload(stmg_ctx* c, void* dst, const void* src, size_t bytes) {
+  return guard([&] {
+    require(c && (bytes == 0 || (dst && src)), "null argument");
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+  });
+}
+
+int stmg_download(stmg_ctx* c, void* dst, const void* src, size_t bytes) {
+  return guard([&] {
+    require(c && (bytes == 0 || (dst && src)), "null argument");
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int stmg_memset_zero(stmg_ctx* c, void* dst, size_t bytes) {
+  return guard([&] {
+    require(c != nullptr, "null context");
+    CK(cudaMemsetAsync(dst, 0, bytes, c->stream));
+  });
+}
+
+int stmg_host_alloc(stmg_ctx* c, size_t bytes, void** hptr) {
+  return guard([&] {
+    require(c && hptr, "null argument");
+    CK(cudaSetDevice(c->device));
+    CK(cudaHostAlloc(hptr, bytes ? bytes : 8, cudaHostAllocDefault));
+  });
+}
+
+int stmg_host_free(stmg_ctx* c, void* hptr) {
+  return guard([&] {
+    require(c != nullptr, "null context");
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaFreeHost(hptr));
+  });
+}
+
+int stmg_synchronize(stmg_ctx* c) {
+  return guard([&] {
+    require(c != nullptr, "null context");
+    CK(cudaStreamSynchronize(c->stream));
+    prof_collect(c);
+  });
+}
+
+int stmg_fill_uniform(stmg_ctx* c, double* dst, int64_t n, uint64_t seed, uint64_t stream,
+                      int64_t offset) {
+  return guard([&] {
+    require(c && (n == 0 || dst), "null argument");
+    CK(stmg::launch_fill_uniform(dst, n, seed, stream, offset, c->stream));
+    count(c);
+  });
+}
+
+int stmg_fold_u0(stmg_ctx* c, double* f, const double* u0) {
+  return guard([&] {
+    require(f && u0, "null vector");
+    Level& L = lev(c, 0);
+    CK(stmg::launch_fold_u0(L.view, f, u0, c->stream));
+    count(c);
+  });
+}
+
+int stmg_apply(stmg_ctx* c, int level, const double* u, double* y) {
+  return guard([&] {
+    Level& L = lev(c, level);
+    require(u && y, "null vector");
+    CK(stmg::launch_apply(L.view, u, nullptr, y, false, c->stream));
+    count(c);
+  });
+}
+
+int stmg_residual(stmg_ctx* c, int level, const double* u, const double* f, double* r) {
+  return guard([&] {
+    Level& L = lev(c, level);
+    require(u && f && r, "null vector");
+    residual(c, L, u, f, r);
+  });
+}
+
+int stmg_norm(stmg_ctx* c, int level, const double* v, double* out) {
+  return guard([&] {
+    Level& L = lev(c, level);
+    require(v && out, "null argument");
+    *out = norm_phys(c, L, v);
+  });
+}
+
+int stmg_block_solve(stmg_ctx* c, int level, const double* b, double* x) {
+  return guard([&] {
+    Level& L = lev(c, level);
+    require(b && x, "null vector");
+    block_solve(c, L, b, x);
+  });
+}
+
+int stmg_smooth(stmg_ctx* c, int level, double* u, const double* f, double omega_t, int nu) {
+  return guard([&] {
+    lev(c, level);
+    require(u && f, "null vector");
+    require(nu >= 0, "nu must be >= 0");
+    smooth_phys(c, level, u, f, omega_t, nu);
+  });
+}
+
+int stmg_restrict(stmg_ctx* c, int level, int mode, const double* fine, double* coarse) {
+  return guard([&] {
+    Level& L = lev(c, level);
+    require(fine && coarse, "null vector");
+    mode = resolve_mode(L, mode);
+    CK(stmg::launch_restrict(L.view, mode, coarse_n1(L, mode), fine, coarse, c->stream));
+    count(c);
+  });
+}
+
+int stmg_prolong(stmg_ctx* c, int level, int mode, const double* coarse, double* fine) {
+  return guard([&] {
+    Level& L = lev(c, level);
+    require(fine && coarse, "null vector");
+    mode = resolve_mode(L, mode);
+    CK(stmg::launch_prolong(L.view, mode, coarse_n1(L, mode), coarse, fine, c->stream));
+    count(c);
+  });
+}
+
+int stmg_forward_substitution(stmg_ctx* c, int level, const double* f, double* u) {
+  return guard([&] {
+    Level& L = lev(c, level);
+    require(f && u, "null vector");
+    fwdsub_phys(c, L, f, u);
+  });
+}
+
+int stmg_mg_cycle(stmg_ctx* c, int level, double* u, const double* f,
+                  const stmg_cycle_config* cfg) {
+  return guard([&] {
+    Level& L = lev(c, level);
+    check_cfg(cfg);
+    require(u && f, "null vector");
+    if (cfg->path == STMG_PATH_PHYSICAL) {
+      phys_cycle(c, level, u, f, *cfg);
+      return;
+    }
+    ensure_spectral(c, level);
+    c->cur[level] = 0;
+    dst_all(c, L, f, L.F.base);
+    dst_all(c, L, u, L.U[0].base);
+    spectral_cycle(c, level, false, *cfg, false, nullptr);
+    dst_all(c, L, L.U[c->cur[level]].base, u);
+  });
+}
+
+int stmg_solve(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config* cfg, double eps,
+               int max_iter, double* history, int history_cap, stmg_solve_report* report) {
+  return guard([&] {
+    require(c != nullptr, "null context");
+    check_cfg(cfg);
+    solve_impl(c, f, u, *cfg, eps, max_iter, history, history_cap, report);
+  });
+}
+
+int stmg_solve_host(stmg_ctx* c, const double* f_host, double* u_host,
+                    const stmg_cycle_config* cfg, double eps, int max_iter, double* history,
+                    int history_cap, stmg_solve_report* report) {
+  return guard([&] {
+    require(c != nullptr, "null context");
+    check_cfg(cfg);
+    require(f_host && u_host, "null vector");
+    Level& L0 = c->levels[0];
+    const i64 n = L0.view.size();
+    ensure(c->user_f, n);
+    ensure(c->user_u, n);
+    const auto t0 = std::chrono::steady_clock::now();
+    CK(cudaMemcpyAsync(c->user_f.base, f_host, size_t(n) * sizeof(double), cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaMemcpyAsync(c->user_u.base, u_host, size_t(n) * sizeof(double), cudaMemcpyHostToDevice,
+                       c->stream));
+    stmg_solve_report r{};
+    solve_impl(c, c->user_f.base, c->user_u.base, *cfg, eps, max_iter, history, history_cap, &r);
+    CK(cudaMemcpyAsync(u_host, c->user_u.base, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    r.wall_time_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (report) *report = r;
+  });
+}
+
+int stmg_profile_enable(stmg_ctx* c, int on) {
+  return guard([&] {
+    require(c != nullptr, "null context");
+    if (bool(on) != c->profile) {
+      for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
+      c->graphs.clear();  // re-capture with / without event nodes
+    }
+    c->profile = on != 0;
+  });
+}
+
+int stmg_profile_read(stmg_ctx* c, int id, double* total_ms, int64_t* launches,
+                      double* bytes_per_launch) {
+  return guard([&] {
+    require(c != nullptr, "null context");
+    require(id >= 0 && id < 4, "kernel id out of range");
+    CK(cudaStreamSynchronize(c->stream));
+    prof_collect(c);
+    if (total_ms) *total_ms = c->prof[id].total_ms;
+    if (launches) *launches = c->prof[id].launches;
+    if (bytes_per_launch) *bytes_per_launch = c->prof[id].bytes;
+  });
+}
+
+int stmg_profile_reset(stmg_ctx* c) {
+  return guard([&] {
+    require(c != nullptr, "null context");
+    CK(cudaStreamSynchronize(c->stream));
+    prof_collect(c);
+    for (auto& s : c->prof) {
+      s.total_ms = 0.0;
+      s.launches = 0;
+      s.in_graph = false;
+    }
+  });
+}
+
+int stmg_launch_count(const stmg_ctx* c, int64_t* out) {
+  return guard([&] {
+    require(c && out, "null argument");
+    *out = c->launches;
+  });
+}
+
+}  // extern "C"

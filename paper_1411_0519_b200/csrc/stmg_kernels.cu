@@ -1,0 +1,1245 @@
+// stmg_kernels.cu -- sm_100a kernels of the space-time multigrid V-cycle.
+//
+// Two families:
+//  * physical-space operators on nodal values, one per reference entry point
+//    (apply/residual st_system.cpp:44-67, transfers transfer.cpp:75-158,
+//    block solves st_system.cpp:103-130 via orthonormal DST-I line kernels);
+//  * the fused spectral V-cycle: on a uniform Dirichlet grid the orthonormal
+//    sine basis diagonalises M_h and K_h, so the damped block-Jacobi smoother
+//    (smoother.cpp:96-106), the residual and the jump coupling act per mode,
+//    and full weighting couples only the 2^dim "alias" modes {k, N-k} per
+//    axis.  One thread owns a mode (the 2^dim members of an alias group sit in
+//    adjacent lanes) and marches through a chunk of time steps, keeping the
+//    previous slab in registers, so one HBM pass does
+//    pre-smooth + residual + restriction (k_down) or prolongation + correction
+//    + post-smooth + residual norm (k_up).
+//
+// All arithmetic is FP64.  Indexing is 64-bit (level vectors exceed 2^31).
+
+#include <cmath>
+#include <cstdio>
+
+#include "stmg_launch.hpp"
+
+namespace stmg {
+namespace {
+
+using i64 = long long;
+
+template <int NL>
+struct TM {
+  double K[NL][NL], M[NL][NL], N[NL][NL], R1[NL][NL], R2[NL][NL];
+};
+
+template <int NL>
+TM<NL> make_tm(const TimeConsts& c) {
+  TM<NL> t;
+  for (int k = 0; k < NL; ++k)
+    for (int l = 0; l < NL; ++l) {
+      const int i = k * kMaxNL + l;
+      t.K[k][l] = c.K[i];
+      t.M[k][l] = c.M[i];
+      t.N[k][l] = c.N[i];
+      t.R1[k][l] = c.R1[i];
+      t.R2[k][l] = c.R2[i];
+    }
+  return t;
+}
+
+struct SP {
+  i64 n1, nx;
+  int G;  // mode groups per axis = (n1 + 1) / 2
+  double h;
+  const double* __restrict__ mval;
+  const double* __restrict__ kval;
+  const double* __restrict__ rfac;
+};
+
+SP make_sp(const SpaceConsts& s) {
+  SP p;
+  p.n1 = s.n1;
+  p.nx = s.nx;
+  p.G = int((s.n1 + 1) / 2);
+  p.h = s.h;
+  p.mval = s.mval;
+  p.kval = s.kval;
+  p.rfac = s.rfac;
+  return p;
+}
+
+__host__ __device__ constexpr i64 ipow(i64 b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
+
+// ------------------------------------------------------------ per-mode math
+// Exact per-mode block: A_j = M_j K_tau + K_j M_tau.  Its symmetric part is
+// positive definite (K_tau + K_tau^T = psi(tau)psi(tau)^T + psi(0)psi(0)^T),
+// so elimination without pivoting is stable.
+template <int NL>
+__device__ __forceinline__ void solve_mode(const TM<NL>& t, double Mj, double Kj,
+                                           const double (&b)[NL], double (&x)[NL]) {
+  double A[NL][NL];
+#pragma unroll
+  for (int i = 0; i < NL; ++i)
+#pragma unroll
+    for (int j = 0; j < NL; ++j) A[i][j] = Mj * t.K[i][j] + Kj * t.M[i][j];
+  double inv[NL];
+#pragma unroll
+  for (int i = 0; i < NL; ++i) x[i] = b[i];
+#pragma unroll
+  for (int c = 0; c < NL; ++c) {
+    inv[c] = 1.0 / A[c][c];
+#pragma unroll
+    for (int r = c + 1; r < NL; ++r) {
+      const double f = A[r][c] * inv[c];
+#pragma unroll
+      for (int k = c + 1; k < NL; ++k) A[r][k] -= f * A[c][k];
+      x[r] -= f * x[c];
+    }
+  }
+#pragma unroll
+  for (int c = NL - 1; c >= 0; --c) {
+    double s = x[c];
+#pragma unroll
+    for (int k = c + 1; k < NL; ++k) s -= A[c][k] * x[k];
+    x[c] = s * inv[c];
+  }
+}
+
+// y = A_j x
+template <int NL>
+__device__ __forceinline__ void apply_mode(const TM<NL>& t, double Mj, double Kj,
+                                           const double (&x)[NL], double (&y)[NL]) {
+#pragma unroll
+  for (int k = 0; k < NL; ++k) {
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      a += t.K[k][l] * x[l];
+      b += t.M[k][l] * x[l];
+    }
+    y[k] = Mj * a + Kj * b;
+  }
+}
+
+template <int NL>
+__device__ __forceinline__ void matvec(const double (&A)[NL][NL], const double (&x)[NL],
+                                       double (&y)[NL]) {
+#pragma unroll
+  for (int k = 0; k < NL; ++k) {
+    double a = 0.0;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) a += A[k][l] * x[l];
+    y[k] = a;
+  }
+}
+
+// y = A^T x
+template <int NL>
+__device__ __forceinline__ void matvec_t(const double (&A)[NL][NL], const double (&x)[NL],
+                                         double (&y)[NL]) {
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < NL; ++k) a += A[k][l] * x[k];
+    y[l] = a;
+  }
+}
+
+template <int DIM>
+__device__ __forceinline__ void mode_eig(const SP& s, i64 r, double& Mj, double& Kj) {
+  double mv[DIM], kv[DIM];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    const i64 q = r % s.n1;
+    r /= s.n1;
+    mv[a] = __ldg(s.mval + q);
+    kv[a] = __ldg(s.kval + q);
+  }
+  Mj = 1.0;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) Mj *= mv[a];
+  Kj = 0.0;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    double p = kv[a];
+#pragma unroll
+    for (int b = 0; b < DIM; ++b)
+      if (b != a) p *= mv[b];
+    Kj += p;
+  }
+}
+
+template <int NL>
+__device__ __forceinline__ void load_nl(const double* __restrict__ p, i64 nx, double (&v)[NL]) {
+#pragma unroll
+  for (int l = 0; l < NL; ++l) v[l] = __ldg(p + l * nx);
+}
+
+template <int NL>
+__device__ __forceinline__ void load_nl_cs(const double* __restrict__ p, i64 nx, double (&v)[NL]) {
+#pragma unroll
+  for (int l = 0; l < NL; ++l) v[l] = __ldcs(p + l * nx);
+}
+
+template <int NL>
+__device__ __forceinline__ void store_nl(double* __restrict__ p, i64 nx, const double (&v)[NL]) {
+#pragma unroll
+  for (int l = 0; l < NL; ++l) p[l * nx] = v[l];
+}
+
+// Alias-mode groups: per axis the pair {i, n1-1-i} (0-based sine index) that
+// full weighting maps onto coarse mode i; the middle index G-1 is alone and
+// restricts to zero.  Lane bits [0, DIM) of a thread select the member of its
+// group, so a group's 2^DIM members sit in adjacent lanes of one warp and the
+// restriction sums with warp shuffles.
+struct Member {
+  i64 idx;       // fine mode (flat sine index)
+  i64 cidx;      // coarse mode of the group (full coarsening)
+  double Mj, Kj;
+  double fac;    // full-weighting factor of this member (product over axes)
+  bool ok;       // member exists (and group exists)
+  bool cok;      // group has a coarse mode
+};
+
+template <int DIM>
+__device__ __forceinline__ Member make_member(const SP& s, i64 t, i64 n1c, bool full) {
+  Member m;
+  const int b = int(t & ((1 << DIM) - 1));
+  i64 g = t >> DIM;
+  const i64 ngroups = ipow(s.G, DIM);
+  m.ok = g < ngroups;
+  if (!m.ok) g = 0;
+  m.cok = m.ok;
+  i64 idx = 0, mul = 1, ci = 0, cm = 1;
+  double mv[DIM], kv[DIM], fac = 1.0;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    const int ia = int(g % s.G);
+    g /= s.G;
+    const bool mid = ia >= s.G - 1;
+    if (mid) m.cok = false;
+    const int bit = (b >> a) & 1;
+    if (bit && mid) m.ok = false;
+    const i64 q = (bit && !mid) ? (s.n1 - 1 - ia) : i64(ia);
+    idx += q * mul;
+    mul *= s.n1;
+    ci += ia * cm;
+    cm *= n1c;
+    mv[a] = __ldg(s.mval + q);
+    kv[a] = __ldg(s.kval + q);
+    if (full) fac *= __ldg(s.rfac + q);
+  }
+  double M = 1.0, K = 0.0;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) M *= mv[a];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    double p = kv[a];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c)
+      if (c != a) p *= mv[c];
+    K += p;
+  }
+  m.idx = idx;
+  m.cidx = ci;
+  m.Mj = M;
+  m.Kj = K;
+  m.fac = fac;
+  return m;
+}
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < int(blockDim.x >> 5); ++i) t += sh[i];
+  return t;
+}
+
+// Sum over the 2^DIM lanes of an alias group.
+template <int DIM>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = 1; o < (1 << DIM); o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ==================================================== fused spectral kernels
+// k_down: one damped block-Jacobi sweep, the residual of the smoothed iterate
+// and its restriction, for a chunk [n0, n0+C) of time steps of one mode.  The
+// Jacobi sweep uses the frozen old iterate of step n-1 (smoother.cpp:101-104):
+//   u'_n = (1-w) u_n + w A_j^-1 (f_n + M_j N u_{n-1}),
+// the residual r_n = f_n - A_j u'_n + M_j N u'_{n-1}, and the restriction
+// c_{n/2} += fac * R_{1|2} r_n summed over the alias group (transfer.cpp:75-85,
+// 138-149 in the sine basis).
+template <int DIM, int NL, bool ZERO, int CO>
+__global__ void __launch_bounds__(256) k_down(const double* __restrict__ f,
+                                              const double* __restrict__ uin,
+                                              double* __restrict__ uout,
+                                              double* __restrict__ fc, const TM<NL> t,
+                                              const SP s, const i64 n_t, const int C,
+                                              const i64 n1c, const double omega,
+                                              const bool first_global) {
+  const i64 tid = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const Member me = make_member<DIM>(s, tid, n1c, CO == 2);
+  const i64 nx = s.nx, slab = NL * nx;
+  const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
+  const i64 n0 = i64(blockIdx.y) * C;
+  const i64 nend = min(n0 + i64(C), n_t);
+  const double om1 = 1.0 - omega;
+  const double Mj = me.Mj, Kj = me.Kj;
+  const double* fp = f + me.idx;
+  const double* up = uin + me.idx;
+  double* op = uout + me.idx;
+
+  double uo[NL], un[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) uo[l] = un[l] = 0.0;
+
+  if (me.ok && (n0 > 0 || !first_global)) {  // warm-up: smoothed step n0-1
+    double fv[NL], x[NL];
+    load_nl<NL>(fp + (n0 - 1) * slab, nx, fv);
+    if (ZERO) {
+      solve_mode<NL>(t, Mj, Kj, fv, x);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) un[l] = omega * x[l];
+    } else {
+      double u1[NL], u2[NL], nv[NL];
+      load_nl<NL>(up + (n0 - 1) * slab, nx, u1);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) u2[l] = 0.0;
+      if (n0 - 1 > 0 || !first_global) load_nl<NL>(up + (n0 - 2) * slab, nx, u2);
+      matvec<NL>(t.N, u2, nv);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
+      solve_mode<NL>(t, Mj, Kj, fv, x);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        un[l] = om1 * u1[l] + omega * x[l];
+        uo[l] = u1[l];
+      }
+    }
+  }
+
+  for (i64 n = n0; n < nend; n += 2) {
+    double acc[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) acc[l] = 0.0;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const i64 m = n + e;
+      double fv[NL], uv[NL], rhs[NL], x[NL], w[NL];
+#pragma unroll
+      for (int l = 0; l < NL; ++l) fv[l] = uv[l] = 0.0;
+      if (me.ok) {
+        load_nl_cs<NL>(fp + m * slab, nx, fv);
+        if (!ZERO) load_nl_cs<NL>(up + m * slab, nx, uv);
+      }
+      if (!ZERO) {
+        double nv[NL];
+        matvec<NL>(t.N, uo, nv);
+#pragma unroll
+        for (int l = 0; l < NL; ++l) rhs[l] = fv[l] + Mj * nv[l];
+      } else {
+#pragma unroll
+        for (int l = 0; l < NL; ++l) rhs[l] = fv[l];
+      }
+      solve_mode<NL>(t, Mj, Kj, rhs, x);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) w[l] = ZERO ? omega * x[l] : om1 * uv[l] + omega * x[l];
+      if (me.ok) store_nl<NL>(op + m * slab, nx, w);
+      double aw[NL], np[NL], res[NL], rt[NL];
+      apply_mode<NL>(t, Mj, Kj, w, aw);
+      matvec<NL>(t.N, un, np);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) res[l] = fv[l] - aw[l] + Mj * np[l];
+      if (e == 0) matvec<NL>(t.R1, res, rt);
+      else matvec<NL>(t.R2, res, rt);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        acc[l] += (CO == 2) ? me.fac * rt[l] : rt[l];
+        if (!ZERO) uo[l] = uv[l];
+        un[l] = w[l];
+      }
+    }
+    const i64 nc = n >> 1;
+    if (CO == 2) {
+#pragma unroll
+      for (int l = 0; l < NL; ++l) acc[l] = group_sum<DIM>(me.ok ? acc[l] : 0.0);
+      if (me.cok && (threadIdx.x & ((1 << DIM) - 1)) == 0)
+        store_nl<NL>(fc + nc * cslab + me.cidx, nxc, acc);
+    } else if (me.ok) {
+      store_nl<NL>(fc + nc * cslab + me.idx, nxc, acc);
+    }
+  }
+}
+
+// k_up: u <- u + P e_c (mg.cpp:123-127), then one damped block-Jacobi sweep
+// (mg.cpp:129-131); with RESID also the residual of the result and its sum of
+// squares per (chunk, block) for the stop test (mg.cpp:152-153).
+template <int DIM, int NL, int CO, bool RESID>
+__global__ void __launch_bounds__(256) k_up(const double* __restrict__ ec,
+                                            const double* __restrict__ uin,
+                                            const double* __restrict__ f,
+                                            double* __restrict__ uout,
+                                            double* __restrict__ partials, const TM<NL> t,
+                                            const SP s, const i64 n_t, const int C,
+                                            const i64 n1c, const double omega,
+                                            const bool first_global) {
+  __shared__ double sh[32];
+  const i64 tid = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const Member me = make_member<DIM>(s, tid, n1c, CO == 2);
+  const i64 nx = s.nx, slab = NL * nx;
+  const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
+  const i64 n0 = i64(blockIdx.y) * C;
+  const i64 nend = min(n0 + i64(C), n_t);
+  const double om1 = 1.0 - omega;
+  const double Mj = me.Mj, Kj = me.Kj;
+  const double fac = (CO == 2) ? me.fac : 1.0;
+  const bool has_c = (CO == 2) ? me.cok : me.ok;
+  const double* ep = ec + ((CO == 2) ? me.cidx : me.idx);
+  const double* fp = f + me.idx;
+  const double* up = uin + me.idx;
+  double* op = uout + me.idx;
+  double sumsq = 0.0;
+
+  if (me.ok) {
+    double vo[NL], wp[NL], ev[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) vo[l] = wp[l] = ev[l] = 0.0;
+
+    if (n0 > 0 || !first_global) {
+      if (has_c) load_nl<NL>(ep + ((n0 >> 1) - 1) * cslab, nxc, ev);  // coarse step of n0-2, n0-1
+      double u1[NL], c1[NL];
+      load_nl<NL>(up + (n0 - 1) * slab, nx, u1);
+      matvec_t<NL>(t.R2, ev, c1);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) vo[l] = u1[l] + fac * c1[l];
+      if (RESID) {
+        double v2[NL], fv[NL], nv[NL], x[NL];
+#pragma unroll
+        for (int l = 0; l < NL; ++l) v2[l] = 0.0;
+        if (n0 - 1 > 0 || !first_global) {
+          double u2[NL], c2[NL];
+          load_nl<NL>(up + (n0 - 2) * slab, nx, u2);
+          matvec_t<NL>(t.R1, ev, c2);
+#pragma unroll
+          for (int l = 0; l < NL; ++l) v2[l] = u2[l] + fac * c2[l];
+        }
+        load_nl<NL>(fp + (n0 - 1) * slab, nx, fv);
+        matvec<NL>(t.N, v2, nv);
+#pragma unroll
+        for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
+        solve_mode<NL>(t, Mj, Kj, fv, x);
+#pragma unroll
+        for (int l = 0; l < NL; ++l) wp[l] = om1 * vo[l] + omega * x[l];
+      }
+    }
+
+    for (i64 n = n0; n < nend; n += 2) {
+      if (has_c) load_nl<NL>(ep + (n >> 1) * cslab, nxc, ev);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const i64 m = n + e;
+        double uv[NL], fv[NL], c[NL], v[NL], nv[NL], rhs[NL], x[NL], w[NL];
+        load_nl_cs<NL>(up + m * slab, nx, uv);
+        load_nl_cs<NL>(fp + m * slab, nx, fv);
+        if (e == 0) matvec_t<NL>(t.R1, ev, c);
+        else matvec_t<NL>(t.R2, ev, c);
+#pragma unroll
+        for (int l = 0; l < NL; ++l) v[l] = uv[l] + fac * c[l];
+        matvec<NL>(t.N, vo, nv);
+#pragma unroll
+        for (int l = 0; l < NL; ++l) rhs[l] = fv[l] + Mj * nv[l];
+        solve_mode<NL>(t, Mj, Kj, rhs, x);
+#pragma unroll
+        for (int l = 0; l < NL; ++l) w[l] = om1 * v[l] + omega * x[l];
+        store_nl<NL>(op + m * slab, nx, w);
+        if (RESID) {
+          double aw[NL], np[NL];
+          apply_mode<NL>(t, Mj, Kj, w, aw);
+          matvec<NL>(t.N, wp, np);
+#pragma unroll
+          for (int l = 0; l < NL; ++l) {
+            const double r = fv[l] - aw[l] + Mj * np[l];
+            sumsq += r * r;
+          }
+        }
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          vo[l] = v[l];
+          wp[l] = w[l];
+        }
+      }
+    }
+  }
+  if (RESID) {
+    const double tot = block_sum(sumsq, sh);
+    if (threadIdx.x == 0) partials[i64(blockIdx.y) * gridDim.x + blockIdx.x] = tot;
+  }
+}
+// Plain damped block-Jacobi sweep per mode (ping-pong: u_out != u_in).
+template <int DIM, int NL, bool ZERO>
+__global__ void __launch_bounds__(128) k_smooth(const double* __restrict__ f,
+                                                const double* __restrict__ uin,
+                                                double* __restrict__ uout, const TM<NL> t,
+                                                const SP s, const i64 n_t, const int C,
+                                                const double omega, const bool first_global) {
+  const i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= s.nx) return;
+  double Mj, Kj;
+  mode_eig<DIM>(s, r, Mj, Kj);
+  const i64 nx = s.nx, slab = NL * nx;
+  const i64 n0 = i64(blockIdx.y) * C;
+  const i64 nend = min(n0 + i64(C), n_t);
+  double uo[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) uo[l] = 0.0;
+  if (!ZERO && (n0 > 0 || !first_global)) load_nl<NL>(uin + (n0 - 1) * slab + r, nx, uo);
+  for (i64 m = n0; m < nend; ++m) {
+    double fv[NL], uv[NL], nv[NL], x[NL], w[NL];
+    load_nl<NL>(f + m * slab + r, nx, fv);
+    if (!ZERO) {
+      load_nl<NL>(uin + m * slab + r, nx, uv);
+      matvec<NL>(t.N, uo, nv);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
+    }
+    solve_mode<NL>(t, Mj, Kj, fv, x);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      w[l] = ZERO ? omega * x[l] : (1.0 - omega) * uv[l] + omega * x[l];
+      if (!ZERO) uo[l] = uv[l];
+    }
+    store_nl<NL>(uout + m * slab + r, nx, w);
+  }
+}
+
+// Residual sum-of-squares partials of f - L u per (chunk, block).
+template <int DIM, int NL>
+__global__ void __launch_bounds__(128) k_resnorm(const double* __restrict__ u,
+                                                 const double* __restrict__ f,
+                                                 double* __restrict__ partials, const TM<NL> t,
+                                                 const SP s, const i64 n_t, const int C,
+                                                 const bool first_global) {
+  __shared__ double sh[32];
+  const i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  double sumsq = 0.0;
+  if (r < s.nx) {
+    double Mj, Kj;
+    mode_eig<DIM>(s, r, Mj, Kj);
+    const i64 nx = s.nx, slab = NL * nx;
+    const i64 n0 = i64(blockIdx.y) * C;
+    const i64 nend = min(n0 + i64(C), n_t);
+    double up[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) up[l] = 0.0;
+    if (n0 > 0 || !first_global) load_nl<NL>(u + (n0 - 1) * slab + r, nx, up);
+    for (i64 m = n0; m < nend; ++m) {
+      double uv[NL], fv[NL], au[NL], np[NL];
+      load_nl<NL>(u + m * slab + r, nx, uv);
+      load_nl<NL>(f + m * slab + r, nx, fv);
+      apply_mode<NL>(t, Mj, Kj, uv, au);
+      matvec<NL>(t.N, up, np);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        const double res = fv[l] - au[l] + Mj * np[l];
+        sumsq += res * res;
+        up[l] = uv[l];
+      }
+    }
+  }
+  const double tot = block_sum(sumsq, sh);
+  if (threadIdx.x == 0) partials[i64(blockIdx.y) * gridDim.x + blockIdx.x] = tot;
+}
+
+// Per-mode forward substitution u_n = A_j^-1 (f_n + M_j N u_{n-1})
+// (st_system.cpp:118-130 in the sine basis).
+template <int DIM, int NL>
+__global__ void __launch_bounds__(128) k_fwdsub(const double* __restrict__ f,
+                                                double* __restrict__ u, const TM<NL> t,
+                                                const SP s, const i64 n_t) {
+  const i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= s.nx) return;
+  double Mj, Kj;
+  mode_eig<DIM>(s, r, Mj, Kj);
+  const i64 nx = s.nx, slab = NL * nx;
+  double prev[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) prev[l] = 0.0;
+  for (i64 m = 0; m < n_t; ++m) {
+    double fv[NL], nv[NL], x[NL];
+    load_nl<NL>(f + m * slab + r, nx, fv);
+    matvec<NL>(t.N, prev, nv);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
+    solve_mode<NL>(t, Mj, Kj, fv, x);
+    store_nl<NL>(u + m * slab + r, nx, x);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) prev[l] = x[l];
+  }
+}
+
+// Per-mode exact block solve in place.
+template <int DIM, int NL>
+__global__ void __launch_bounds__(256) k_modal_solve(double* __restrict__ x, const TM<NL> t,
+                                                     const SP s, const i64 n_t) {
+  const i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n_t * s.nx) return;
+  const i64 n = e / s.nx, r = e - n * s.nx;
+  double Mj, Kj;
+  mode_eig<DIM>(s, r, Mj, Kj);
+  double b[NL], y[NL];
+  double* p = x + n * NL * s.nx + r;
+  load_nl<NL>(p, s.nx, b);
+  solve_mode<NL>(t, Mj, Kj, b, y);
+  store_nl<NL>(p, s.nx, y);
+}
+
+// ===================================================== physical operators
+// Q1 stencils: M = (x)_a M1, K = sum_a K1 on axis a, M1 elsewhere,
+// M1 = h/6 {1,4,1}, K1 = 1/h {-1,2,-1} (fem_space.cpp:40-58, + 3D).
+template <int DIM>
+__device__ __forceinline__ void coords(i64 r, i64 n1, int (&c)[3]) {
+  c[0] = int(r % n1);
+  c[1] = DIM > 1 ? int((r / n1) % n1) : 0;
+  c[2] = DIM > 2 ? int(r / (n1 * n1)) : 0;
+}
+
+// Accumulate M v and K v at node c of one component vector v.
+template <int DIM>
+__device__ __forceinline__ void stencil_MK(const double* __restrict__ v, i64 n1, double h,
+                                           const int (&c)[3], double& Mv, double& Kv,
+                                           bool want_k) {
+  const double m0 = 4.0 * h / 6.0, m1 = h / 6.0, k0 = 2.0 / h, k1 = -1.0 / h;
+  Mv = 0.0;
+  Kv = 0.0;
+  const int dzlo = DIM > 2 ? -1 : 0, dzhi = DIM > 2 ? 1 : 0;
+  const int dylo = DIM > 1 ? -1 : 0, dyhi = DIM > 1 ? 1 : 0;
+  for (int dz = dzlo; dz <= dzhi; ++dz) {
+    const int z = c[2] + dz;
+    if (z < 0 || z >= n1) continue;
+    for (int dy = dylo; dy <= dyhi; ++dy) {
+      const int y = c[1] + dy;
+      if (y < 0 || y >= n1) continue;
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int x = c[0] + dx;
+        if (x < 0 || x >= n1) continue;
+        const double val = __ldg(v + (i64(z) * n1 + y) * n1 + x);
+        const double mx = dx ? m1 : m0, my = dy ? m1 : m0, mz = dz ? m1 : m0;
+        const double kx = dx ? k1 : k0, ky = dy ? k1 : k0, kz = dz ? k1 : k0;
+        double wm = mx, wk = kx;
+        if (DIM == 2) {
+          wm = mx * my;
+          wk = kx * my + mx * ky;
+        } else if (DIM == 3) {
+          wm = mx * my * mz;
+          wk = kx * my * mz + mx * ky * mz + mx * my * kz;
+        }
+        Mv += wm * val;
+        if (want_k) Kv += wk * val;
+      }
+    }
+  }
+}
+
+// y_n = (M U_n) K^T + (K U_n) M^T - (M U_{n-1}) N^T; residual: r = f - y
+// (st_system.cpp:18-33, 57-67).
+template <int DIM, int NL, bool RES>
+__global__ void __launch_bounds__(256) k_apply(const double* __restrict__ u,
+                                               const double* __restrict__ f,
+                                               double* __restrict__ y, const TM<NL> t,
+                                               const i64 n1, const i64 nx, const double h,
+                                               const i64 n_t, const bool first_global) {
+  const i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n_t * nx) return;
+  const i64 n = e / nx, r = e - n * nx;
+  int c[3];
+  coords<DIM>(r, n1, c);
+  const i64 slab = NL * nx;
+  double MU[NL], KU[NL], MP[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    stencil_MK<DIM>(u + n * slab + l * nx, n1, h, c, MU[l], KU[l], true);
+    MP[l] = 0.0;
+  }
+  if (n > 0 || !first_global) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      double dummy;
+      stencil_MK<DIM>(u + (n - 1) * slab + l * nx, n1, h, c, MP[l], dummy, false);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NL; ++k) {
+    double a = 0.0;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) a += MU[l] * t.K[k][l];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) a += KU[l] * t.M[k][l];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) a -= MP[l] * t.N[k][l];
+    const i64 o = n * slab + k * nx + r;
+    y[o] = RES ? __ldg(f + o) - a : a;
+  }
+}
+
+// restrict_semi / restrict_full (transfer.cpp:75-85, 138-149): one thread per
+// coarse (step, node): full weighting 1/2{1 2 1} per axis of the time
+// restriction c_n = U_2n R1^T + U_2n+1 R2^T.
+template <int DIM, int NL, int CO>
+__global__ void __launch_bounds__(256) k_restrict(const double* __restrict__ fine,
+                                                  double* __restrict__ coarse, const TM<NL> t,
+                                                  const i64 n1, const i64 n1c, const i64 ntc) {
+  const i64 nx = ipow(n1, DIM), nxc = ipow(n1c, DIM);
+  const i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= ntc * nxc) return;
+  const i64 nc = e / nxc, rc = e - nc * nxc;
+  int c[3];
+  coords<DIM>(rc, n1c, c);
+  double v0[NL], v1[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) v0[l] = v1[l] = 0.0;
+  const double* a0 = fine + (2 * nc) * NL * nx;
+  const double* a1 = a0 + NL * nx;
+  if (CO == 1) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      v0[l] = __ldg(a0 + l * nx + rc);
+      v1[l] = __ldg(a1 + l * nx + rc);
+    }
+  } else {
+    const int dzn = DIM > 2 ? 3 : 1, dyn = DIM > 1 ? 3 : 1;
+    for (int dz = 0; dz < dzn; ++dz)
+      for (int dy = 0; dy < dyn; ++dy)
+        for (int dx = 0; dx < 3; ++dx) {
+          const i64 fx = 2 * c[0] + dx;
+          const i64 fy = DIM > 1 ? 2 * c[1] + dy : 0;
+          const i64 fz = DIM > 2 ? 2 * c[2] + dz : 0;
+          const double w = (dx == 1 ? 1.0 : 0.5) * (DIM > 1 ? (dy == 1 ? 1.0 : 0.5) : 1.0) *
+                           (DIM > 2 ? (dz == 1 ? 1.0 : 0.5) : 1.0);
+          const i64 rf = (fz * n1 + fy) * n1 + fx;
+#pragma unroll
+          for (int l = 0; l < NL; ++l) {
+            v0[l] += w * __ldg(a0 + l * nx + rf);
+            v1[l] += w * __ldg(a1 + l * nx + rf);
+          }
+        }
+  }
+  double* o = coarse + nc * NL * nxc + rc;
+#pragma unroll
+  for (int k = 0; k < NL; ++k) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      s0 += v0[l] * t.R1[k][l];
+      s1 += v1[l] * t.R2[k][l];
+    }
+    o[k * nxc] = s0 + s1;
+  }
+}
+
+// prolong_semi / prolong_full (transfer.cpp:87-96, 151-158): one thread per
+// fine (step, node); linear interpolation per axis, U_2n = C_n R1, U_2n+1 = C_n R2.
+template <int DIM, int NL, int CO>
+__global__ void __launch_bounds__(256) k_prolong(const double* __restrict__ coarse,
+                                                 double* __restrict__ fine, const TM<NL> t,
+                                                 const i64 n1, const i64 n1c, const i64 n_t) {
+  const i64 nx = ipow(n1, DIM), nxc = ipow(n1c, DIM);
+  const i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n_t * nx) return;
+  const i64 n = e / nx, r = e - n * nx;
+  const i64 nc = n >> 1;
+  int c[3];
+  coords<DIM>(r, n1, c);
+  double cv[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) cv[l] = 0.0;
+  const double* src = coarse + nc * NL * nxc;
+  if (CO == 1) {
+#pragma unroll
+    for (int k = 0; k < NL; ++k) cv[k] = __ldg(src + k * nxc + r);
+  } else {
+    // per axis: up to two coarse neighbours with weights
+    int j[3][2];
+    double w[3][2];
+    int cnt[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      cnt[a] = 1;
+      j[a][0] = 0;
+      w[a][0] = 1.0;
+      j[a][1] = 0;
+      w[a][1] = 0.0;
+      if (a >= DIM) continue;
+      const int i = c[a];
+      if (i % 2 == 1) {
+        j[a][0] = i / 2;
+      } else {
+        const int jj = i / 2;
+        cnt[a] = 0;
+        if (jj > 0) {
+          j[a][cnt[a]] = jj - 1;
+          w[a][cnt[a]] = 0.5;
+          ++cnt[a];
+        }
+        if (jj < n1c) {
+          j[a][cnt[a]] = jj;
+          w[a][cnt[a]] = 0.5;
+          ++cnt[a];
+        }
+      }
+    }
+    for (int iz = 0; iz < cnt[2]; ++iz)
+      for (int iy = 0; iy < cnt[1]; ++iy)
+        for (int ix = 0; ix < cnt[0]; ++ix) {
+          const double ww = w[0][ix] * w[1][iy] * w[2][iz];
+          const i64 rc = (i64(j[2][iz]) * n1c + j[1][iy]) * n1c + j[0][ix];
+#pragma unroll
+          for (int k = 0; k < NL; ++k) cv[k] += ww * __ldg(src + k * nxc + rc);
+        }
+  }
+  double* o = fine + n * NL * nx + r;
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < NL; ++k) s += cv[k] * ((n & 1) ? t.R2[k][l] : t.R1[k][l]);
+    o[l * nx] = s;
+  }
+}
+
+// f(0,k,:) += psi_k(0) M_h u0.
+template <int DIM, int NL>
+__global__ void k_fold_u0(double* __restrict__ f, const double* __restrict__ u0, const i64 n1,
+                          const i64 nx, const double h, TimeConsts tc) {
+  const i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= nx) return;
+  int c[3];
+  coords<DIM>(r, n1, c);
+  double Mv, Kv;
+  stencil_MK<DIM>(u0, n1, h, c, Mv, Kv, false);
+#pragma unroll
+  for (int k = 0; k < NL; ++k) f[k * nx + r] += tc.psi0[k] * Mv;
+}
+
+// ================================================================ DST-I
+// Orthonormal DST-I of length n1 = N-1 (N = 2^LOG2N) along one axis, two real
+// lines per complex FFT of length 2N: z = a + i b, odd extension; then
+// Z_k = -2i A_k + 2 B_k, so A_k = -Im Z_k / 2, B_k = Re Z_k / 2.
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+template <int LOG2N>
+__global__ void __launch_bounds__(256) k_dst_lines(const double* __restrict__ in,
+                                                   double* __restrict__ out, const i64 n_lines,
+                                                   const i64 stride, const double scale,
+                                                   const double alpha, const int accumulate,
+                                                   const double2* __restrict__ twiddle) {
+  constexpr int N = 1 << LOG2N;
+  constexpr int n1 = N - 1;
+  constexpr int LOG2L = LOG2N + 1;
+  constexpr int L = 1 << LOG2L;
+  constexpr int PAIRS = (2048 / L) > 0 ? (2048 / L) : 1;
+  constexpr int TL = 2 * PAIRS;  // lines per tile
+  extern __shared__ double2 sm[];
+  double2* tw = sm + PAIRS * L;
+  double* smd = reinterpret_cast<double*>(sm);
+
+  for (int k = threadIdx.x; k < L / 2; k += blockDim.x) tw[k] = twiddle[k];
+  for (int k = threadIdx.x; k < PAIRS * L; k += blockDim.x) sm[k] = make_double2(0.0, 0.0);
+  __syncthreads();
+
+  const i64 line0 = i64(blockIdx.x) * TL;
+  const int nt = int(min(i64(TL), n_lines - line0));
+  const int tile = TL * n1;
+  for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+    int li, j;
+    if (stride == 1) {
+      li = e / n1;
+      j = e - li * n1;
+    } else {
+      j = e / TL;
+      li = e - j * TL;
+    }
+    if (li >= nt) continue;
+    const i64 line = line0 + li;
+    const i64 o = line / stride, tt = line - o * stride;
+    const double v = in[(o * n1 + j) * stride + tt];
+    const int p = li >> 1, comp = li & 1;
+    const int pos = j + 1;
+    const int b1 = int(__brev(unsigned(pos)) >> (32 - LOG2L));
+    const int b2 = int(__brev(unsigned(L - pos)) >> (32 - LOG2L));
+    smd[2 * (p * L + b1) + comp] = v;
+    smd[2 * (p * L + b2) + comp] = -v;
+  }
+  __syncthreads();
+
+#pragma unroll 1
+  for (int s = 1; s <= LOG2L; ++s) {
+    const int half = 1 << (s - 1);
+    for (int bf = threadIdx.x; bf < PAIRS * (L / 2); bf += blockDim.x) {
+      const int p = bf >> (LOG2L - 1);
+      const int b = bf & (L / 2 - 1);
+      const int grp = b >> (s - 1);
+      const int pos = b & (half - 1);
+      const int i = p * L + grp * 2 * half + pos;
+      const int jj = i + half;
+      const double2 w = tw[pos << (LOG2L - s)];
+      const double2 x = sm[i];
+      const double2 y = cmul(w, sm[jj]);
+      sm[i] = make_double2(x.x + y.x, x.y + y.y);
+      sm[jj] = make_double2(x.x - y.x, x.y - y.y);
+    }
+    __syncthreads();
+  }
+
+  const double hs = 0.5 * scale;
+  for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+    int li, j;
+    if (stride == 1) {
+      li = e / n1;
+      j = e - li * n1;
+    } else {
+      j = e / TL;
+      li = e - j * TL;
+    }
+    if (li >= nt) continue;
+    const i64 line = line0 + li;
+    const i64 o = line / stride, tt = line - o * stride;
+    const int p = li >> 1, comp = li & 1;
+    const double2 Z = sm[p * L + j + 1];
+    const double v = (comp == 0 ? -Z.y : Z.x) * hs;
+    const i64 addr = (o * n1 + j) * stride + tt;
+    if (accumulate) out[addr] += alpha * v;
+    else out[addr] = v;
+  }
+}
+
+// ================================================================ misc
+__global__ void __launch_bounds__(256) k_step_sumsq(const double* __restrict__ v, const i64 slab,
+                                                    double* __restrict__ partial) {
+  __shared__ double sh[32];
+  const double* p = v + i64(blockIdx.x) * slab;
+  double s = 0.0;
+  for (i64 i = threadIdx.x; i < slab; i += blockDim.x) {
+    const double x = p[i];
+    s += x * x;
+  }
+  const double tot = block_sum(s, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+// Fixed-order reduction: thread t sums partial[t], partial[t+256], ...
+// then a fixed tree; bitwise reproducible for a given partial array.
+__global__ void __launch_bounds__(256) k_norm_final(const double* __restrict__ partial,
+                                                    const i64 n, double* __restrict__ out,
+                                                    double* __restrict__ hist, const int hidx) {
+  __shared__ double sh[256];
+  double s = 0.0;
+  for (i64 i = threadIdx.x; i < n; i += 256) s += partial[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (int(threadIdx.x) < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double r = sqrt(sh[0]);
+    out[0] = r;
+    if (hist) hist[hidx] = r;
+  }
+}
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_fill_uniform(double* __restrict__ v, const i64 n, const unsigned long long seed,
+                               const unsigned long long stream, const i64 offset) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long ctr = (stream << 56) + (unsigned long long)(offset + i);
+  const unsigned long long x = mix64(seed + 0x9E3779B97F4A7C15ULL * ctr);
+  v[i] = 2.0 * (double(x >> 11) * 0x1.0p-53) - 1.0;
+}
+
+__global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, const double a,
+                       const i64 n) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) y[i] += a * x[i];
+}
+
+inline unsigned grid1(i64 n, int bs) { return unsigned((n + bs - 1) / bs); }
+
+}  // namespace
+
+// ============================================================== dispatch
+#define STMG_CASE(D, Q, ...)           \
+  case (D) * 8 + (Q): {                \
+    constexpr int DIM = (D), NL = (Q); \
+    __VA_ARGS__;                       \
+  } break;
+
+#define STMG_DISPATCH(dim, nl, ...)                                                    \
+  switch ((dim) * 8 + (nl)) {                                                          \
+    STMG_CASE(1, 1, __VA_ARGS__)                                                       \
+    STMG_CASE(1, 2, __VA_ARGS__)                                                       \
+    STMG_CASE(1, 3, __VA_ARGS__)                                                       \
+    STMG_CASE(1, 4, __VA_ARGS__)                                                       \
+    STMG_CASE(2, 1, __VA_ARGS__)                                                       \
+    STMG_CASE(2, 2, __VA_ARGS__)                                                       \
+    STMG_CASE(2, 3, __VA_ARGS__)                                                       \
+    STMG_CASE(2, 4, __VA_ARGS__)                                                       \
+    STMG_CASE(3, 1, __VA_ARGS__)                                                       \
+    STMG_CASE(3, 2, __VA_ARGS__)                                                       \
+    STMG_CASE(3, 3, __VA_ARGS__)                                                       \
+    STMG_CASE(3, 4, __VA_ARGS__)                                                       \
+    default:                                                                           \
+      return cudaErrorInvalidValue;                                                    \
+  }
+
+cudaError_t launch_apply(const LevelView& L, const double* u, const double* f, double* y,
+                         bool residual, cudaStream_t st) {
+  const i64 total = L.n_t * L.sp.nx;
+  if (total == 0) return cudaSuccess;
+  STMG_DISPATCH(L.sp.dim, L.tc.nl, {
+    const TM<NL> t = make_tm<NL>(L.tc);
+    if (residual)
+      k_apply<DIM, NL, true><<<grid1(total, 256), 256, 0, st>>>(u, f, y, t, L.sp.n1, L.sp.nx,
+                                                                 L.sp.h, L.n_t, L.first_global);
+    else
+      k_apply<DIM, NL, false><<<grid1(total, 256), 256, 0, st>>>(u, f, y, t, L.sp.n1, L.sp.nx,
+                                                                  L.sp.h, L.n_t, L.first_global);
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_restrict(const LevelView& F, int mode, int64_t n1c, const double* fine,
+                            double* coarse, cudaStream_t st) {
+  const i64 ntc = F.n_t / 2;
+  const i64 n1o = mode == 2 ? n1c : F.sp.n1;
+  const i64 total = ntc * ipow(n1o, 1) * (F.sp.dim > 1 ? n1o : 1) * (F.sp.dim > 2 ? n1o : 1);
+  if (total == 0) return cudaSuccess;
+  STMG_DISPATCH(F.sp.dim, F.tc.nl, {
+    const TM<NL> t = make_tm<NL>(F.tc);
+    if (mode == 2)
+      k_restrict<DIM, NL, 2><<<grid1(total, 256), 256, 0, st>>>(fine, coarse, t, F.sp.n1, n1c, ntc);
+    else
+      k_restrict<DIM, NL, 1><<<grid1(total, 256), 256, 0, st>>>(fine, coarse, t, F.sp.n1, F.sp.n1,
+                                                               ntc);
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prolong(const LevelView& F, int mode, int64_t n1c, const double* coarse,
+                           double* fine, cudaStream_t st) {
+  const i64 total = F.n_t * F.sp.nx;
+  if (total == 0) return cudaSuccess;
+  STMG_DISPATCH(F.sp.dim, F.tc.nl, {
+    const TM<NL> t = make_tm<NL>(F.tc);
+    if (mode == 2)
+      k_prolong<DIM, NL, 2><<<grid1(total, 256), 256, 0, st>>>(coarse, fine, t, F.sp.n1, n1c, F.n_t);
+    else
+      k_prolong<DIM, NL, 1><<<grid1(total, 256), 256, 0, st>>>(coarse, fine, t, F.sp.n1, F.sp.n1,
+                                                              F.n_t);
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fold_u0(const LevelView& L, double* f, const double* u0, cudaStream_t st) {
+  STMG_DISPATCH(L.sp.dim, L.tc.nl, {
+    k_fold_u0<DIM, NL><<<grid1(L.sp.nx, 256), 256, 0, st>>>(f, u0, L.sp.n1, L.sp.nx, L.sp.h, L.tc);
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dst_axis(const LevelView& L, int axis, const double* in, double* out,
+                            bool accumulate, double alpha, const void* twiddles,
+                            cudaStream_t st) {
+  const i64 n1 = L.sp.n1;
+  const i64 n_lines = L.size() / n1;
+  if (n_lines == 0) return cudaSuccess;
+  i64 stride = 1;
+  for (int a = 0; a < axis; ++a) stride *= n1;
+  int log2n = 0;
+  while ((i64(1) << log2n) < n1 + 1) ++log2n;
+  if ((i64(1) << log2n) != n1 + 1) return cudaErrorInvalidValue;
+  const double scale = std::sqrt(2.0 / double(n1 + 1));
+  const double2* tw = static_cast<const double2*>(twiddles);
+  switch (log2n) {
+#define STMG_DST_CASE(K)                                                                   \
+  case K: {                                                                                \
+    constexpr int Lf = 2 << K;                                                             \
+    constexpr int PAIRS = (2048 / Lf) > 0 ? (2048 / Lf) : 1;                               \
+    const size_t smem = size_t(PAIRS) * Lf * sizeof(double2) + size_t(Lf / 2) * sizeof(double2); \
+    const unsigned grid = unsigned((n_lines + 2 * PAIRS - 1) / (2 * PAIRS));             \
+    if (smem > 48 * 1024)                                                                  \
+      cudaFuncSetAttribute(k_dst_lines<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                           int(smem));                                                     \
+    k_dst_lines<K><<<grid, 256, smem, st>>>(in, out, n_lines, stride, scale, alpha,        \
+                                             accumulate ? 1 : 0, tw);                      \
+  } break;
+    STMG_DST_CASE(1)
+    STMG_DST_CASE(2)
+    STMG_DST_CASE(3)
+    STMG_DST_CASE(4)
+    STMG_DST_CASE(5)
+    STMG_DST_CASE(6)
+    STMG_DST_CASE(7)
+    STMG_DST_CASE(8)
+    STMG_DST_CASE(9)
+    STMG_DST_CASE(10)
+#undef STMG_DST_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_modal_solve(const LevelView& L, double* x, cudaStream_t st) {
+  const i64 total = L.n_t * L.sp.nx;
+  if (total == 0) return cudaSuccess;
+  const SP s = make_sp(L.sp);
+  STMG_DISPATCH(L.sp.dim, L.tc.nl, {
+    k_modal_solve<DIM, NL><<<grid1(total, 256), 256, 0, st>>>(x, make_tm<NL>(L.tc), s, L.n_t);
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_modal_fwdsub(const LevelView& L, const double* f, double* u, cudaStream_t st) {
+  const SP s = make_sp(L.sp);
+  STMG_DISPATCH(L.sp.dim, L.tc.nl, {
+    k_fwdsub<DIM, NL><<<grid1(L.sp.nx, 128), 128, 0, st>>>(f, u, make_tm<NL>(L.tc), s, L.n_t);
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_step_sumsq(const LevelView& L, const double* v, double* partial,
+                              cudaStream_t st) {
+  if (L.n_t == 0) return cudaSuccess;
+  k_step_sumsq<<<unsigned(L.n_t), 256, 0, st>>>(v, L.slab(), partial);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_norm_final(const double* partial, int64_t n, double* out, double* hist,
+                              int hidx, cudaStream_t st) {
+  k_norm_final<<<1, 256, 0, st>>>(partial, n, out, hist, hidx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_uniform(double* v, int64_t n, uint64_t seed, uint64_t stream,
+                                int64_t offset, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_fill_uniform<<<grid1(n, 256), 256, 0, st>>>(v, n, seed, stream, offset);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_axpy<<<grid1(n, 256), 256, 0, st>>>(y, x, a, n);
+  return cudaGetLastError();
+}
+
+int pick_chunk(const LevelView& L, bool grouped) {
+  const i64 G = (L.sp.n1 + 1) / 2;
+  const i64 units = grouped ? (ipow(G, L.sp.dim) << L.sp.dim) : L.sp.nx;
+  // aim for ~64K threads; chunks are even and divide the (power-of-two) n_t
+  const i64 target = 65536;
+  i64 c = 2;
+  while (c < 64 && c * 2 <= L.n_t && units * (L.n_t / (c * 2)) >= target) c *= 2;
+  if (c > L.n_t) c = L.n_t;
+  if (c < 2) c = 2;
+  return int(c);
+}
+
+cudaError_t launch_down(const LevelView& L, ModalArgs& a, bool zero_guess, const double* f,
+                        const double* u_in, double* u_out, double* fc, cudaStream_t st) {
+  const SP s = make_sp(L.sp);
+  const i64 lanes = ipow(s.G, L.sp.dim) << L.sp.dim;
+  const dim3 grid(grid1(lanes, 128), unsigned((L.n_t + a.chunk - 1) / a.chunk));
+  STMG_DISPATCH(L.sp.dim, L.tc.nl, {
+    const TM<NL> t = make_tm<NL>(L.tc);
+    if (a.mode == 2) {
+      if (zero_guess)
+        k_down<DIM, NL, true, 2><<<grid, 128, 0, st>>>(f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
+                                                      a.n1c, a.omega, L.first_global);
+      else
+        k_down<DIM, NL, false, 2><<<grid, 128, 0, st>>>(f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
+                                                       a.n1c, a.omega, L.first_global);
+    } else {
+      if (zero_guess)
+        k_down<DIM, NL, true, 1><<<grid, 128, 0, st>>>(f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
+                                                      L.sp.n1, a.omega, L.first_global);
+      else
+        k_down<DIM, NL, false, 1><<<grid, 128, 0, st>>>(f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
+                                                       L.sp.n1, a.omega, L.first_global);
+    }
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_up(const LevelView& L, ModalArgs& a, const double* ec, const double* u_in,
+                      const double* f, double* u_out, double* partials, cudaStream_t st) {
+  const SP s = make_sp(L.sp);
+  const i64 lanes = ipow(s.G, L.sp.dim) << L.sp.dim;
+  const dim3 grid(grid1(lanes, 128), unsigned((L.n_t + a.chunk - 1) / a.chunk));
+  a.n_partials = i64(grid.x) * grid.y;
+  STMG_DISPATCH(L.sp.dim, L.tc.nl, {
+    const TM<NL> t = make_tm<NL>(L.tc);
+    const i64 n1c = a.mode == 2 ? a.n1c : L.sp.n1;
+    if (a.mode == 2) {
+      if (partials)
+        k_up<DIM, NL, 2, true><<<grid, 128, 0, st>>>(ec, u_in, f, u_out, partials, t, s, L.n_t,
+                                                    a.chunk, n1c, a.omega, L.first_global);
+      else
+        k_up<DIM, NL, 2, false><<<grid, 128, 0, st>>>(ec, u_in, f, u_out, partials, t, s, L.n_t,
+                                                     a.chunk, n1c, a.omega, L.first_global);
+    } else {
+      if (partials)
+        k_up<DIM, NL, 1, true><<<grid, 128, 0, st>>>(ec, u_in, f, u_out, partials, t, s, L.n_t,
+                                                    a.chunk, n1c, a.omega, L.first_global);
+      else
+        k_up<DIM, NL, 1, false><<<grid, 128, 0, st>>>(ec, u_in, f, u_out, partials, t, s, L.n_t,
+                                                     a.chunk, n1c, a.omega, L.first_global);
+    }
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_smooth(const LevelView& L, ModalArgs& a, bool zero_guess, const double* f,
+                          const double* u_in, double* u_out, cudaStream_t st) {
+  const SP s = make_sp(L.sp);
+  const dim3 grid(grid1(L.sp.nx, 128), unsigned((L.n_t + a.chunk - 1) / a.chunk));
+  STMG_DISPATCH(L.sp.dim, L.tc.nl, {
+    const TM<NL> t = make_tm<NL>(L.tc);
+    if (zero_guess)
+      k_smooth<DIM, NL, true><<<grid, 128, 0, st>>>(f, u_in, u_out, t, s, L.n_t, a.chunk, a.omega,
+                                                   L.first_global);
+    else
+      k_smooth<DIM, NL, false><<<grid, 128, 0, st>>>(f, u_in, u_out, t, s, L.n_t, a.chunk, a.omega,
+                                                    L.first_global);
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_resnorm(const LevelView& L, ModalArgs& a, const double* u, const double* f,
+                           double* partials, cudaStream_t st) {
+  const SP s = make_sp(L.sp);
+  const dim3 grid(grid1(L.sp.nx, 128), unsigned((L.n_t + a.chunk - 1) / a.chunk));
+  a.n_partials = i64(grid.x) * grid.y;
+  STMG_DISPATCH(L.sp.dim, L.tc.nl, {
+    k_resnorm<DIM, NL><<<grid, 128, 0, st>>>(u, f, partials, make_tm<NL>(L.tc), s, L.n_t, a.chunk,
+                                            L.first_global);
+  });
+  return cudaGetLastError();
+}
+
+}  // namespace stmg

@@ -1,0 +1,104 @@
+// stmg_launch.hpp -- internal interface between the host driver
+// (stmg_capi.cu) and the sm_100a kernels (stmg_kernels.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace stmg {
+
+constexpr int kMaxNL = 4;  // p_t <= 3 on the GPU path
+
+// DG time-step blocks and transfer blocks, row-major with row stride kMaxNL.
+struct TimeConsts {
+  int nl = 1;
+  double K[kMaxNL * kMaxNL] = {};
+  double M[kMaxNL * kMaxNL] = {};
+  double N[kMaxNL * kMaxNL] = {};
+  double R1[kMaxNL * kMaxNL] = {};
+  double R2[kMaxNL * kMaxNL] = {};
+  double psi0[kMaxNL] = {};  // psi_k(0), for folding u0
+};
+
+// Uniform Dirichlet grid of one level and its device-side sine tables.
+struct SpaceConsts {
+  int dim = 1;
+  int64_t n1 = 1;  // interior nodes per axis
+  int64_t nx = 1;  // n1^dim
+  double h = 0.5;
+  const double* mval = nullptr;  // [n1] eigenvalues of M1 in the sine basis
+  const double* kval = nullptr;  // [n1] eigenvalues of K1
+  const double* rfac = nullptr;  // [n1] full-weighting factor per fine mode
+};
+
+// One level as the kernels see it.  first_global: local step 0 is global
+// step 0 (no previous slab); otherwise step -1/-2 live in halo slabs in
+// front of every level buffer.
+struct LevelView {
+  int64_t n_t = 1;  // local time steps
+  bool first_global = true;
+  TimeConsts tc;
+  SpaceConsts sp;
+  int64_t slab() const { return int64_t(tc.nl) * sp.nx; }
+  int64_t size() const { return n_t * slab(); }
+};
+
+// ---- physical-space operators (nodal values) ------------------------------
+cudaError_t launch_apply(const LevelView& L, const double* u, const double* f,
+                         double* y, bool residual, cudaStream_t st);
+cudaError_t launch_restrict(const LevelView& F, int mode, int64_t n1c,
+                            const double* fine, double* coarse, cudaStream_t st);
+cudaError_t launch_prolong(const LevelView& F, int mode, int64_t n1c,
+                           const double* coarse, double* fine, cudaStream_t st);
+cudaError_t launch_fold_u0(const LevelView& L, double* f, const double* u0,
+                           cudaStream_t st);
+// Orthonormal DST-I along `axis` of every line of a level vector (in may be
+// == out).  accumulate: out += alpha * DST(in), else out = DST(in).
+cudaError_t launch_dst_axis(const LevelView& L, int axis, const double* in,
+                            double* out, bool accumulate, double alpha,
+                            const void* twiddles, cudaStream_t st);
+// Per-mode exact block solve in the sine basis, in place.
+cudaError_t launch_modal_solve(const LevelView& L, double* x, cudaStream_t st);
+// Per-mode sequential forward substitution in the sine basis.
+cudaError_t launch_modal_fwdsub(const LevelView& L, const double* f, double* u,
+                                cudaStream_t st);
+// Per-step sum of squares: partial[n] = sum over slab n of v^2.
+cudaError_t launch_step_sumsq(const LevelView& L, const double* v,
+                              double* partial, cudaStream_t st);
+// out[0] = sqrt(sum partial[0..n)) in a fixed order; hist[hidx] too if hist.
+cudaError_t launch_norm_final(const double* partial, int64_t n, double* out,
+                              double* hist, int hidx, cudaStream_t st);
+cudaError_t launch_fill_uniform(double* v, int64_t n, uint64_t seed,
+                                uint64_t stream, int64_t offset, cudaStream_t st);
+cudaError_t launch_axpy(double* y, const double* x, double a, int64_t n,
+                        cudaStream_t st);
+
+// ---- fused spectral V-cycle kernels (sine coefficients) -------------------
+struct ModalArgs {
+  double omega = 0.5;
+  int chunk = 2;         // time steps per thread (even)
+  int64_t n1c = 0;       // coarse nodes per axis (full coarsening)
+  int mode = 1;          // 1 semi, 2 full (coarsening to the next level)
+  int64_t n_partials = 0;  // out: number of partial sums written
+};
+// Pre-smooth (one damped block-Jacobi sweep) + residual + restriction.
+// zero_guess: u_in == 0 (coarse levels).  Writes u_out and fc.
+cudaError_t launch_down(const LevelView& L, ModalArgs& a, bool zero_guess,
+                        const double* f, const double* u_in, double* u_out,
+                        double* fc, cudaStream_t st);
+// Prolong + correct + post-smooth (+ residual sum of squares if partials).
+cudaError_t launch_up(const LevelView& L, ModalArgs& a, const double* ec,
+                      const double* u_in, const double* f, double* u_out,
+                      double* partials, cudaStream_t st);
+// Plain damped block-Jacobi sweep u_out = S(u_in).
+cudaError_t launch_smooth(const LevelView& L, ModalArgs& a, bool zero_guess,
+                          const double* f, const double* u_in, double* u_out,
+                          cudaStream_t st);
+// Residual sum-of-squares partials of f - L u.
+cudaError_t launch_resnorm(const LevelView& L, ModalArgs& a, const double* u,
+                           const double* f, double* partials, cudaStream_t st);
+
+// Chunk length heuristic for the modal kernels at a level.
+int pick_chunk(const LevelView& L, bool grouped);
+
+}  // namespace stmg

@@ -1,0 +1,37 @@
+// Uses the C++ shim exactly like a caller of the reference stmg:: API would
+// (mg.hpp / st_system.hpp / smoother.hpp / transfer.hpp) and prints a JSON
+// line; run on a GPU by tests/test_gpu_parity.py::test_cpp_shim_solves_c1.
+#include <cmath>
+#include <cstdio>
+
+#include "stmg_b200.hpp"
+
+int main() {
+  using namespace stmg;
+  HierarchyParams p;
+  p.p_t = 1;
+  p.dim = 1;
+  p.space_level = 5;
+  p.time_level = 6;
+  p.t_final = 1.0;
+  p.mu_star = lfa::critical_mu(1);
+  const STHierarchy h = build_hierarchy(p);
+  const STOperator op = h.finest().op();
+  BlockVector f = make_vector(op), u = make_vector(op), r = make_vector(op);
+  fill_random(f, 42, 0);
+  CycleConfig cfg;
+  cfg.nu1 = cfg.nu2 = 1;
+  const SolveReport rep = solve(h, f, u, cfg, 1e-8);
+  residual(op, u, f, r);
+  const double rel = norm(op, r) / norm(op, f);
+  bool threw = false;
+  try {
+    BlockVector odd(op.ctx, 3, 63, 2);
+    (void)restrict_semi(STOperator{op.ctx, int(h.levels.size()) - 1}, odd);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  std::printf("{\"iterations\": %d, \"converged\": %d, \"rel_residual\": %.17g, \"levels\": %zu, \"threw\": %d}\n",
+              rep.iterations, int(rep.converged), rel, h.levels.size(), int(threw));
+  return rep.converged && rel <= 1e-8 && threw ? 0 : 1;
+}

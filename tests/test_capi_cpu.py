@@ -1,0 +1,98 @@
+"""CPU-only checks of the C-ABI library: it builds for sm_100a, loads, exports
+every symbol include/stmg_b200.h declares, its host setup agrees with the
+oracle, and it refuses to run without a GPU (no CPU fallback)."""
+import ctypes
+import math
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_1411_0519_b200 import build as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def capi():
+    B.build()
+    from paper_1411_0519_b200 import _capi
+    return _capi
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "stmg_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(stmg_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_symbols_are_exported(capi):
+    lib = ctypes.CDLL(capi.LIB_PATH)
+    names = _declared_symbols()
+    assert len(names) >= 30
+    for n in names:
+        assert hasattr(lib, n), n
+    bound = {s[0] for s in capi.SIGNATURES}
+    assert set(names) == bound
+
+
+def test_library_is_sm100a(capi):
+    out = subprocess.run(["cuobjdump", "--list-elf", capi.LIB_PATH], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_cpp_shim_compiles(capi):
+    """The C++ shim with the reference signatures compiles against the C ABI."""
+    src = os.path.join(ROOT, "tests", "cpp", "shim_smoke.cpp")
+    out = os.path.join(ROOT, "tests", "cpp", "_shim_smoke")
+    r = subprocess.run(["/usr/bin/g++", "-std=c++17", "-O1", "-I" + os.path.join(ROOT, "include"),
+                        src, capi.LIB_PATH, "-Wl,-rpath," + os.path.dirname(capi.LIB_PATH),
+                        "-o", out], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
+def test_host_setup_matches_oracle(capi, oracle):
+    from paper_1411_0519_b200 import stmg
+    for p in range(0, 4):
+        for tau in (0.3, 1.0 / 256):
+            K, M, N = stmg.assemble_dg_block(p, tau)
+            Ko, Mo, No = oracle.assemble_dg(p, tau)
+            assert np.abs(K - Ko).max() < 1e-13
+            assert np.abs(M - Mo).max() < 1e-15 + 1e-13 * tau
+            assert np.abs(N - No).max() < 1e-14
+            R1, R2 = stmg.build_time_transfer(p, tau)
+            R1o, R2o = oracle.time_transfer(p, tau)
+            assert np.abs(R1 - R1o).max() < 1e-12 and np.abs(R2 - R2o).max() < 1e-12
+    for p in range(0, 11):
+        assert abs(stmg.critical_mu(p) - oracle.critical_mu(p)) < 1e-11
+
+
+def test_host_setup_rejects_bad_arguments(capi):
+    from paper_1411_0519_b200 import stmg
+    with pytest.raises(ValueError):
+        stmg.assemble_dg_block(11, 1.0)
+    with pytest.raises(ValueError):
+        stmg.assemble_dg_block(1, 0.0)
+    with pytest.raises(ValueError):
+        stmg.Hierarchy(1, 4, 3, 3)
+    with pytest.raises(ValueError):
+        stmg.Hierarchy(4, 1, 3, 3)  # p_t > 3 not on the GPU path
+    with pytest.raises(ValueError):
+        stmg.Hierarchy(1, 1, 0, 2, two_grid=2)
+
+
+def _has_gpu():
+    try:
+        r = subprocess.run(["nvidia-smi", "-L"], capture_output=True, text=True, timeout=20)
+        return r.returncode == 0 and "GPU" in r.stdout
+    except Exception:
+        return False
+
+
+@pytest.mark.skipif(_has_gpu(), reason="checks the no-GPU failure mode")
+def test_no_cpu_fallback(capi):
+    from paper_1411_0519_b200 import stmg
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        stmg.Hierarchy(1, 1, 5, 6)

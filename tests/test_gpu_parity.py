@@ -1,0 +1,260 @@
+"""GPU parity: every C-ABI entry point against the CPU oracle on the same
+seeded inputs (oracle = C++ restatement of the reference, pinned in
+tests/test_oracle.py).
+
+Tolerances: operators 1e-12 relative (the reference's matrix-free vs dense
+bar, test_st_system.cpp:83-84); V-cycle iterates 1e-10 relative per cycle and
+identical iteration counts to 1e-8 (BASELINE.json north_star).
+"""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_1411_0519_b200 import build
+    build.build()
+    O.build()
+    from paper_1411_0519_b200 import stmg
+    return stmg
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+CASES = [  # (p_t, dim, space_level, time_level, T, policy)
+    (0, 1, 3, 3, 1.0, 0),
+    (1, 1, 5, 6, 1.0, 0),
+    (2, 1, 4, 4, 0.5, 0),
+    (3, 1, 3, 3, 1.0, 0),
+    (1, 2, 3, 4, 1.0, 0),
+    (2, 2, 3, 3, 0.25, 0),
+    (1, 3, 2, 3, 1.0, 0),
+    (1, 2, 3, 3, 1.0, 1),
+    (1, 2, 3, 3, 1.0, 2),
+]
+
+
+def pair(S, p, dim, sl, tl, T, policy=0, two_grid=0):
+    g = S.Hierarchy(p, dim, sl, tl, t_final=T, policy=policy, two_grid=two_grid)
+    o = O.Hierarchy(p, dim, sl, tl, t_final=T, policy=policy, two_grid=two_grid)
+    assert [L["coarsen_to_next"] for L in g.levels] == [L.coarsen_to_next for L in o.levels]
+    assert [L["n_t"] for L in g.levels] == [L.n_t for L in o.levels]
+    return g, o
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_operators_match_oracle(S, case):
+    p, dim, sl, tl, T, pol = case
+    g, o = pair(S, p, dim, sl, tl, T, pol)
+    for lev in range(len(o.levels)):
+        n = o.levels[lev].size
+        u = O.fill_uniform(n, 100 + lev, 0)
+        f = O.fill_uniform(n, 200 + lev, 0)
+        du, df = g.upload(u, lev), g.upload(f, lev)
+        # apply / residual (st_system.cpp:44-67)
+        assert rel(g.apply(lev, du).numpy(), o.apply(lev, u)) < 1e-12
+        r_o = o.residual(lev, u, f)
+        assert rel(g.residual(lev, du, df).numpy(), r_o) < 1e-12
+        # norm (st_system.cpp:8-16)
+        assert abs(g.norm(lev, df) - o.norm(lev, f)) <= 1e-13 * o.norm(lev, f)
+        # exact block solves (st_system.cpp:103-116)
+        assert rel(g.block_solve(lev, df).numpy(), o.block_solve(lev, f)) < 1e-12
+        # block Jacobi (smoother.cpp:96-106)
+        us = g.block_jacobi_step(lev, g.upload(u, lev), df, 0.5, 2).numpy()
+        assert rel(us, o.smooth(lev, u, f, 0.5, 2)) < 1e-11
+        # forward substitution (st_system.cpp:118-130)
+        assert rel(g.forward_substitution_solve(lev, df).numpy(), o.forward_substitution(lev, f)) < 1e-11
+        # transfers (transfer.cpp)
+        if o.levels[lev].coarsen_to_next:
+            for mode in (1, 2):
+                if mode == 2 and o.levels[lev].n1 == 1:
+                    continue
+                rc = g.restrict(lev, du, mode).numpy()
+                assert rel(rc, o.restrict(lev, u, mode)) < 1e-13
+                c = O.fill_uniform(rc.size, 300 + lev, 0)
+                dc = g.coarse_vector(lev, mode).copy_from(c)
+                assert rel(g.prolong(lev, dc, mode).numpy(), o.prolong(lev, c, mode)) < 1e-13
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("path", ["spectral", "physical"])
+def test_vcycle_iterates_match_oracle(S, case, path):
+    p, dim, sl, tl, T, pol = case
+    g, o = pair(S, p, dim, sl, tl, T, pol)
+    f = O.fill_uniform(o.levels[0].size, 7, 0)
+    df = g.upload(f)
+    u = np.zeros_like(f)
+    du = g.upload(u)
+    cfg = S.CycleConfig(nu1=1, nu2=1, gamma=1, omega_t=0.5, path=path)
+    for k in range(4):
+        u = o.mg_cycle(0, u, f, 1, 1, 1, 0.5)
+        g.mg_cycle(0, du, df, cfg)
+        assert rel(du.numpy(), u) < 1e-10, (k, path)
+
+
+@pytest.mark.parametrize("nu", [(2, 2), (1, 0), (0, 1), (2, 1)])
+def test_vcycle_general_nu_and_gamma(S, nu):
+    g, o = pair(S, 1, 2, 3, 4, 1.0)
+    f = O.fill_uniform(o.levels[0].size, 8, 0)
+    df = g.upload(f)
+    for gamma in (1, 2):
+        u = np.zeros_like(f)
+        du = g.upload(u)
+        cfg = S.CycleConfig(nu1=nu[0], nu2=nu[1], gamma=gamma, omega_t=0.5)
+        for _ in range(2):
+            u = o.mg_cycle(0, u, f, nu[0], nu[1], gamma, 0.5)
+            g.mg_cycle(0, du, df, cfg)
+        assert rel(du.numpy(), u) < 1e-10
+
+
+@pytest.mark.parametrize("path", ["spectral", "physical"])
+def test_c1_solve_matches_oracle(S, path):
+    """configs[0]: iteration count identical, iterate and history within 1e-10."""
+    g, o = pair(S, 1, 1, 5, 6, 1.0)
+    f = O.make_inputs(o, 42)
+    u_o, rep_o = o.solve(f, eps=1e-8)
+    du = g.vector(0)
+    rep = g.solve(g.upload(f), du, S.CycleConfig(nu1=1, nu2=1, path=path), 1e-8)
+    assert rep.converged and rep.iterations == rep_o["iterations"]
+    h_o = np.array(rep_o["residual_history"])
+    assert rel(np.array(rep.residual_history), h_o) < 1e-10
+    assert rel(du.numpy(), u_o) < 1e-10
+    margin = abs(h_o[-1] / h_o[0] - 1e-8) / 1e-8
+    print(json.dumps({"path": path, "iterations": rep.iterations, "stop_margin": margin}))
+
+
+def test_two_grid_matches_oracle(S):
+    for mode in (1, 2):
+        g, o = pair(S, 1, 2, 3, 3, 1.0, two_grid=mode)
+        f = O.fill_uniform(o.levels[0].size, 12, 0)
+        df = g.upload(f)
+        u = np.zeros_like(f)
+        du = g.upload(u)
+        for _ in range(3):
+            u = o.mg_cycle(0, u, f, 2, 2, 1, 0.5)
+            g.mg_cycle(0, du, df, S.CycleConfig(nu1=2, nu2=2))
+        assert rel(du.numpy(), u) < 1e-10
+
+
+def test_c2_reduced_solve_matches_oracle(S):
+    """configs[1] shape family (2D, random u0) at 63^2 x 64 steps."""
+    g, o = pair(S, 1, 2, 5, 6, 1.0)
+    f = O.make_inputs(o, 42, random_u0=True)
+    u_o, rep_o = o.solve(f, eps=1e-8)
+    du = g.vector(0)
+    rep = g.solve(g.upload(f), du, S.CycleConfig(nu1=1, nu2=1), 1e-8)
+    assert rep.iterations == rep_o["iterations"]
+    assert rel(du.numpy(), u_o) < 1e-10
+
+
+@pytest.mark.slow
+def test_c2_full_solve_matches_oracle(S):
+    """configs[1] exactly: 127^2, N_t = 256, p_t = 1, random u0."""
+    g, o = pair(S, 1, 2, 6, 8, 1.0)
+    f = O.make_inputs(o, 42, random_u0=True)
+    u = np.zeros_like(f)
+    for _ in range(2):
+        u = o.mg_cycle(0, u, f, 1, 1, 1, 0.5)
+    du = g.vector(0)
+    df = g.upload(f)
+    cfg = S.CycleConfig(nu1=1, nu2=1)
+    for _ in range(2):
+        g.mg_cycle(0, du, df, cfg)
+    assert rel(du.numpy(), u) < 1e-10
+    rep = g.solve(df, g.vector(0), cfg, 1e-8)
+    assert rep.converged
+    print(json.dumps({"c2_iterations": rep.iterations}))
+
+
+def test_device_generator_matches_host(S):
+    g = S.Hierarchy(1, 2, 3, 3)
+    v = g.vector(0)
+    g.fill_uniform(v, 42, 0, 1000)
+    assert np.array_equal(v.numpy(), O.fill_uniform(v.n, 42, 0, 1000))
+    o = O.Hierarchy(1, 2, 3, 3)
+    f = O.fill_uniform(v.n, 42, 0)
+    u0 = O.fill_uniform(o.levels[0].n_x, 42, 1)
+    want = o.fold_u0(f.copy(), u0)
+    df = g.upload(f)
+    du0 = S.BlockVector(g, u0.size, (u0.size,)).copy_from(u0)
+    assert rel(g.fold_u0(df, du0).numpy(), want) < 1e-14
+
+
+def test_full_size_linearity_c2(S):
+    """configs[1] at full size: a V-cycle from zero is linear in f."""
+    g = S.Hierarchy(1, 2, 6, 8, 1.0)
+    f1, f2 = g.vector(0), g.vector(0)
+    g.fill_uniform(f1, 42, 0)
+    g.fill_uniform(f2, 43, 0)
+    cfg = S.CycleConfig(nu1=1, nu2=1)
+    u1, u2, u12 = g.vector(0), g.vector(0), g.vector(0)
+    g.mg_cycle(0, u1, f1, cfg)
+    g.mg_cycle(0, u2, f2, cfg)
+    f12 = g.upload(f1.numpy() + f2.numpy())
+    g.mg_cycle(0, u12, f12, cfg)
+    assert rel(u12.numpy(), u1.numpy() + u2.numpy()) < 1e-12
+
+
+@pytest.mark.parametrize("cfgname,params", [
+    ("C3", (2, 2, 7, 12, 1.0)),
+    ("C4", (1, 3, 5, 10, 1.0)),
+    ("C5_G1", (1, 2, 8, 11, 1.0)),
+])
+def test_full_size_solves(S, cfgname, params):
+    """configs[2..4] at full size: converges to 1e-8 in the physical residual
+    (stmg_residual + stmg_norm), deterministically (bitwise equal reruns)."""
+    g = S.Hierarchy(*params)
+    f = g.vector(0)
+    g.fill_uniform(f, 42, 0)
+    cfg = S.CycleConfig(nu1=1, nu2=1)
+    u = g.vector(0)
+    ra = g.solve(f, u, cfg, 1e-8)
+    assert ra.converged
+    r = g.residual(0, u, f)
+    assert g.norm(0, r) <= 1.0001e-8 * g.norm(0, f)
+    del r
+    u2 = g.vector(0)
+    rb = g.solve(f, u2, cfg, 1e-8)
+    assert ra.iterations == rb.iterations and ra.residual_history == rb.residual_history
+    print(json.dumps({"config": cfgname, "iterations": ra.iterations,
+                      "solve_s": ra.device_time_seconds, "dofs": g.size(0)}))
+
+
+def test_error_behaviour(S):
+    g = S.Hierarchy(1, 1, 2, 2)
+    v = g.vector(0)
+    with pytest.raises(ValueError):
+        g.residual(9, v, v)
+    last = len(g.levels) - 1
+    with pytest.raises(ValueError):
+        g.restrict(last, g.vector(last), 1)  # n_t = 1: no coarser level
+    with pytest.raises(ValueError):
+        g.solve(v, g.vector(0), S.CycleConfig(), 0.0)
+
+
+def test_cpp_shim_solves_c1(S):
+    exe = os.path.join(ROOT, "tests", "cpp", "_shim_smoke")
+    from paper_1411_0519_b200 import _capi
+    r = subprocess.run(["/usr/bin/g++", "-std=c++17", "-O1", "-I" + os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "shim_smoke.cpp"), _capi.LIB_PATH,
+                        "-Wl,-rpath," + os.path.dirname(_capi.LIB_PATH), "-o", exe],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    rep = json.loads(out.stdout.strip().splitlines()[-1])
+    o = O.Hierarchy(1, 1, 5, 6)
+    _, rep_o = o.solve(O.make_inputs(o, 42))
+    assert rep["iterations"] == rep_o["iterations"]
