@@ -142,16 +142,21 @@ class Hierarchy:
             pass
 
     # ---- vectors ----------------------------------------------------------
+    def _lev(self, level: int) -> dict:
+        if not 0 <= level < len(self.levels):
+            raise ValueError("level index out of range")
+        return self.levels[level]
+
     def size(self, level: int = 0) -> int:
-        L = self.levels[level]
+        L = self._lev(level)
         return L["n_t"] * L["n_loc"] * L["n_x"]
 
     def vector(self, level: int = 0) -> BlockVector:
-        L = self.levels[level]
+        L = self._lev(level)
         return BlockVector(self, self.size(level), (L["n_t"], L["n_loc"], L["n_x"]))
 
     def coarse_vector(self, level: int, mode: int = 0) -> BlockVector:
-        L = self.levels[level]
+        L = self._lev(level)
         mode = mode or L["coarsen_to_next"]
         n1 = L["n1"] if mode == COARSEN_SEMI else (L["n1"] - 1) // 2
         nx = n1 ** L["dim"]
