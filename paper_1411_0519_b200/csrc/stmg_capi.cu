@@ -141,6 +141,12 @@ struct stmg_ctx {
   bool capturing = false;
   i64 captured_kernels = 0;
   cudaEvent_t ev_solve[2] = {nullptr, nullptr};
+  // single-CTA coarse tail (levels >= tail_start), built on first solve
+  void* tail_table = nullptr;
+  int tail_start = -1;
+  size_t tail_smem = 0;
+  int* d_flag = nullptr;
+  int* h_flag = nullptr;  // pinned
 };
 
 namespace {
@@ -405,6 +411,41 @@ void ensure_spectral(stmg_ctx* c, int from_level) {
   ensure(c->partials, need);
 }
 
+// The suffix of levels whose vectors (f, u, u') fit in one SM's shared
+// memory runs inside the single-CTA tail kernel.
+constexpr i64 kTailSmemBytes = 200 * 1024;
+
+void ensure_tail(stmg_ctx* c) {
+  if (c->tail_table || c->tail_start == 0) return;
+  const int nl = int(c->levels.size());
+  int start = nl;  // first level of the small suffix
+  i64 bytes = 0;
+  while (start - 1 >= 1) {
+    const i64 b = 24 * c->levels[start - 1].view.size();
+    if (bytes + b > kTailSmemBytes || nl - (start - 1) > 32) break;
+    bytes += b;
+    --start;
+  }
+  if (start >= nl) {
+    c->tail_start = 0;  // not even the coarsest fits: per-level path
+    return;
+  }
+  std::vector<stmg::TailSpec> spec(nl - start);
+  for (int l = start; l < nl; ++l) {
+    Level& L = c->levels[l];
+    stmg::TailSpec& t = spec[l - start];
+    t.view = L.view;
+    t.mode = L.spec.coarsen;
+    t.n1c = (l + 1 < nl) ? c->levels[l + 1].spec.n1() : L.spec.n1();
+    t.F = L.F.base;
+    t.U0 = L.U[0].base;
+    t.U1 = L.U[1].base;
+  }
+  CK(stmg::build_tail_table(spec.data(), int(spec.size()), &c->tail_table));
+  c->tail_start = start;
+  c->tail_smem = size_t(bytes);
+}
+
 stmg::ModalArgs modal_args(const Level& L, const Level* C, double omega, bool grouped) {
   stmg::ModalArgs a;
   a.omega = omega;
@@ -455,8 +496,17 @@ void spectral_cycle(stmg_ctx* c, int level, bool zero_guess, const stmg_cycle_co
     count(c);
     cur ^= 1;
   }
-  for (int g = 0; g < std::max(cfg.gamma, 1); ++g)
-    spectral_cycle(c, level + 1, g == 0, cfg, false, nullptr);
+  const bool fused = nu1 == 1 && nu2 == 1 && cfg.gamma == 1;
+  if (fused && c->tail_table && level + 1 == c->tail_start) {
+    CK(stmg::launch_tail(L.spec.dim, L.spec.p_t + 1, c->tail_table,
+                         int(c->levels.size()) - c->tail_start, cfg.omega_t, c->tail_smem,
+                         c->stream));
+    count(c);
+    for (int l = c->tail_start; l < int(c->levels.size()); ++l) c->cur[l] = 0;
+  } else {
+    for (int g = 0; g < std::max(cfg.gamma, 1); ++g)
+      spectral_cycle(c, level + 1, g == 0, cfg, false, nullptr);
+  }
   // prolong + correct + first post-sweep (+ residual norm on the finest level)
   const bool fuse_resid = want_resid && nu2 <= 1;
   {
@@ -577,9 +627,17 @@ void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config
     }
   } else {
     ensure_spectral(c, 0);
+    ensure_tail(c);
     c->cur[0] = 0;
+    // a zero initial guess (the usual case) needs no transform
+    CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+    CK(stmg::launch_nonzero(u, L0.view.size(), c->d_flag, c->stream));
+    count(c);
+    CK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     dst_all(c, L0, f, L0.F.base);
-    dst_all(c, L0, u, L0.U[0].base);
+    CK(cudaStreamSynchronize(c->stream));
+    if (*c->h_flag) dst_all(c, L0, u, L0.U[0].base);
+    else CK(cudaMemsetAsync(L0.U[0].base, 0, size_t(L0.view.size()) * sizeof(double), c->stream));
     const double r0 = spectral_resnorm(c, 0);
     r.r0 = r.r_final = r0;
     push(r0);
@@ -671,6 +729,8 @@ int stmg_create(const stmg_hierarchy_params* p, stmg_ctx** out) {
     }
     CK(cudaMalloc(&c->d_norm, sizeof(double)));
     CK(cudaMallocHost(&c->h_norm, sizeof(double)));
+    CK(cudaMalloc(&c->d_flag, sizeof(int)));
+    CK(cudaMallocHost(&c->h_flag, sizeof(int)));
     CK(cudaEventCreate(&c->ev_solve[0]));
     CK(cudaEventCreate(&c->ev_solve[1]));
     for (auto& s : c->prof) {
@@ -708,6 +768,9 @@ int stmg_destroy(stmg_ctx* c) {
     cudaEventDestroy(c->ev_solve[1]);
     cudaFree(c->d_norm);
     cudaFree(c->d_hist);
+    cudaFree(c->d_flag);
+    cudaFreeHost(c->h_flag);
+    if (c->tail_table) cudaFree(c->tail_table);
     cudaFreeHost(c->h_norm);
     cudaStreamDestroy(c->stream);
     delete c;
@@ -906,7 +969,8 @@ int stmg_mg_cycle(stmg_ctx* c, int level, double* u, const double* f,
       phys_cycle(c, level, u, f, *cfg);
       return;
     }
-    ensure_spectral(c, level);
+    ensure_spectral(c, 0);
+    ensure_tail(c);
     c->cur[level] = 0;
     dst_all(c, L, f, L.F.base);
     dst_all(c, L, u, L.U[0].base);

@@ -16,8 +16,10 @@
 //
 // All arithmetic is FP64.  Indexing is 64-bit (level vectors exceed 2^31).
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <vector>
 
 #include "stmg_launch.hpp"
 
@@ -263,33 +265,44 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 // Sum over the 2^DIM lanes of an alias group.
 template <int DIM>
 __device__ __forceinline__ double group_sum(double v) {
+  constexpr unsigned gm = (1u << (1 << DIM)) - 1u;
+  const unsigned mask = gm << ((threadIdx.x & 31) & ~((1 << DIM) - 1));
 #pragma unroll
-  for (int o = 1; o < (1 << DIM); o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = 1; o < (1 << DIM); o <<= 1) v += __shfl_xor_sync(mask, v, o);
   return v;
 }
 
 // ==================================================== fused spectral kernels
-// k_down: one damped block-Jacobi sweep, the residual of the smoothed iterate
-// and its restriction, for a chunk [n0, n0+C) of time steps of one mode.  The
+// Loads: the standalone kernels read through the read-only / streaming paths;
+// the single-CTA tail kernel reads data written earlier in the same launch
+// (in shared memory), so it uses plain generic loads (COH).
+template <bool COH, int NL>
+__device__ __forceinline__ void ld_ro(const double* p, i64 nx, double (&v)[NL]) {
+#pragma unroll
+  for (int l = 0; l < NL; ++l) v[l] = COH ? p[l * nx] : __ldg(p + l * nx);
+}
+template <bool COH, int NL>
+__device__ __forceinline__ void ld_st(const double* p, i64 nx, double (&v)[NL]) {
+#pragma unroll
+  for (int l = 0; l < NL; ++l) v[l] = COH ? p[l * nx] : __ldcs(p + l * nx);
+}
+
+// down: one damped block-Jacobi sweep, the residual of the smoothed iterate
+// and its restriction, for steps [n0, nend) of one mode (lane `tid`).  The
 // Jacobi sweep uses the frozen old iterate of step n-1 (smoother.cpp:101-104):
 //   u'_n = (1-w) u_n + w A_j^-1 (f_n + M_j N u_{n-1}),
 // the residual r_n = f_n - A_j u'_n + M_j N u'_{n-1}, and the restriction
 // c_{n/2} += fac * R_{1|2} r_n summed over the alias group (transfer.cpp:75-85,
-// 138-149 in the sine basis).
-template <int DIM, int NL, bool ZERO, int CO>
-__global__ void __launch_bounds__(256) k_down(const double* __restrict__ f,
-                                              const double* __restrict__ uin,
-                                              double* __restrict__ uout,
-                                              double* __restrict__ fc, const TM<NL> t,
-                                              const SP s, const i64 n_t, const int C,
-                                              const i64 n1c, const double omega,
-                                              const bool first_global) {
-  const i64 tid = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+// 138-149 in the sine basis).  has_prev: step n0-1 exists (warm-up).
+template <int DIM, int NL, bool ZERO, int CO, bool COH>
+__device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64 nend,
+                                          const double* f, const double* uin, double* uout,
+                                          double* fc, const TM<NL>& t, const SP& s,
+                                          const i64 n1c, const double omega, const bool has_prev,
+                                          const bool has_prev2) {
   const Member me = make_member<DIM>(s, tid, n1c, CO == 2);
   const i64 nx = s.nx, slab = NL * nx;
   const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
-  const i64 n0 = i64(blockIdx.y) * C;
-  const i64 nend = min(n0 + i64(C), n_t);
   const double om1 = 1.0 - omega;
   const double Mj = me.Mj, Kj = me.Kj;
   const double* fp = f + me.idx;
@@ -300,19 +313,19 @@ __global__ void __launch_bounds__(256) k_down(const double* __restrict__ f,
 #pragma unroll
   for (int l = 0; l < NL; ++l) uo[l] = un[l] = 0.0;
 
-  if (me.ok && (n0 > 0 || !first_global)) {  // warm-up: smoothed step n0-1
+  if (me.ok && has_prev) {  // warm-up: smoothed step n0-1
     double fv[NL], x[NL];
-    load_nl<NL>(fp + (n0 - 1) * slab, nx, fv);
+    ld_ro<COH, NL>(fp + (n0 - 1) * slab, nx, fv);
     if (ZERO) {
       solve_mode<NL>(t, Mj, Kj, fv, x);
 #pragma unroll
       for (int l = 0; l < NL; ++l) un[l] = omega * x[l];
     } else {
       double u1[NL], u2[NL], nv[NL];
-      load_nl<NL>(up + (n0 - 1) * slab, nx, u1);
+      ld_ro<COH, NL>(up + (n0 - 1) * slab, nx, u1);
 #pragma unroll
       for (int l = 0; l < NL; ++l) u2[l] = 0.0;
-      if (n0 - 1 > 0 || !first_global) load_nl<NL>(up + (n0 - 2) * slab, nx, u2);
+      if (has_prev2) ld_ro<COH, NL>(up + (n0 - 2) * slab, nx, u2);
       matvec<NL>(t.N, u2, nv);
 #pragma unroll
       for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
@@ -329,40 +342,47 @@ __global__ void __launch_bounds__(256) k_down(const double* __restrict__ f,
     double acc[NL];
 #pragma unroll
     for (int l = 0; l < NL; ++l) acc[l] = 0.0;
+    // issue all loads of the step pair up front (memory-level parallelism)
+    double f2[2][NL], u2[2][NL];
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int l = 0; l < NL; ++l) f2[e][l] = u2[e][l] = 0.0;
+    if (me.ok) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        ld_st<COH, NL>(fp + (n + e) * slab, nx, f2[e]);
+        if (!ZERO) ld_st<COH, NL>(up + (n + e) * slab, nx, u2[e]);
+      }
+    }
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const i64 m = n + e;
-      double fv[NL], uv[NL], rhs[NL], x[NL], w[NL];
-#pragma unroll
-      for (int l = 0; l < NL; ++l) fv[l] = uv[l] = 0.0;
-      if (me.ok) {
-        load_nl_cs<NL>(fp + m * slab, nx, fv);
-        if (!ZERO) load_nl_cs<NL>(up + m * slab, nx, uv);
-      }
+      double rhs[NL], x[NL], w[NL];
       if (!ZERO) {
         double nv[NL];
         matvec<NL>(t.N, uo, nv);
 #pragma unroll
-        for (int l = 0; l < NL; ++l) rhs[l] = fv[l] + Mj * nv[l];
+        for (int l = 0; l < NL; ++l) rhs[l] = f2[e][l] + Mj * nv[l];
       } else {
 #pragma unroll
-        for (int l = 0; l < NL; ++l) rhs[l] = fv[l];
+        for (int l = 0; l < NL; ++l) rhs[l] = f2[e][l];
       }
       solve_mode<NL>(t, Mj, Kj, rhs, x);
 #pragma unroll
-      for (int l = 0; l < NL; ++l) w[l] = ZERO ? omega * x[l] : om1 * uv[l] + omega * x[l];
+      for (int l = 0; l < NL; ++l) w[l] = ZERO ? omega * x[l] : om1 * u2[e][l] + omega * x[l];
       if (me.ok) store_nl<NL>(op + m * slab, nx, w);
       double aw[NL], np[NL], res[NL], rt[NL];
       apply_mode<NL>(t, Mj, Kj, w, aw);
       matvec<NL>(t.N, un, np);
 #pragma unroll
-      for (int l = 0; l < NL; ++l) res[l] = fv[l] - aw[l] + Mj * np[l];
+      for (int l = 0; l < NL; ++l) res[l] = f2[e][l] - aw[l] + Mj * np[l];
       if (e == 0) matvec<NL>(t.R1, res, rt);
       else matvec<NL>(t.R2, res, rt);
 #pragma unroll
       for (int l = 0; l < NL; ++l) {
         acc[l] += (CO == 2) ? me.fac * rt[l] : rt[l];
-        if (!ZERO) uo[l] = uv[l];
+        if (!ZERO) uo[l] = u2[e][l];
         un[l] = w[l];
       }
     }
@@ -370,17 +390,151 @@ __global__ void __launch_bounds__(256) k_down(const double* __restrict__ f,
     if (CO == 2) {
 #pragma unroll
       for (int l = 0; l < NL; ++l) acc[l] = group_sum<DIM>(me.ok ? acc[l] : 0.0);
-      if (me.cok && (threadIdx.x & ((1 << DIM) - 1)) == 0)
-        store_nl<NL>(fc + nc * cslab + me.cidx, nxc, acc);
+      if (me.cok && (tid & ((1 << DIM) - 1)) == 0) store_nl<NL>(fc + nc * cslab + me.cidx, nxc, acc);
     } else if (me.ok) {
       store_nl<NL>(fc + nc * cslab + me.idx, nxc, acc);
     }
   }
 }
 
-// k_up: u <- u + P e_c (mg.cpp:123-127), then one damped block-Jacobi sweep
-// (mg.cpp:129-131); with RESID also the residual of the result and its sum of
-// squares per (chunk, block) for the stop test (mg.cpp:152-153).
+// up: u <- u + P e_c (mg.cpp:123-127), then one damped block-Jacobi sweep
+// (mg.cpp:129-131); with RESID also the residual of the result, returning its
+// sum of squares (stop test, mg.cpp:152-153).
+template <int DIM, int NL, int CO, bool RESID, bool COH>
+__device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64 nend,
+                                          const double* ec, const double* uin, const double* f,
+                                          double* uout, const TM<NL>& t, const SP& s,
+                                          const i64 n1c, const double omega, const bool has_prev,
+                                          const bool has_prev2) {
+  const Member me = make_member<DIM>(s, tid, n1c, CO == 2);
+  const i64 nx = s.nx, slab = NL * nx;
+  const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
+  const double om1 = 1.0 - omega;
+  const double Mj = me.Mj, Kj = me.Kj;
+  const double fac = (CO == 2) ? me.fac : 1.0;
+  const bool has_c = (CO == 2) ? me.cok : me.ok;
+  const double* ep = ec + ((CO == 2) ? me.cidx : me.idx);
+  const double* fp = f + me.idx;
+  const double* up = uin + me.idx;
+  double* op = uout + me.idx;
+  double sumsq = 0.0;
+  if (!me.ok) return 0.0;
+
+  double vo[NL], wp[NL], ev[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) vo[l] = wp[l] = ev[l] = 0.0;
+
+  if (has_prev) {
+    if (has_c) ld_ro<COH, NL>(ep + ((n0 >> 1) - 1) * cslab, nxc, ev);  // coarse step of n0-2, n0-1
+    double u1[NL], c1[NL];
+    ld_ro<COH, NL>(up + (n0 - 1) * slab, nx, u1);
+    matvec_t<NL>(t.R2, ev, c1);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) vo[l] = u1[l] + fac * c1[l];
+    if (RESID) {
+      double v2[NL], fv[NL], nv[NL], x[NL];
+#pragma unroll
+      for (int l = 0; l < NL; ++l) v2[l] = 0.0;
+      if (has_prev2) {
+        double u2[NL], c2[NL];
+        ld_ro<COH, NL>(up + (n0 - 2) * slab, nx, u2);
+        matvec_t<NL>(t.R1, ev, c2);
+#pragma unroll
+        for (int l = 0; l < NL; ++l) v2[l] = u2[l] + fac * c2[l];
+      }
+      ld_ro<COH, NL>(fp + (n0 - 1) * slab, nx, fv);
+      matvec<NL>(t.N, v2, nv);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
+      solve_mode<NL>(t, Mj, Kj, fv, x);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) wp[l] = om1 * vo[l] + omega * x[l];
+    }
+  }
+
+  for (i64 n = n0; n < nend; n += 2) {
+    if (has_c) ld_ro<COH, NL>(ep + (n >> 1) * cslab, nxc, ev);
+    double u2[2][NL], f2[2][NL];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      ld_st<COH, NL>(up + (n + e) * slab, nx, u2[e]);
+      ld_st<COH, NL>(fp + (n + e) * slab, nx, f2[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const i64 m = n + e;
+      double c[NL], v[NL], nv[NL], rhs[NL], x[NL], w[NL];
+      if (e == 0) matvec_t<NL>(t.R1, ev, c);
+      else matvec_t<NL>(t.R2, ev, c);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) v[l] = u2[e][l] + fac * c[l];
+      matvec<NL>(t.N, vo, nv);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) rhs[l] = f2[e][l] + Mj * nv[l];
+      solve_mode<NL>(t, Mj, Kj, rhs, x);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) w[l] = om1 * v[l] + omega * x[l];
+      store_nl<NL>(op + m * slab, nx, w);
+      if (RESID) {
+        double aw[NL], np[NL];
+        apply_mode<NL>(t, Mj, Kj, w, aw);
+        matvec<NL>(t.N, wp, np);
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          const double r = f2[e][l] - aw[l] + Mj * np[l];
+          sumsq += r * r;
+        }
+      }
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        vo[l] = v[l];
+        wp[l] = w[l];
+      }
+    }
+  }
+  return sumsq;
+}
+
+// Per-mode forward substitution u_n = A_j^-1 (f_n + M_j N u_{n-1})
+// (st_system.cpp:118-130 in the sine basis).
+template <int DIM, int NL, bool COH>
+__device__ __forceinline__ void fwdsub_body(const i64 r, const double* f, double* u,
+                                            const TM<NL>& t, const SP& s, const i64 n_t) {
+  if (r >= s.nx) return;
+  double Mj, Kj;
+  mode_eig<DIM>(s, r, Mj, Kj);
+  const i64 nx = s.nx, slab = NL * nx;
+  double prev[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) prev[l] = 0.0;
+  for (i64 m = 0; m < n_t; ++m) {
+    double fv[NL], nv[NL], x[NL];
+    ld_ro<COH, NL>(f + m * slab + r, nx, fv);
+    matvec<NL>(t.N, prev, nv);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
+    solve_mode<NL>(t, Mj, Kj, fv, x);
+    store_nl<NL>(u + m * slab + r, nx, x);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) prev[l] = x[l];
+  }
+}
+
+template <int DIM, int NL, bool ZERO, int CO>
+__global__ void __launch_bounds__(256) k_down(const double* __restrict__ f,
+                                              const double* __restrict__ uin,
+                                              double* __restrict__ uout,
+                                              double* __restrict__ fc, const TM<NL> t,
+                                              const SP s, const i64 n_t, const int C,
+                                              const i64 n1c, const double omega,
+                                              const bool first_global) {
+  const i64 tid = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 n0 = i64(blockIdx.y) * C;
+  const i64 nend = min(n0 + i64(C), n_t);
+  down_body<DIM, NL, ZERO, CO, false>(tid, n0, nend, f, uin, uout, fc, t, s, n1c, omega,
+                                      n0 > 0 || !first_global, n0 - 1 > 0 || !first_global);
+}
+
 template <int DIM, int NL, int CO, bool RESID>
 __global__ void __launch_bounds__(256) k_up(const double* __restrict__ ec,
                                             const double* __restrict__ uin,
@@ -392,96 +546,119 @@ __global__ void __launch_bounds__(256) k_up(const double* __restrict__ ec,
                                             const bool first_global) {
   __shared__ double sh[32];
   const i64 tid = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  const Member me = make_member<DIM>(s, tid, n1c, CO == 2);
-  const i64 nx = s.nx, slab = NL * nx;
-  const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
   const i64 n0 = i64(blockIdx.y) * C;
   const i64 nend = min(n0 + i64(C), n_t);
-  const double om1 = 1.0 - omega;
-  const double Mj = me.Mj, Kj = me.Kj;
-  const double fac = (CO == 2) ? me.fac : 1.0;
-  const bool has_c = (CO == 2) ? me.cok : me.ok;
-  const double* ep = ec + ((CO == 2) ? me.cidx : me.idx);
-  const double* fp = f + me.idx;
-  const double* up = uin + me.idx;
-  double* op = uout + me.idx;
-  double sumsq = 0.0;
-
-  if (me.ok) {
-    double vo[NL], wp[NL], ev[NL];
-#pragma unroll
-    for (int l = 0; l < NL; ++l) vo[l] = wp[l] = ev[l] = 0.0;
-
-    if (n0 > 0 || !first_global) {
-      if (has_c) load_nl<NL>(ep + ((n0 >> 1) - 1) * cslab, nxc, ev);  // coarse step of n0-2, n0-1
-      double u1[NL], c1[NL];
-      load_nl<NL>(up + (n0 - 1) * slab, nx, u1);
-      matvec_t<NL>(t.R2, ev, c1);
-#pragma unroll
-      for (int l = 0; l < NL; ++l) vo[l] = u1[l] + fac * c1[l];
-      if (RESID) {
-        double v2[NL], fv[NL], nv[NL], x[NL];
-#pragma unroll
-        for (int l = 0; l < NL; ++l) v2[l] = 0.0;
-        if (n0 - 1 > 0 || !first_global) {
-          double u2[NL], c2[NL];
-          load_nl<NL>(up + (n0 - 2) * slab, nx, u2);
-          matvec_t<NL>(t.R1, ev, c2);
-#pragma unroll
-          for (int l = 0; l < NL; ++l) v2[l] = u2[l] + fac * c2[l];
-        }
-        load_nl<NL>(fp + (n0 - 1) * slab, nx, fv);
-        matvec<NL>(t.N, v2, nv);
-#pragma unroll
-        for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
-        solve_mode<NL>(t, Mj, Kj, fv, x);
-#pragma unroll
-        for (int l = 0; l < NL; ++l) wp[l] = om1 * vo[l] + omega * x[l];
-      }
-    }
-
-    for (i64 n = n0; n < nend; n += 2) {
-      if (has_c) load_nl<NL>(ep + (n >> 1) * cslab, nxc, ev);
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const i64 m = n + e;
-        double uv[NL], fv[NL], c[NL], v[NL], nv[NL], rhs[NL], x[NL], w[NL];
-        load_nl_cs<NL>(up + m * slab, nx, uv);
-        load_nl_cs<NL>(fp + m * slab, nx, fv);
-        if (e == 0) matvec_t<NL>(t.R1, ev, c);
-        else matvec_t<NL>(t.R2, ev, c);
-#pragma unroll
-        for (int l = 0; l < NL; ++l) v[l] = uv[l] + fac * c[l];
-        matvec<NL>(t.N, vo, nv);
-#pragma unroll
-        for (int l = 0; l < NL; ++l) rhs[l] = fv[l] + Mj * nv[l];
-        solve_mode<NL>(t, Mj, Kj, rhs, x);
-#pragma unroll
-        for (int l = 0; l < NL; ++l) w[l] = om1 * v[l] + omega * x[l];
-        store_nl<NL>(op + m * slab, nx, w);
-        if (RESID) {
-          double aw[NL], np[NL];
-          apply_mode<NL>(t, Mj, Kj, w, aw);
-          matvec<NL>(t.N, wp, np);
-#pragma unroll
-          for (int l = 0; l < NL; ++l) {
-            const double r = fv[l] - aw[l] + Mj * np[l];
-            sumsq += r * r;
-          }
-        }
-#pragma unroll
-        for (int l = 0; l < NL; ++l) {
-          vo[l] = v[l];
-          wp[l] = w[l];
-        }
-      }
-    }
-  }
+  const double sumsq = up_body<DIM, NL, CO, RESID, false>(
+      tid, n0, nend, ec, uin, f, uout, t, s, n1c, omega, n0 > 0 || !first_global,
+      n0 - 1 > 0 || !first_global);
   if (RESID) {
     const double tot = block_sum(sumsq, sh);
     if (threadIdx.x == 0) partials[i64(blockIdx.y) * gridDim.x + blockIdx.x] = tot;
   }
 }
+
+// Coarse-level tail: all levels of the V-cycle from the first "small" level
+// down to the coarsest and back, in ONE thread block with every vector in
+// shared memory (the levels are tiny; a launch per level, or time-marching
+// through L2, would dominate).  Zero initial guess on entry (mg.cpp:119),
+// V(1,1), gamma = 1.  Work items are (mode lane, time chunk); the lanes of an
+// alias group always share a chunk.  In: F of the first tail level (global);
+// out: its corrected iterate U0 (global), as the per-level path leaves it.
+template <int NL>
+struct TailLevel {
+  TM<NL> t;
+  SP s;
+  i64 n_t;
+  i64 n1c;
+  int mode;  // coarsening to the next level (0 on the coarsest)
+  double* F;
+  double* U0;
+  double* U1;
+};
+
+constexpr int kTailMaxLevels = 32;
+
+template <int DIM, int NL>
+__global__ void __launch_bounds__(1024) k_tail(const TailLevel<NL>* __restrict__ lv,
+                                               const int nlev, const double omega) {
+  extern __shared__ double smem[];
+  __shared__ TailLevel<NL> A, B;
+  __shared__ i64 off[kTailMaxLevels + 1];
+  const int T = blockDim.x;
+  if (threadIdx.x == 0) {
+    off[0] = 0;
+    for (int k = 0; k < nlev; ++k) off[k + 1] = off[k] + 3 * lv[k].n_t * NL * lv[k].s.nx;
+  }
+  __syncthreads();
+  auto load_level = [&](TailLevel<NL>& D, int k) {
+    D = lv[k];
+    const i64 sz = D.n_t * NL * D.s.nx;
+    D.F = smem + off[k];
+    D.U0 = D.F + sz;
+    D.U1 = D.U0 + sz;
+  };
+  {  // stage the first level's rhs
+    const i64 sz = lv[0].n_t * NL * lv[0].s.nx;
+    const double* g = lv[0].F;
+    for (i64 i = threadIdx.x; i < sz; i += T) smem[i] = g[i];
+  }
+  for (int k = 0; k + 1 < nlev; ++k) {
+    if (threadIdx.x == 0) {
+      load_level(A, k);
+      load_level(B, k + 1);
+    }
+    __syncthreads();
+    const i64 lanes = ipow(A.s.G, DIM) << DIM;
+    i64 C = 2;
+    while (C < A.n_t && lanes * (A.n_t / C) > T) C *= 2;
+    const i64 items = lanes * ((A.n_t + C - 1) / C);
+    const i64 rounded = (items + T - 1) / T * T;
+    for (i64 it = threadIdx.x; it < rounded; it += T) {
+      const i64 lane = it % lanes, n0 = (it / lanes) * C;
+      if (n0 >= A.n_t) continue;  // whole alias groups skip together
+      const i64 nend = min(n0 + C, A.n_t);
+      if (A.mode == 2)
+        down_body<DIM, NL, true, 2, true>(lane, n0, nend, A.F, A.U1, A.U1, B.F, A.t, A.s, A.n1c,
+                                          omega, n0 > 0, n0 - 1 > 0);
+      else
+        down_body<DIM, NL, true, 1, true>(lane, n0, nend, A.F, A.U1, A.U1, B.F, A.t, A.s, A.s.n1,
+                                          omega, n0 > 0, n0 - 1 > 0);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) load_level(A, nlev - 1);
+  __syncthreads();
+  for (i64 r = threadIdx.x; r < A.s.nx; r += T) fwdsub_body<DIM, NL, true>(r, A.F, A.U0, A.t, A.s, A.n_t);
+  __syncthreads();
+  for (int k = nlev - 2; k >= 0; --k) {
+    if (threadIdx.x == 0) {
+      load_level(A, k);
+      load_level(B, k + 1);
+    }
+    __syncthreads();
+    const i64 lanes = ipow(A.s.G, DIM) << DIM;
+    i64 C = 2;
+    while (C < A.n_t && lanes * (A.n_t / C) > T) C *= 2;
+    const i64 items = lanes * ((A.n_t + C - 1) / C);
+    for (i64 it = threadIdx.x; it < items; it += T) {
+      const i64 lane = it % lanes, n0 = (it / lanes) * C;
+      const i64 nend = min(n0 + C, A.n_t);
+      if (A.mode == 2)
+        up_body<DIM, NL, 2, false, true>(lane, n0, nend, B.U0, A.U1, A.F, A.U0, A.t, A.s, A.n1c,
+                                         omega, n0 > 0, n0 - 1 > 0);
+      else
+        up_body<DIM, NL, 1, false, true>(lane, n0, nend, B.U0, A.U1, A.F, A.U0, A.t, A.s, A.s.n1,
+                                         omega, n0 > 0, n0 - 1 > 0);
+    }
+    __syncthreads();
+  }
+  {  // hand the first level's iterate back
+    const i64 sz = lv[0].n_t * NL * lv[0].s.nx;
+    double* g = lv[0].U0;
+    for (i64 i = threadIdx.x; i < sz; i += T) g[i] = smem[sz + i];
+  }
+}
+
 // Plain damped block-Jacobi sweep per mode (ping-pong: u_out != u_in).
 template <int DIM, int NL, bool ZERO>
 __global__ void __launch_bounds__(128) k_smooth(const double* __restrict__ f,
@@ -557,31 +734,12 @@ __global__ void __launch_bounds__(128) k_resnorm(const double* __restrict__ u,
   if (threadIdx.x == 0) partials[i64(blockIdx.y) * gridDim.x + blockIdx.x] = tot;
 }
 
-// Per-mode forward substitution u_n = A_j^-1 (f_n + M_j N u_{n-1})
-// (st_system.cpp:118-130 in the sine basis).
 template <int DIM, int NL>
 __global__ void __launch_bounds__(128) k_fwdsub(const double* __restrict__ f,
                                                 double* __restrict__ u, const TM<NL> t,
                                                 const SP s, const i64 n_t) {
   const i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= s.nx) return;
-  double Mj, Kj;
-  mode_eig<DIM>(s, r, Mj, Kj);
-  const i64 nx = s.nx, slab = NL * nx;
-  double prev[NL];
-#pragma unroll
-  for (int l = 0; l < NL; ++l) prev[l] = 0.0;
-  for (i64 m = 0; m < n_t; ++m) {
-    double fv[NL], nv[NL], x[NL];
-    load_nl<NL>(f + m * slab + r, nx, fv);
-    matvec<NL>(t.N, prev, nv);
-#pragma unroll
-    for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
-    solve_mode<NL>(t, Mj, Kj, fv, x);
-    store_nl<NL>(u + m * slab + r, nx, x);
-#pragma unroll
-    for (int l = 0; l < NL; ++l) prev[l] = x[l];
-  }
+  fwdsub_body<DIM, NL, false>(r, f, u, t, s, n_t);
 }
 
 // Per-mode exact block solve in place.
@@ -828,11 +986,128 @@ __global__ void k_fold_u0(double* __restrict__ f, const double* __restrict__ u0,
 }
 
 // ================================================================ DST-I
-// Orthonormal DST-I of length n1 = N-1 (N = 2^LOG2N) along one axis, two real
-// lines per complex FFT of length 2N: z = a + i b, odd extension; then
-// Z_k = -2i A_k + 2 B_k, so A_k = -Im Z_k / 2, B_k = Re Z_k / 2.
+// Orthonormal DST-I of length n1 = N-1 (N = 2^LOG2N) along one axis.  Two
+// real lines a, b are packed into one complex sequence z = a + i b, oddly
+// extended to length L = 2N (z_0 = z_N = 0, z_{L-j} = -z_j); its DFT is
+// Z_k = -2i A_k + 2 B_k, so A_k = -Im Z_k / 2 and B_k = Re Z_k / 2.
+// The FFT is a Stockham autosort with register-resident radix-16 passes
+// (smem ping-pong between passes, padded against bank conflicts).
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// exp(-2 pi i k / 16), k in [0, 16)
+__device__ __forceinline__ double2 w16(int k) {
+  constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
+  constexpr double r2 = 0.70710678118654752440;
+  switch (k & 15) {
+    case 0: return make_double2(1.0, 0.0);
+    case 1: return make_double2(c1, -s1);
+    case 2: return make_double2(r2, -r2);
+    case 3: return make_double2(s1, -c1);
+    case 4: return make_double2(0.0, -1.0);
+    case 5: return make_double2(-s1, -c1);
+    case 6: return make_double2(-r2, -r2);
+    case 7: return make_double2(-c1, -s1);
+    case 8: return make_double2(-1.0, 0.0);
+    case 9: return make_double2(-c1, s1);
+    case 10: return make_double2(-r2, r2);
+    case 11: return make_double2(-s1, c1);
+    case 12: return make_double2(0.0, 1.0);
+    case 13: return make_double2(s1, c1);
+    case 14: return make_double2(r2, r2);
+    default: return make_double2(c1, s1);
+  }
+}
+
+// In-register radix-R DFT (R = 2, 4, 8, 16), natural order in and out.
+template <int R>
+struct RegFFT {
+  static __device__ __forceinline__ void run(double2 (&v)[R]) {
+    double2 e[R / 2], o[R / 2];
+#pragma unroll
+    for (int k = 0; k < R / 2; ++k) {
+      e[k] = v[2 * k];
+      o[k] = v[2 * k + 1];
+    }
+    RegFFT<R / 2>::run(e);
+    RegFFT<R / 2>::run(o);
+#pragma unroll
+    for (int k = 0; k < R / 2; ++k) {
+      const double2 t = (k == 0) ? o[k] : cmul(w16(k * (16 / R)), o[k]);
+      v[k] = make_double2(e[k].x + t.x, e[k].y + t.y);
+      v[k + R / 2] = make_double2(e[k].x - t.x, e[k].y - t.y);
+    }
+  }
+};
+template <>
+struct RegFFT<1> {
+  static __device__ __forceinline__ void run(double2 (&)[1]) {}
+};
+
+__host__ __device__ constexpr int dst_pass_radix(int m, int p) {
+  // radix-16 passes while >= 4 bits remain, then the remainder
+  return (m - 4 * p) >= 4 ? 16 : (1 << (m - 4 * p));
+}
+__host__ __device__ constexpr int dst_num_passes(int m) { return (m + 3) / 4; }
+__host__ __device__ constexpr int dst_pad(int i) { return i + (i >> 4); }
+
+template <int L, int F, int R>
+__device__ __forceinline__ void stockham_pass(const double2* __restrict__ src,
+                                              double2* __restrict__ dst, int Ns,
+                                              const double2* __restrict__ tw) {
+  constexpr int NJ = L / R;
+  constexpr int BUF = L + L / 16;
+  for (int w = threadIdx.x; w < F * NJ; w += blockDim.x) {
+    const int f = w / NJ, j = w - f * NJ;
+    const double2* X = src + f * BUF;
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = X[dst_pad(j + r * NJ)];
+    if (Ns > 1) {
+      const int jm = j % Ns;
+      const int step = jm * (L / (Ns * R));
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const int idx = (r * step) & (L - 1);
+        double2 w = __ldg(tw + (idx & (L / 2 - 1)));
+        if (idx >= L / 2) w = make_double2(-w.x, -w.y);
+        v[r] = cmul(v[r], w);
+      }
+    }
+    RegFFT<R>::run(v);
+    const int idxD = (j / Ns) * Ns * R + (j % Ns);
+    double2* Y = dst + f * BUF;
+#pragma unroll
+    for (int r = 0; r < R; ++r) Y[dst_pad(idxD + r * Ns)] = v[r];
+  }
+}
+
+template <int LOG2N>
+struct DSTShape {
+  static constexpr int N = 1 << LOG2N;
+  static constexpr int n1 = N - 1;
+  static constexpr int M = LOG2N + 1;
+  static constexpr int L = 1 << M;
+  static constexpr int F = (2048 / L) > 0 ? (2048 / L) : 1;  // FFTs per block
+  static constexpr int TL = 2 * F;                            // lines per block
+  static constexpr int BUF = L + L / 16;
+  static constexpr size_t smem = size_t(2) * F * BUF * sizeof(double2);
+};
+
+// Runs passes P.. of the Stockham FFT; returns the buffer holding the result.
+template <int LOG2N, int P>
+__device__ __forceinline__ const double2* dst_passes(double2* src, double2* dst, int Ns,
+                                                     const double2* __restrict__ tw) {
+  using S = DSTShape<LOG2N>;
+  if constexpr (P >= dst_num_passes(S::M)) {
+    return src;
+  } else {
+    constexpr int R = dst_pass_radix(S::M, P);
+    stockham_pass<S::L, S::F, R>(src, dst, Ns, tw);
+    __syncthreads();
+    return dst_passes<LOG2N, P + 1>(dst, src, Ns * R, tw);
+  }
 }
 
 template <int LOG2N>
@@ -840,23 +1115,24 @@ __global__ void __launch_bounds__(256) k_dst_lines(const double* __restrict__ in
                                                    double* __restrict__ out, const i64 n_lines,
                                                    const i64 stride, const double scale,
                                                    const double alpha, const int accumulate,
-                                                   const double2* __restrict__ twiddle) {
-  constexpr int N = 1 << LOG2N;
-  constexpr int n1 = N - 1;
-  constexpr int LOG2L = LOG2N + 1;
-  constexpr int L = 1 << LOG2L;
-  constexpr int PAIRS = (2048 / L) > 0 ? (2048 / L) : 1;
-  constexpr int TL = 2 * PAIRS;  // lines per tile
+                                                   const double2* __restrict__ tw) {
+  using S = DSTShape<LOG2N>;
+  constexpr int L = S::L, F = S::F, TL = S::TL, n1 = S::n1, N = S::N, BUF = S::BUF;
   extern __shared__ double2 sm[];
-  double2* tw = sm + PAIRS * L;
-  double* smd = reinterpret_cast<double*>(sm);
-
-  for (int k = threadIdx.x; k < L / 2; k += blockDim.x) tw[k] = twiddle[k];
-  for (int k = threadIdx.x; k < PAIRS * L; k += blockDim.x) sm[k] = make_double2(0.0, 0.0);
-  __syncthreads();
+  double2* bufA = sm;
+  double2* bufB = sm + F * BUF;
+  double* smd = reinterpret_cast<double*>(bufA);
 
   const i64 line0 = i64(blockIdx.x) * TL;
   const int nt = int(min(i64(TL), n_lines - line0));
+  // zero the slots that are not written by the load (z_0, z_N, missing lines)
+  for (int f = threadIdx.x; f < F; f += blockDim.x) {
+    bufA[f * BUF + dst_pad(0)] = make_double2(0.0, 0.0);
+    bufA[f * BUF + dst_pad(N)] = make_double2(0.0, 0.0);
+  }
+  if (nt < TL)
+    for (int k = threadIdx.x; k < F * BUF; k += blockDim.x) bufA[k] = make_double2(0.0, 0.0);
+  __syncthreads();
   const int tile = TL * n1;
   for (int e = threadIdx.x; e < tile; e += blockDim.x) {
     int li, j;
@@ -871,34 +1147,13 @@ __global__ void __launch_bounds__(256) k_dst_lines(const double* __restrict__ in
     const i64 line = line0 + li;
     const i64 o = line / stride, tt = line - o * stride;
     const double v = in[(o * n1 + j) * stride + tt];
-    const int p = li >> 1, comp = li & 1;
-    const int pos = j + 1;
-    const int b1 = int(__brev(unsigned(pos)) >> (32 - LOG2L));
-    const int b2 = int(__brev(unsigned(L - pos)) >> (32 - LOG2L));
-    smd[2 * (p * L + b1) + comp] = v;
-    smd[2 * (p * L + b2) + comp] = -v;
+    const int f = li >> 1, comp = li & 1;
+    smd[2 * (f * BUF + dst_pad(j + 1)) + comp] = v;
+    smd[2 * (f * BUF + dst_pad(L - 1 - j)) + comp] = -v;
   }
   __syncthreads();
 
-#pragma unroll 1
-  for (int s = 1; s <= LOG2L; ++s) {
-    const int half = 1 << (s - 1);
-    for (int bf = threadIdx.x; bf < PAIRS * (L / 2); bf += blockDim.x) {
-      const int p = bf >> (LOG2L - 1);
-      const int b = bf & (L / 2 - 1);
-      const int grp = b >> (s - 1);
-      const int pos = b & (half - 1);
-      const int i = p * L + grp * 2 * half + pos;
-      const int jj = i + half;
-      const double2 w = tw[pos << (LOG2L - s)];
-      const double2 x = sm[i];
-      const double2 y = cmul(w, sm[jj]);
-      sm[i] = make_double2(x.x + y.x, x.y + y.y);
-      sm[jj] = make_double2(x.x - y.x, x.y - y.y);
-    }
-    __syncthreads();
-  }
-
+  const double2* src = dst_passes<LOG2N, 0>(bufA, bufB, 1, tw);
   const double hs = 0.5 * scale;
   for (int e = threadIdx.x; e < tile; e += blockDim.x) {
     int li, j;
@@ -912,8 +1167,8 @@ __global__ void __launch_bounds__(256) k_dst_lines(const double* __restrict__ in
     if (li >= nt) continue;
     const i64 line = line0 + li;
     const i64 o = line / stride, tt = line - o * stride;
-    const int p = li >> 1, comp = li & 1;
-    const double2 Z = sm[p * L + j + 1];
+    const int f = li >> 1, comp = li & 1;
+    const double2 Z = src[f * BUF + dst_pad(j + 1)];
     const double v = (comp == 0 ? -Z.y : Z.x) * hs;
     const i64 addr = (o * n1 + j) * stride + tt;
     if (accumulate) out[addr] += alpha * v;
@@ -969,6 +1224,13 @@ __global__ void k_fill_uniform(double* __restrict__ v, const i64 n, const unsign
   const unsigned long long ctr = (stream << 56) + (unsigned long long)(offset + i);
   const unsigned long long x = mix64(seed + 0x9E3779B97F4A7C15ULL * ctr);
   v[i] = 2.0 * (double(x >> 11) * 0x1.0p-53) - 1.0;
+}
+
+__global__ void k_nonzero(const double* __restrict__ v, const i64 n, int* __restrict__ flag) {
+  bool nz = false;
+  for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x)
+    nz |= (v[i] != 0.0);
+  if (__syncthreads_or(nz) && threadIdx.x == 0) *flag = 1;
 }
 
 __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, const double a,
@@ -1077,15 +1339,16 @@ cudaError_t launch_dst_axis(const LevelView& L, int axis, const double* in, doub
   switch (log2n) {
 #define STMG_DST_CASE(K)                                                                   \
   case K: {                                                                                \
-    constexpr int Lf = 2 << K;                                                             \
-    constexpr int PAIRS = (2048 / Lf) > 0 ? (2048 / Lf) : 1;                               \
-    const size_t smem = size_t(PAIRS) * Lf * sizeof(double2) + size_t(Lf / 2) * sizeof(double2); \
-    const unsigned grid = unsigned((n_lines + 2 * PAIRS - 1) / (2 * PAIRS));             \
-    if (smem > 48 * 1024)                                                                  \
+    using SH = DSTShape<K>;                                                                \
+    const unsigned grid = unsigned((n_lines + SH::TL - 1) / SH::TL);                       \
+    static bool attr_set = false;                                                          \
+    if (!attr_set) {                                                                       \
       cudaFuncSetAttribute(k_dst_lines<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                           int(smem));                                                     \
-    k_dst_lines<K><<<grid, 256, smem, st>>>(in, out, n_lines, stride, scale, alpha,        \
-                                             accumulate ? 1 : 0, tw);                      \
+                           int(SH::smem));                                                 \
+      attr_set = true;                                                                     \
+    }                                                                                      \
+    k_dst_lines<K><<<grid, 256, SH::smem, st>>>(in, out, n_lines, stride, scale, alpha,    \
+                                                 accumulate ? 1 : 0, tw);                  \
   } break;
     STMG_DST_CASE(1)
     STMG_DST_CASE(2)
@@ -1148,11 +1411,59 @@ cudaError_t launch_axpy(double* y, const double* x, double a, int64_t n, cudaStr
   return cudaGetLastError();
 }
 
+cudaError_t launch_nonzero(const double* v, int64_t n, int* flag, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  const unsigned g = unsigned(std::min<i64>((n + 255) / 256, 148 * 8));
+  k_nonzero<<<g, 256, 0, st>>>(v, n, flag);
+  return cudaGetLastError();
+}
+
+template <int NL>
+cudaError_t build_tail_table_t(const TailSpec* lv, int nlev, void** out) {
+  std::vector<TailLevel<NL>> h(nlev);
+  for (int k = 0; k < nlev; ++k) {
+    h[k].t = make_tm<NL>(lv[k].view.tc);
+    h[k].s = make_sp(lv[k].view.sp);
+    h[k].n_t = lv[k].view.n_t;
+    h[k].n1c = lv[k].n1c;
+    h[k].mode = lv[k].mode;
+    h[k].F = lv[k].F;
+    h[k].U0 = lv[k].U0;
+    h[k].U1 = lv[k].U1;
+  }
+  cudaError_t e = cudaMalloc(out, sizeof(TailLevel<NL>) * nlev);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(*out, h.data(), sizeof(TailLevel<NL>) * nlev, cudaMemcpyHostToDevice);
+}
+
+cudaError_t build_tail_table(const TailSpec* levels, int nlev, void** dev_table) {
+  switch (levels[0].view.tc.nl) {
+    case 1: return build_tail_table_t<1>(levels, nlev, dev_table);
+    case 2: return build_tail_table_t<2>(levels, nlev, dev_table);
+    case 3: return build_tail_table_t<3>(levels, nlev, dev_table);
+    case 4: return build_tail_table_t<4>(levels, nlev, dev_table);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_tail(int dim, int nl, const void* dev_table, int nlev, double omega,
+                        size_t smem_bytes, cudaStream_t st) {
+  if (nlev > kTailMaxLevels) return cudaErrorInvalidValue;
+  STMG_DISPATCH(dim, nl, {
+    cudaFuncSetAttribute(k_tail<DIM, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem_bytes));
+    k_tail<DIM, NL><<<1, 1024, smem_bytes, st>>>(static_cast<const TailLevel<NL>*>(dev_table),
+                                                  nlev, omega);
+  });
+  return cudaGetLastError();
+}
+
 int pick_chunk(const LevelView& L, bool grouped) {
   const i64 G = (L.sp.n1 + 1) / 2;
   const i64 units = grouped ? (ipow(G, L.sp.dim) << L.sp.dim) : L.sp.nx;
-  // aim for ~64K threads; chunks are even and divide the (power-of-two) n_t
-  const i64 target = 65536;
+  // aim for ~1K resident threads per SM; chunks are even and divide the
+  // (power-of-two) n_t; longer chunks amortise the one-step warm-up
+  const i64 target = 148 * 1024;
   i64 c = 2;
   while (c < 64 && c * 2 <= L.n_t && units * (L.n_t / (c * 2)) >= target) c *= 2;
   if (c > L.n_t) c = L.n_t;

@@ -101,4 +101,20 @@ cudaError_t launch_resnorm(const LevelView& L, ModalArgs& a, const double* u,
 // Chunk length heuristic for the modal kernels at a level.
 int pick_chunk(const LevelView& L, bool grouped);
 
+// Single-CTA coarse tail (levels[0..nlev) = the small levels down to the
+// coarsest).  The device table is built once (outside graph capture).
+struct TailSpec {
+  LevelView view;
+  int64_t n1c = 0;
+  int mode = 0;
+  double* F = nullptr;
+  double* U0 = nullptr;
+  double* U1 = nullptr;
+};
+cudaError_t build_tail_table(const TailSpec* levels, int nlev, void** dev_table);
+cudaError_t launch_tail(int dim, int nl, const void* dev_table, int nlev, double omega,
+                        size_t smem_bytes, cudaStream_t st);
+// flag[0] = 1 if any v[i] != 0 (flag must be zeroed before).
+cudaError_t launch_nonzero(const double* v, int64_t n, int* flag, cudaStream_t st);
+
 }  // namespace stmg
