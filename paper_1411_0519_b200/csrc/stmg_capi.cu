@@ -413,7 +413,7 @@ void ensure_spectral(stmg_ctx* c, int from_level) {
 
 // The suffix of levels whose vectors (f, u, u') fit in one SM's shared
 // memory runs inside the single-CTA tail kernel.
-constexpr i64 kTailSmemBytes = 200 * 1024;
+constexpr i64 kTailSmemBytes = 184 * 1024;
 
 void ensure_tail(stmg_ctx* c) {
   if (c->tail_table || c->tail_start == 0) return;
@@ -422,7 +422,7 @@ void ensure_tail(stmg_ctx* c) {
   i64 bytes = 0;
   while (start - 1 >= 1) {
     const i64 b = 24 * c->levels[start - 1].view.size();
-    if (bytes + b > kTailSmemBytes || nl - (start - 1) > 32) break;
+    if (bytes + b > kTailSmemBytes || nl - (start - 1) > 24) break;
     bytes += b;
     --start;
   }

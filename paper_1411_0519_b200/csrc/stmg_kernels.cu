@@ -207,17 +207,18 @@ template <int DIM>
 __device__ __forceinline__ Member make_member(const SP& s, i64 t, i64 n1c, bool full) {
   Member m;
   const int b = int(t & ((1 << DIM) - 1));
-  i64 g = t >> DIM;
+  const i64 gg = t >> DIM;
   const i64 ngroups = ipow(s.G, DIM);
-  m.ok = g < ngroups;
-  if (!m.ok) g = 0;
+  m.ok = gg < ngroups;
+  unsigned g = m.ok ? unsigned(gg) : 0u;  // < 2^31 groups: 32-bit index math
   m.cok = m.ok;
   i64 idx = 0, mul = 1, ci = 0, cm = 1;
   double mv[DIM], kv[DIM], fac = 1.0;
+  const unsigned G = unsigned(s.G);
 #pragma unroll
   for (int a = 0; a < DIM; ++a) {
-    const int ia = int(g % s.G);
-    g /= s.G;
+    const int ia = int(g % G);
+    g /= G;
     const bool mid = ia >= s.G - 1;
     if (mid) m.cok = false;
     const int bit = (b >> a) & 1;
@@ -576,47 +577,54 @@ struct TailLevel {
   double* U1;
 };
 
-constexpr int kTailMaxLevels = 32;
+constexpr int kTailMaxLevels = 24;
 
 template <int DIM, int NL>
 __global__ void __launch_bounds__(1024) k_tail(const TailLevel<NL>* __restrict__ lv,
                                                const int nlev, const double omega) {
   extern __shared__ double smem[];
-  __shared__ TailLevel<NL> A, B;
+  __shared__ TailLevel<NL> lvs[kTailMaxLevels];
   __shared__ i64 off[kTailMaxLevels + 1];
   const int T = blockDim.x;
-  if (threadIdx.x == 0) {
-    off[0] = 0;
-    for (int k = 0; k < nlev; ++k) off[k + 1] = off[k] + 3 * lv[k].n_t * NL * lv[k].s.nx;
+  {  // level table -> shared memory in one cooperative copy
+    static_assert(sizeof(TailLevel<NL>) % 8 == 0, "table copy in 8-byte words");
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(lv);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(lvs);
+    const int words = int(nlev * sizeof(TailLevel<NL>) / 8);
+    for (int i = threadIdx.x; i < words; i += T) dst[i] = src[i];
   }
   __syncthreads();
-  auto load_level = [&](TailLevel<NL>& D, int k) {
-    D = lv[k];
-    const i64 sz = D.n_t * NL * D.s.nx;
-    D.F = smem + off[k];
-    D.U0 = D.F + sz;
-    D.U1 = D.U0 + sz;
-  };
-  {  // stage the first level's rhs
-    const i64 sz = lv[0].n_t * NL * lv[0].s.nx;
-    const double* g = lv[0].F;
-    for (i64 i = threadIdx.x; i < sz; i += T) smem[i] = g[i];
+  if (threadIdx.x == 0) {
+    off[0] = 0;
+    for (int k = 0; k < nlev; ++k) off[k + 1] = off[k] + 3 * lvs[k].n_t * NL * lvs[k].s.nx;
   }
+  __syncthreads();
+  if (threadIdx.x < nlev) {  // point every level at its shared-memory vectors
+    const int k = threadIdx.x;
+    const i64 sz = lvs[k].n_t * NL * lvs[k].s.nx;
+    lvs[k].F = smem + off[k];
+    lvs[k].U0 = smem + off[k] + sz;
+    lvs[k].U1 = smem + off[k] + 2 * sz;
+  }
+  const int sz0 = int(lv[0].n_t * NL * lv[0].s.nx);
+  {  // stage the first level's rhs
+    const double* g = lv[0].F;
+    for (int i = threadIdx.x; i < sz0; i += T) smem[i] = g[i];
+  }
+  __syncthreads();
   for (int k = 0; k + 1 < nlev; ++k) {
-    if (threadIdx.x == 0) {
-      load_level(A, k);
-      load_level(B, k + 1);
-    }
-    __syncthreads();
-    const i64 lanes = ipow(A.s.G, DIM) << DIM;
-    i64 C = 2;
-    while (C < A.n_t && lanes * (A.n_t / C) > T) C *= 2;
-    const i64 items = lanes * ((A.n_t + C - 1) / C);
-    const i64 rounded = (items + T - 1) / T * T;
-    for (i64 it = threadIdx.x; it < rounded; it += T) {
-      const i64 lane = it % lanes, n0 = (it / lanes) * C;
-      if (n0 >= A.n_t) continue;  // whole alias groups skip together
-      const i64 nend = min(n0 + C, A.n_t);
+    const TailLevel<NL>& A = lvs[k];
+    const TailLevel<NL>& B = lvs[k + 1];
+    const int nt = int(A.n_t);
+    const int lanes = int(ipow(A.s.G, DIM) << DIM);
+    int C = 2;
+    while (C < nt && lanes * (nt / C) > T) C *= 2;
+    const int items = lanes * ((nt + C - 1) / C);
+    const int rounded = (items + T - 1) / T * T;
+    for (int it = threadIdx.x; it < rounded; it += T) {
+      const int lane = it % lanes, n0 = (it / lanes) * C;
+      if (n0 >= nt) continue;  // whole alias groups skip together
+      const int nend = min(n0 + C, nt);
       if (A.mode == 2)
         down_body<DIM, NL, true, 2, true>(lane, n0, nend, A.F, A.U1, A.U1, B.F, A.t, A.s, A.n1c,
                                           omega, n0 > 0, n0 - 1 > 0);
@@ -626,23 +634,23 @@ __global__ void __launch_bounds__(1024) k_tail(const TailLevel<NL>* __restrict__
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) load_level(A, nlev - 1);
-  __syncthreads();
-  for (i64 r = threadIdx.x; r < A.s.nx; r += T) fwdsub_body<DIM, NL, true>(r, A.F, A.U0, A.t, A.s, A.n_t);
+  {
+    const TailLevel<NL>& A = lvs[nlev - 1];
+    for (int r = threadIdx.x; r < int(A.s.nx); r += T)
+      fwdsub_body<DIM, NL, true>(r, A.F, A.U0, A.t, A.s, A.n_t);
+  }
   __syncthreads();
   for (int k = nlev - 2; k >= 0; --k) {
-    if (threadIdx.x == 0) {
-      load_level(A, k);
-      load_level(B, k + 1);
-    }
-    __syncthreads();
-    const i64 lanes = ipow(A.s.G, DIM) << DIM;
-    i64 C = 2;
-    while (C < A.n_t && lanes * (A.n_t / C) > T) C *= 2;
-    const i64 items = lanes * ((A.n_t + C - 1) / C);
-    for (i64 it = threadIdx.x; it < items; it += T) {
-      const i64 lane = it % lanes, n0 = (it / lanes) * C;
-      const i64 nend = min(n0 + C, A.n_t);
+    const TailLevel<NL>& A = lvs[k];
+    const TailLevel<NL>& B = lvs[k + 1];
+    const int nt = int(A.n_t);
+    const int lanes = int(ipow(A.s.G, DIM) << DIM);
+    int C = 2;
+    while (C < nt && lanes * (nt / C) > T) C *= 2;
+    const int items = lanes * ((nt + C - 1) / C);
+    for (int it = threadIdx.x; it < items; it += T) {
+      const int lane = it % lanes, n0 = (it / lanes) * C;
+      const int nend = min(n0 + C, nt);
       if (A.mode == 2)
         up_body<DIM, NL, 2, false, true>(lane, n0, nend, B.U0, A.U1, A.F, A.U0, A.t, A.s, A.n1c,
                                          omega, n0 > 0, n0 - 1 > 0);
@@ -653,9 +661,8 @@ __global__ void __launch_bounds__(1024) k_tail(const TailLevel<NL>* __restrict__
     __syncthreads();
   }
   {  // hand the first level's iterate back
-    const i64 sz = lv[0].n_t * NL * lv[0].s.nx;
     double* g = lv[0].U0;
-    for (i64 i = threadIdx.x; i < sz; i += T) g[i] = smem[sz + i];
+    for (int i = threadIdx.x; i < sz0; i += T) g[i] = smem[sz0 + i];
   }
 }
 
@@ -746,23 +753,24 @@ __global__ void __launch_bounds__(128) k_fwdsub(const double* __restrict__ f,
 template <int DIM, int NL>
 __global__ void __launch_bounds__(256) k_modal_solve(double* __restrict__ x, const TM<NL> t,
                                                      const SP s, const i64 n_t) {
-  const i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= n_t * s.nx) return;
-  const i64 n = e / s.nx, r = e - n * s.nx;
+  const unsigned r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= s.nx) return;
   double Mj, Kj;
   mode_eig<DIM>(s, r, Mj, Kj);
-  double b[NL], y[NL];
-  double* p = x + n * NL * s.nx + r;
-  load_nl<NL>(p, s.nx, b);
-  solve_mode<NL>(t, Mj, Kj, b, y);
-  store_nl<NL>(p, s.nx, y);
+  for (i64 n = blockIdx.y; n < n_t; n += gridDim.y) {
+    double b[NL], y[NL];
+    double* p = x + n * NL * s.nx + r;
+    load_nl<NL>(p, s.nx, b);
+    solve_mode<NL>(t, Mj, Kj, b, y);
+    store_nl<NL>(p, s.nx, y);
+  }
 }
 
 // ===================================================== physical operators
 // Q1 stencils: M = (x)_a M1, K = sum_a K1 on axis a, M1 elsewhere,
 // M1 = h/6 {1,4,1}, K1 = 1/h {-1,2,-1} (fem_space.cpp:40-58, + 3D).
 template <int DIM>
-__device__ __forceinline__ void coords(i64 r, i64 n1, int (&c)[3]) {
+__device__ __forceinline__ void coords(unsigned r, unsigned n1, int (&c)[3]) {
   c[0] = int(r % n1);
   c[1] = DIM > 1 ? int((r / n1) % n1) : 0;
   c[2] = DIM > 2 ? int(r / (n1 * n1)) : 0;
@@ -813,12 +821,12 @@ __global__ void __launch_bounds__(256) k_apply(const double* __restrict__ u,
                                                double* __restrict__ y, const TM<NL> t,
                                                const i64 n1, const i64 nx, const double h,
                                                const i64 n_t, const bool first_global) {
-  const i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= n_t * nx) return;
-  const i64 n = e / nx, r = e - n * nx;
+  const unsigned r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nx) return;
   int c[3];
-  coords<DIM>(r, n1, c);
+  coords<DIM>(r, unsigned(n1), c);
   const i64 slab = NL * nx;
+  for (i64 n = blockIdx.y; n < n_t; n += gridDim.y) {
   double MU[NL], KU[NL], MP[NL];
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
@@ -844,6 +852,7 @@ __global__ void __launch_bounds__(256) k_apply(const double* __restrict__ u,
     const i64 o = n * slab + k * nx + r;
     y[o] = RES ? __ldg(f + o) - a : a;
   }
+  }
 }
 
 // restrict_semi / restrict_full (transfer.cpp:75-85, 138-149): one thread per
@@ -854,11 +863,11 @@ __global__ void __launch_bounds__(256) k_restrict(const double* __restrict__ fin
                                                   double* __restrict__ coarse, const TM<NL> t,
                                                   const i64 n1, const i64 n1c, const i64 ntc) {
   const i64 nx = ipow(n1, DIM), nxc = ipow(n1c, DIM);
-  const i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= ntc * nxc) return;
-  const i64 nc = e / nxc, rc = e - nc * nxc;
+  const unsigned rc = blockIdx.x * blockDim.x + threadIdx.x;
+  if (rc >= nxc) return;
   int c[3];
-  coords<DIM>(rc, n1c, c);
+  coords<DIM>(rc, unsigned(n1c), c);
+  for (i64 nc = blockIdx.y; nc < ntc; nc += gridDim.y) {
   double v0[NL], v1[NL];
 #pragma unroll
   for (int l = 0; l < NL; ++l) v0[l] = v1[l] = 0.0;
@@ -899,6 +908,7 @@ __global__ void __launch_bounds__(256) k_restrict(const double* __restrict__ fin
     }
     o[k * nxc] = s0 + s1;
   }
+  }
 }
 
 // prolong_semi / prolong_full (transfer.cpp:87-96, 151-158): one thread per
@@ -908,12 +918,12 @@ __global__ void __launch_bounds__(256) k_prolong(const double* __restrict__ coar
                                                  double* __restrict__ fine, const TM<NL> t,
                                                  const i64 n1, const i64 n1c, const i64 n_t) {
   const i64 nx = ipow(n1, DIM), nxc = ipow(n1c, DIM);
-  const i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= n_t * nx) return;
-  const i64 n = e / nx, r = e - n * nx;
-  const i64 nc = n >> 1;
+  const unsigned r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nx) return;
   int c[3];
-  coords<DIM>(r, n1, c);
+  coords<DIM>(r, unsigned(n1), c);
+  for (i64 n = blockIdx.y; n < n_t; n += gridDim.y) {
+  const i64 nc = n >> 1;
   double cv[NL];
 #pragma unroll
   for (int l = 0; l < NL; ++l) cv[l] = 0.0;
@@ -969,16 +979,17 @@ __global__ void __launch_bounds__(256) k_prolong(const double* __restrict__ coar
     for (int k = 0; k < NL; ++k) s += cv[k] * ((n & 1) ? t.R2[k][l] : t.R1[k][l]);
     o[l * nx] = s;
   }
+  }
 }
 
 // f(0,k,:) += psi_k(0) M_h u0.
 template <int DIM, int NL>
 __global__ void k_fold_u0(double* __restrict__ f, const double* __restrict__ u0, const i64 n1,
                           const i64 nx, const double h, TimeConsts tc) {
-  const i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const unsigned r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nx) return;
   int c[3];
-  coords<DIM>(r, n1, c);
+  coords<DIM>(r, unsigned(n1), c);
   double Mv, Kv;
   stencil_MK<DIM>(u0, n1, h, c, Mv, Kv, false);
 #pragma unroll
@@ -1052,89 +1063,111 @@ __host__ __device__ constexpr int dst_pass_radix(int m, int p) {
 __host__ __device__ constexpr int dst_num_passes(int m) { return (m + 3) / 4; }
 __host__ __device__ constexpr int dst_pad(int i) { return i + (i >> 4); }
 
-template <int L, int F, int R>
-__device__ __forceinline__ void stockham_pass(const double2* __restrict__ src,
-                                              double2* __restrict__ dst, int Ns,
-                                              const double2* __restrict__ tw) {
-  constexpr int NJ = L / R;
-  constexpr int BUF = L + L / 16;
-  for (int w = threadIdx.x; w < F * NJ; w += blockDim.x) {
-    const int f = w / NJ, j = w - f * NJ;
-    const double2* X = src + f * BUF;
-    double2 v[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = X[dst_pad(j + r * NJ)];
-    if (Ns > 1) {
-      const int jm = j % Ns;
-      const int step = jm * (L / (Ns * R));
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        const int idx = (r * step) & (L - 1);
-        double2 w = __ldg(tw + (idx & (L / 2 - 1)));
-        if (idx >= L / 2) w = make_double2(-w.x, -w.y);
-        v[r] = cmul(v[r], w);
-      }
-    }
-    RegFFT<R>::run(v);
-    const int idxD = (j / Ns) * Ns * R + (j % Ns);
-    double2* Y = dst + f * BUF;
-#pragma unroll
-    for (int r = 0; r < R; ++r) Y[dst_pad(idxD + r * Ns)] = v[r];
-  }
-}
-
+// A team of TS = L / V threads owns one length-L FFT; every thread holds V
+// values per pass (one radix-16 butterfly, or 16/R radix-R ones), so a pass
+// is: load to registers, team barrier, store (in place), team barrier.
 template <int LOG2N>
 struct DSTShape {
   static constexpr int N = 1 << LOG2N;
   static constexpr int n1 = N - 1;
   static constexpr int M = LOG2N + 1;
   static constexpr int L = 1 << M;
-  static constexpr int F = (2048 / L) > 0 ? (2048 / L) : 1;  // FFTs per block
-  static constexpr int TL = 2 * F;                            // lines per block
+  static constexpr int V = L >= 16 ? 16 : L;
+  static constexpr int TS = L / V;
+  static constexpr int BLOCK = TS > 128 ? TS : 128;
+  static constexpr int F = BLOCK / TS;  // FFTs per block
+  static constexpr int TL = 2 * F;      // lines per block
   static constexpr int BUF = L + L / 16;
-  static constexpr size_t smem = size_t(2) * F * BUF * sizeof(double2);
+  static constexpr size_t smem = size_t(F) * BUF * sizeof(double2);
 };
 
-// Runs passes P.. of the Stockham FFT; returns the buffer holding the result.
+template <int TS>
+__device__ __forceinline__ void team_sync() {
+  if (TS <= 32) __syncwarp();
+  else __syncthreads();
+}
+
+template <int L, int TS, int R>
+__device__ __forceinline__ void stockham_pass(double2* __restrict__ X, const int tt, const int Ns,
+                                              const double2* __restrict__ tw) {
+  constexpr int NJ = L / R;        // butterflies per FFT
+  constexpr int IPT = NJ / TS;     // butterflies per thread
+  double2 v[IPT][R];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int j = tt + i * TS;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[i][r] = X[dst_pad(j + r * NJ)];
+    if (Ns > 1) {
+      const int step = (j % Ns) * (L / (Ns * R));
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const int idx = (r * step) & (L - 1);
+        double2 w = __ldg(tw + (idx & (L / 2 - 1)));
+        if (idx >= L / 2) w = make_double2(-w.x, -w.y);
+        v[i][r] = cmul(v[i][r], w);
+      }
+    }
+    RegFFT<R>::run(v[i]);
+  }
+  team_sync<TS>();
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int j = tt + i * TS;
+    const int idxD = (j / Ns) * Ns * R + (j % Ns);
+#pragma unroll
+    for (int r = 0; r < R; ++r) X[dst_pad(idxD + r * Ns)] = v[i][r];
+  }
+  team_sync<TS>();
+}
+
 template <int LOG2N, int P>
-__device__ __forceinline__ const double2* dst_passes(double2* src, double2* dst, int Ns,
-                                                     const double2* __restrict__ tw) {
+__device__ __forceinline__ void dst_passes(double2* X, const int tt, const int Ns,
+                                           const double2* __restrict__ tw) {
   using S = DSTShape<LOG2N>;
-  if constexpr (P >= dst_num_passes(S::M)) {
-    return src;
-  } else {
+  if constexpr (P < dst_num_passes(S::M)) {
     constexpr int R = dst_pass_radix(S::M, P);
-    stockham_pass<S::L, S::F, R>(src, dst, Ns, tw);
-    __syncthreads();
-    return dst_passes<LOG2N, P + 1>(dst, src, Ns * R, tw);
+    stockham_pass<S::L, S::TS, R>(X, tt, Ns, tw);
+    dst_passes<LOG2N, P + 1>(X, tt, Ns * R, tw);
   }
 }
 
 template <int LOG2N>
-__global__ void __launch_bounds__(256) k_dst_lines(const double* __restrict__ in,
-                                                   double* __restrict__ out, const i64 n_lines,
-                                                   const i64 stride, const double scale,
-                                                   const double alpha, const int accumulate,
-                                                   const double2* __restrict__ tw) {
+__global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK) k_dst_lines(
+    const double* __restrict__ in, double* __restrict__ out, const i64 n_lines, const i64 stride,
+    const double scale, const double alpha, const int accumulate,
+    const double2* __restrict__ tw) {
   using S = DSTShape<LOG2N>;
   constexpr int L = S::L, F = S::F, TL = S::TL, n1 = S::n1, N = S::N, BUF = S::BUF;
+  constexpr int TS = S::TS;
   extern __shared__ double2 sm[];
-  double2* bufA = sm;
-  double2* bufB = sm + F * BUF;
-  double* smd = reinterpret_cast<double*>(bufA);
+  double* smd = reinterpret_cast<double*>(sm);
 
+  __shared__ i64 lbase[TL];  // global offset of element 0 of each tile line
   const i64 line0 = i64(blockIdx.x) * TL;
   const int nt = int(min(i64(TL), n_lines - line0));
-  // zero the slots that are not written by the load (z_0, z_N, missing lines)
-  for (int f = threadIdx.x; f < F; f += blockDim.x) {
-    bufA[f * BUF + dst_pad(0)] = make_double2(0.0, 0.0);
-    bufA[f * BUF + dst_pad(N)] = make_double2(0.0, 0.0);
+  for (int li = threadIdx.x; li < nt; li += blockDim.x) {
+    const i64 line = line0 + li;
+    const i64 o = line / stride;
+    lbase[li] = o * stride * n1 + (line - o * stride);
   }
   if (nt < TL)
-    for (int k = threadIdx.x; k < F * BUF; k += blockDim.x) bufA[k] = make_double2(0.0, 0.0);
+    for (int k = threadIdx.x; k < F * BUF; k += blockDim.x) sm[k] = make_double2(0.0, 0.0);
+  else
+    for (int f = threadIdx.x; f < F; f += blockDim.x) {
+      sm[f * BUF + dst_pad(0)] = make_double2(0.0, 0.0);
+      sm[f * BUF + dst_pad(N)] = make_double2(0.0, 0.0);
+    }
   __syncthreads();
-  const int tile = TL * n1;
-  for (int e = threadIdx.x; e < tile; e += blockDim.x) {
+  constexpr int tile = TL * n1;
+  constexpr int BLK = S::BLOCK;
+  constexpr int ITEMS = (tile + BLK - 1) / BLK;
+  // all global loads of this thread first (memory-level parallelism), then
+  // the odd-extension scatter into shared memory
+  double vals[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int e = threadIdx.x + i * BLK;
     int li, j;
     if (stride == 1) {
       li = e / n1;
@@ -1143,18 +1176,30 @@ __global__ void __launch_bounds__(256) k_dst_lines(const double* __restrict__ in
       j = e / TL;
       li = e - j * TL;
     }
-    if (li >= nt) continue;
-    const i64 line = line0 + li;
-    const i64 o = line / stride, tt = line - o * stride;
-    const double v = in[(o * n1 + j) * stride + tt];
+    vals[i] = (e < tile && li < nt) ? __ldcs(in + lbase[li] + i64(j) * stride) : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int e = threadIdx.x + i * BLK;
+    int li, j;
+    if (stride == 1) {
+      li = e / n1;
+      j = e - li * n1;
+    } else {
+      j = e / TL;
+      li = e - j * TL;
+    }
+    if (e >= tile || li >= nt) continue;
     const int f = li >> 1, comp = li & 1;
-    smd[2 * (f * BUF + dst_pad(j + 1)) + comp] = v;
-    smd[2 * (f * BUF + dst_pad(L - 1 - j)) + comp] = -v;
+    smd[2 * (f * BUF + dst_pad(j + 1)) + comp] = vals[i];
+    smd[2 * (f * BUF + dst_pad(L - 1 - j)) + comp] = -vals[i];
   }
   __syncthreads();
+  dst_passes<LOG2N, 0>(sm + (threadIdx.x / TS) * BUF, threadIdx.x % TS, 1, tw);
+  __syncthreads();
 
-  const double2* src = dst_passes<LOG2N, 0>(bufA, bufB, 1, tw);
   const double hs = 0.5 * scale;
+#pragma unroll 4
   for (int e = threadIdx.x; e < tile; e += blockDim.x) {
     int li, j;
     if (stride == 1) {
@@ -1165,12 +1210,10 @@ __global__ void __launch_bounds__(256) k_dst_lines(const double* __restrict__ in
       li = e - j * TL;
     }
     if (li >= nt) continue;
-    const i64 line = line0 + li;
-    const i64 o = line / stride, tt = line - o * stride;
     const int f = li >> 1, comp = li & 1;
-    const double2 Z = src[f * BUF + dst_pad(j + 1)];
+    const double2 Z = sm[f * BUF + dst_pad(j + 1)];
     const double v = (comp == 0 ? -Z.y : Z.x) * hs;
-    const i64 addr = (o * n1 + j) * stride + tt;
+    const i64 addr = lbase[li] + i64(j) * stride;
     if (accumulate) out[addr] += alpha * v;
     else out[addr] = v;
   }
@@ -1240,6 +1283,10 @@ __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, con
 }
 
 inline unsigned grid1(i64 n, int bs) { return unsigned((n + bs - 1) / bs); }
+// nodes along x (blocks of bs), time steps along y (grid-stride beyond 65535)
+inline dim3 grid2(i64 nodes, i64 steps, int bs) {
+  return dim3(grid1(nodes, bs), unsigned(std::max<i64>(1, std::min<i64>(steps, 65535))));
+}
 
 }  // namespace
 
@@ -1272,14 +1319,15 @@ cudaError_t launch_apply(const LevelView& L, const double* u, const double* f, d
                          bool residual, cudaStream_t st) {
   const i64 total = L.n_t * L.sp.nx;
   if (total == 0) return cudaSuccess;
+  const dim3 g = grid2(L.sp.nx, L.n_t, 256);
   STMG_DISPATCH(L.sp.dim, L.tc.nl, {
     const TM<NL> t = make_tm<NL>(L.tc);
     if (residual)
-      k_apply<DIM, NL, true><<<grid1(total, 256), 256, 0, st>>>(u, f, y, t, L.sp.n1, L.sp.nx,
-                                                                 L.sp.h, L.n_t, L.first_global);
+      k_apply<DIM, NL, true><<<g, 256, 0, st>>>(u, f, y, t, L.sp.n1, L.sp.nx, L.sp.h, L.n_t,
+                                                 L.first_global);
     else
-      k_apply<DIM, NL, false><<<grid1(total, 256), 256, 0, st>>>(u, f, y, t, L.sp.n1, L.sp.nx,
-                                                                  L.sp.h, L.n_t, L.first_global);
+      k_apply<DIM, NL, false><<<g, 256, 0, st>>>(u, f, y, t, L.sp.n1, L.sp.nx, L.sp.h, L.n_t,
+                                                  L.first_global);
   });
   return cudaGetLastError();
 }
@@ -1288,15 +1336,15 @@ cudaError_t launch_restrict(const LevelView& F, int mode, int64_t n1c, const dou
                             double* coarse, cudaStream_t st) {
   const i64 ntc = F.n_t / 2;
   const i64 n1o = mode == 2 ? n1c : F.sp.n1;
-  const i64 total = ntc * ipow(n1o, 1) * (F.sp.dim > 1 ? n1o : 1) * (F.sp.dim > 2 ? n1o : 1);
-  if (total == 0) return cudaSuccess;
+  const i64 nxo = n1o * (F.sp.dim > 1 ? n1o : 1) * (F.sp.dim > 2 ? n1o : 1);
+  if (ntc * nxo == 0) return cudaSuccess;
+  const dim3 g = grid2(nxo, ntc, 256);
   STMG_DISPATCH(F.sp.dim, F.tc.nl, {
     const TM<NL> t = make_tm<NL>(F.tc);
     if (mode == 2)
-      k_restrict<DIM, NL, 2><<<grid1(total, 256), 256, 0, st>>>(fine, coarse, t, F.sp.n1, n1c, ntc);
+      k_restrict<DIM, NL, 2><<<g, 256, 0, st>>>(fine, coarse, t, F.sp.n1, n1c, ntc);
     else
-      k_restrict<DIM, NL, 1><<<grid1(total, 256), 256, 0, st>>>(fine, coarse, t, F.sp.n1, F.sp.n1,
-                                                               ntc);
+      k_restrict<DIM, NL, 1><<<g, 256, 0, st>>>(fine, coarse, t, F.sp.n1, F.sp.n1, ntc);
   });
   return cudaGetLastError();
 }
@@ -1305,13 +1353,13 @@ cudaError_t launch_prolong(const LevelView& F, int mode, int64_t n1c, const doub
                            double* fine, cudaStream_t st) {
   const i64 total = F.n_t * F.sp.nx;
   if (total == 0) return cudaSuccess;
+  const dim3 g = grid2(F.sp.nx, F.n_t, 256);
   STMG_DISPATCH(F.sp.dim, F.tc.nl, {
     const TM<NL> t = make_tm<NL>(F.tc);
     if (mode == 2)
-      k_prolong<DIM, NL, 2><<<grid1(total, 256), 256, 0, st>>>(coarse, fine, t, F.sp.n1, n1c, F.n_t);
+      k_prolong<DIM, NL, 2><<<g, 256, 0, st>>>(coarse, fine, t, F.sp.n1, n1c, F.n_t);
     else
-      k_prolong<DIM, NL, 1><<<grid1(total, 256), 256, 0, st>>>(coarse, fine, t, F.sp.n1, F.sp.n1,
-                                                              F.n_t);
+      k_prolong<DIM, NL, 1><<<g, 256, 0, st>>>(coarse, fine, t, F.sp.n1, F.sp.n1, F.n_t);
   });
   return cudaGetLastError();
 }
@@ -1347,7 +1395,7 @@ cudaError_t launch_dst_axis(const LevelView& L, int axis, const double* in, doub
                            int(SH::smem));                                                 \
       attr_set = true;                                                                     \
     }                                                                                      \
-    k_dst_lines<K><<<grid, 256, SH::smem, st>>>(in, out, n_lines, stride, scale, alpha,    \
+    k_dst_lines<K><<<grid, SH::BLOCK, SH::smem, st>>>(in, out, n_lines, stride, scale, alpha, \
                                                  accumulate ? 1 : 0, tw);                  \
   } break;
     STMG_DST_CASE(1)
@@ -1372,7 +1420,8 @@ cudaError_t launch_modal_solve(const LevelView& L, double* x, cudaStream_t st) {
   if (total == 0) return cudaSuccess;
   const SP s = make_sp(L.sp);
   STMG_DISPATCH(L.sp.dim, L.tc.nl, {
-    k_modal_solve<DIM, NL><<<grid1(total, 256), 256, 0, st>>>(x, make_tm<NL>(L.tc), s, L.n_t);
+    k_modal_solve<DIM, NL><<<grid2(L.sp.nx, L.n_t, 256), 256, 0, st>>>(x, make_tm<NL>(L.tc), s,
+                                                                        L.n_t);
   });
   return cudaGetLastError();
 }
