@@ -224,7 +224,7 @@ void build_level_tables(Level& L) {
   const i64 n1 = L.spec.n1();
   const double h = L.spec.h, N = double(n1 + 1);
   const i64 G = (n1 + 1) / 2;
-  std::vector<double> tab(3 * n1);
+  std::vector<double> tab(3 * n1 + 2 * stmg::kMaxNL, 0.0);
   const long double pi = 3.141592653589793238462643383279502884L;
   for (i64 q = 0; q < n1; ++q) {
     const long double th = pi * (long double)(q + 1) / (long double)N;
@@ -235,6 +235,14 @@ void build_level_tables(Level& L) {
     const double c2 = double(std::cos(th / 2));
     const double f = 2.0 * c2 * c2 / std::sqrt(2.0);  // (1 + cos)/sqrt(2)
     tab[2 * n1 + q] = q < G - 1 ? f : (q == G - 1 ? 0.0 : -f);
+  }
+  {  // N_tau = a b^T with a_k = psi_k(0), b_l = psi_l(tau) (Legendre: psi_0 = 1)
+    const stmg::DGBlock dg0 = stmg::dg_block(L.spec.p_t, L.spec.tau);
+    const int nl = L.spec.p_t + 1;
+    for (int k = 0; k < nl; ++k) {
+      tab[3 * n1 + k] = dg0.N[k * nl + 0];
+      tab[3 * n1 + stmg::kMaxNL + k] = dg0.N[0 * nl + k];
+    }
   }
   CK(cudaMalloc(&L.d_tables, tab.size() * sizeof(double)));
   CK(cudaMemcpy(L.d_tables, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -320,7 +328,7 @@ void block_solve(stmg_ctx* c, Level& L, const double* b, double* x, double* acc_
 
 void residual(stmg_ctx* c, Level& L, const double* u, const double* f, double* r) {
   prof_begin(c, 3);
-  CK(stmg::launch_apply(L.view, u, f, r, true, c->stream));
+  CK(stmg::launch_apply(L.view, u, f, r, true, L.d_tables + 3 * L.spec.n1(), c->stream));
   prof_end(c, 3, 24.0 * double(L.view.size()));
   count(c);
 }
@@ -893,7 +901,7 @@ int stmg_apply(stmg_ctx* c, int level, const double* u, double* y) {
   return guard([&] {
     Level& L = lev(c, level);
     require(u && y, "null vector");
-    CK(stmg::launch_apply(L.view, u, nullptr, y, false, c->stream));
+    CK(stmg::launch_apply(L.view, u, nullptr, y, false, L.d_tables + 3 * L.spec.n1(), c->stream));
     count(c);
   });
 }

@@ -814,44 +814,200 @@ __device__ __forceinline__ void stencil_MK(const double* __restrict__ v, i64 n1,
 }
 
 // y_n = (M U_n) K^T + (K U_n) M^T - (M U_{n-1}) N^T; residual: r = f - y
-// (st_system.cpp:18-33, 57-67).
-template <int DIM, int NL, bool RES>
-__global__ void __launch_bounds__(256) k_apply(const double* __restrict__ u,
-                                               const double* __restrict__ f,
-                                               double* __restrict__ y, const TM<NL> t,
-                                               const i64 n1, const i64 nx, const double h,
-                                               const i64 n_t, const bool first_global) {
-  const unsigned r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= nx) return;
-  int c[3];
-  coords<DIM>(r, unsigned(n1), c);
-  const i64 slab = NL * nx;
-  for (i64 n = blockIdx.y; n < n_t; n += gridDim.y) {
-  double MU[NL], KU[NL], MP[NL];
+// (st_system.cpp:18-33, 57-67).  One CTA owns a spatial tile and marches
+// through a chunk of time steps: slab n (tile + 1-node halo, all DG
+// components) is staged in shared memory with cp.async while slab n-1 is
+// being used, so u is read from HBM once.  N_tau = a b^T is rank one
+// (N[k,l] = psi_l(tau) psi_k(0)), so the jump term is a_k * sum_l b_l (M u_{n-1,l})
+// and reuses the M-stencils of the previous step kept in registers.
+template <int DIM>
+struct ResTile {
+  static constexpr int TX = DIM == 1 ? 256 : 32;
+  static constexpr int TY = DIM == 1 ? 1 : (DIM == 2 ? 8 : 4);
+  static constexpr int TZ = DIM == 3 ? 2 : 1;
+  static constexpr int HX = TX + 2;
+  static constexpr int HY = DIM >= 2 ? TY + 2 : 1;
+  static constexpr int HZ = DIM == 3 ? TZ + 2 : 1;
+  static constexpr int HALO = HX * HY * HZ;
+  static constexpr int THREADS = TX * TY * TZ;
+};
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* g, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(g),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Staging plan of one thread: the (tile + halo) x NL elements it copies each
+// step, as slab-relative global offsets (-1: outside the Dirichlet domain ->
+// zero fill).  Step-invariant, so computed once per CTA.
+template <int DIM, int NL>
+struct StagePlan {
+  static constexpr int ITEMS = (NL * ResTile<DIM>::HALO + ResTile<DIM>::THREADS - 1) /
+                               ResTile<DIM>::THREADS;
+  int off[ITEMS];
+};
+
+template <int DIM, int NL>
+__device__ __forceinline__ void make_plan(StagePlan<DIM, NL>& P, int n1, i64 nx, int x0, int y0,
+                                          int z0) {
+  using T = ResTile<DIM>;
 #pragma unroll
-  for (int l = 0; l < NL; ++l) {
-    stencil_MK<DIM>(u + n * slab + l * nx, n1, h, c, MU[l], KU[l], true);
-    MP[l] = 0.0;
-  }
-  if (n > 0 || !first_global) {
-#pragma unroll
-    for (int l = 0; l < NL; ++l) {
-      double dummy;
-      stencil_MK<DIM>(u + (n - 1) * slab + l * nx, n1, h, c, MP[l], dummy, false);
+  for (int i = 0; i < StagePlan<DIM, NL>::ITEMS; ++i) {
+    const int e = threadIdx.x + i * T::THREADS;
+    int o = -1;
+    if (e < NL * T::HALO) {
+      const int l = e / T::HALO;
+      const int h = e - l * T::HALO;
+      const int hx = h % T::HX;
+      const int hy = (h / T::HX) % T::HY;
+      const int hz = h / (T::HX * T::HY);
+      const int x = x0 + hx - 1, y = DIM >= 2 ? y0 + hy - 1 : 0, z = DIM == 3 ? z0 + hz - 1 : 0;
+      if (x >= 0 && x < n1 && y >= 0 && y < n1 && z >= 0 && z < n1)
+        o = int(l * nx + (i64(z) * n1 + y) * n1 + x);
     }
+    P.off[i] = o;
   }
+}
+
+// Stage slab n of u into buf (cp.async, zero fill outside the domain).
+template <int DIM, int NL>
+__device__ __forceinline__ void stage_slab(double* buf, const double* u, i64 n, i64 nx,
+                                           const StagePlan<DIM, NL>& P) {
+  using T = ResTile<DIM>;
+  const double* base = u + n * NL * nx;
+#pragma unroll
+  for (int i = 0; i < StagePlan<DIM, NL>::ITEMS; ++i) {
+    const int e = threadIdx.x + i * T::THREADS;
+    if (StagePlan<DIM, NL>::ITEMS * T::THREADS == NL * T::HALO || e < NL * T::HALO)
+      cp_async8(buf + e, P.off[i] >= 0 ? base + P.off[i] : base, P.off[i] >= 0);
+  }
+}
+
+// M and K stencils of one staged component at tile-local (tx, ty, tz).
+template <int DIM>
+__device__ __forceinline__ void stencil_smem(const double* s, int tx, int ty, int tz, double h,
+                                             double& Mv, double& Kv) {
+  using T = ResTile<DIM>;
+  const double m0 = 4.0 * h / 6.0, m1 = h / 6.0, k0 = 2.0 / h, k1 = -1.0 / h;
+  auto row = [&](int yy, int zz, double& Mr, double& Kr) {
+    const double* p = s + (zz * T::HY + yy) * T::HX + tx + 1;
+    const double a = p[-1] + p[1], c = p[0];
+    Mr = m1 * a + m0 * c;
+    Kr = k1 * a + k0 * c;
+  };
+  auto plane = [&](int zz, double& Mp, double& Kp) {
+    if (DIM == 1) {
+      row(0, zz, Mp, Kp);
+    } else {
+      double Ma, Ka, Mb, Kb, Mc, Kc;
+      row(ty, zz, Ma, Ka);
+      row(ty + 1, zz, Mb, Kb);
+      row(ty + 2, zz, Mc, Kc);
+      const double ms = Ma + Mc;
+      Mp = m1 * ms + m0 * Mb;
+      Kp = m1 * (Ka + Kc) + m0 * Kb + k1 * ms + k0 * Mb;
+    }
+  };
+  if (DIM < 3) {
+    plane(0, Mv, Kv);
+  } else {
+    double Ma, Ka, Mb, Kb, Mc, Kc;
+    plane(tz, Ma, Ka);
+    plane(tz + 1, Mb, Kb);
+    plane(tz + 2, Mc, Kc);
+    const double ms = Ma + Mc;
+    Mv = m1 * ms + m0 * Mb;
+    Kv = m1 * (Ka + Kc) + m0 * Kb + k1 * ms + k0 * Mb;
+  }
+}
+
+template <int DIM, int NL, bool RES>
+__global__ void __launch_bounds__(ResTile<DIM>::THREADS) k_apply(
+    const double* __restrict__ u, const double* __restrict__ f, double* __restrict__ y,
+    const TM<NL> t, const i64 n1_, const i64 nx, const double h, const i64 n_t, const int C,
+    const bool first_global, const double* __restrict__ ab) {
+  using T = ResTile<DIM>;
+  extern __shared__ double dsm[];
+  constexpr int BS = NL * T::HALO;  // one staged slab
+  const int n1 = int(n1_);
+  const int tilesx = (n1 + T::TX - 1) / T::TX;
+  const int tilesy = DIM >= 2 ? (n1 + T::TY - 1) / T::TY : 1;
+  int tile = blockIdx.x;
+  const int bx = tile % tilesx;
+  tile /= tilesx;
+  const int by = tile % tilesy;
+  const int bz = tile / tilesy;
+  const int x0 = bx * T::TX, y0 = by * T::TY, z0 = bz * T::TZ;
+  const int tx = threadIdx.x % T::TX;
+  const int ty = (threadIdx.x / T::TX) % T::TY;
+  const int tz = threadIdx.x / (T::TX * T::TY);
+  const int x = x0 + tx, yy = y0 + ty, z = z0 + tz;
+  const bool inside = x < n1 && (DIM < 2 || yy < n1) && (DIM < 3 || z < n1);
+  const i64 r = (i64(DIM == 3 ? z : 0) * n1 + (DIM >= 2 ? yy : 0)) * n1 + x;
+  const i64 n0 = i64(blockIdx.y) * C;
+  const i64 nend = min(n0 + i64(C), n_t);
+  const i64 slab = NL * nx;
+  double a[NL], b[NL];
 #pragma unroll
   for (int k = 0; k < NL; ++k) {
-    double a = 0.0;
-#pragma unroll
-    for (int l = 0; l < NL; ++l) a += MU[l] * t.K[k][l];
-#pragma unroll
-    for (int l = 0; l < NL; ++l) a += KU[l] * t.M[k][l];
-#pragma unroll
-    for (int l = 0; l < NL; ++l) a -= MP[l] * t.N[k][l];
-    const i64 o = n * slab + k * nx + r;
-    y[o] = RES ? __ldg(f + o) - a : a;
+    a[k] = ab[k];
+    b[k] = ab[kMaxNL + k];
   }
+
+  // warm-up: M-stencil trace of step n0-1
+  double mw_prev = 0.0;
+  const bool has_prev = n0 > 0 || !first_global;
+  StagePlan<DIM, NL> plan;
+  make_plan<DIM, NL>(plan, n1, nx, x0, y0, z0);
+  if (has_prev) stage_slab<DIM, NL>(dsm, u, n0 - 1, nx, plan);
+  cp_async_commit();
+  stage_slab<DIM, NL>(dsm + BS, u, n0, nx, plan);
+  cp_async_commit();
+  cp_async_wait<1>();
+  __syncthreads();
+  if (has_prev && inside) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      double Mv, Kv;
+      stencil_smem<DIM>(dsm + l * T::HALO, tx, ty, tz, h, Mv, Kv);
+      mw_prev += b[l] * Mv;
+    }
+  }
+  for (i64 n = n0; n < nend; ++n) {
+    const int cur = int((n - n0 + 1) & 1);
+    cp_async_wait<0>();
+    __syncthreads();  // slab n visible; slab n-1's buffer free
+    if (n + 1 < nend) stage_slab<DIM, NL>(dsm + (cur ^ 1) * BS, u, n + 1, nx, plan);
+    cp_async_commit();
+    if (inside) {
+      double fv[NL];
+      if (RES) {
+#pragma unroll
+        for (int k = 0; k < NL; ++k) fv[k] = __ldcs(f + n * slab + k * nx + r);
+      }
+      double MU[NL], KU[NL], mw = 0.0;
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        stencil_smem<DIM>(dsm + cur * BS + l * T::HALO, tx, ty, tz, h, MU[l], KU[l]);
+        mw += b[l] * MU[l];
+      }
+#pragma unroll
+      for (int k = 0; k < NL; ++k) {
+        double acc = 0.0;
+#pragma unroll
+        for (int l = 0; l < NL; ++l) acc += MU[l] * t.K[k][l] + KU[l] * t.M[k][l];
+        acc -= a[k] * mw_prev;
+        const i64 o = n * slab + k * nx + r;
+        __stcs(y + o, RES ? fv[k] - acc : acc);
+      }
+      mw_prev = mw;
+    }
   }
 }
 
@@ -1316,18 +1472,34 @@ inline dim3 grid2(i64 nodes, i64 steps, int bs) {
   }
 
 cudaError_t launch_apply(const LevelView& L, const double* u, const double* f, double* y,
-                         bool residual, cudaStream_t st) {
-  const i64 total = L.n_t * L.sp.nx;
-  if (total == 0) return cudaSuccess;
-  const dim3 g = grid2(L.sp.nx, L.n_t, 256);
+                         bool residual, const double* ab, cudaStream_t st) {
+  if (L.n_t * L.sp.nx == 0) return cudaSuccess;
   STMG_DISPATCH(L.sp.dim, L.tc.nl, {
+    using T = ResTile<DIM>;
+    const i64 n1 = L.sp.n1;
+    const i64 tiles = ((n1 + T::TX - 1) / T::TX) * (DIM >= 2 ? (n1 + T::TY - 1) / T::TY : 1) *
+                      (DIM == 3 ? (n1 + T::TZ - 1) / T::TZ : 1);
+    // chunk: enough CTAs for ~8 per SM, at least 4 steps to amortise the warm-up
+    i64 C = 64;
+    while (C > 4 && tiles * ((L.n_t + C - 1) / C) < 148 * 8) C /= 2;
+    C = std::min<i64>(C, L.n_t);
+    const dim3 g(unsigned(tiles), unsigned((L.n_t + C - 1) / C));
     const TM<NL> t = make_tm<NL>(L.tc);
+    const size_t smem = 2 * size_t(NL) * T::HALO * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_apply<DIM, NL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(smem));
+      cudaFuncSetAttribute(k_apply<DIM, NL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(smem));
+      attr = true;
+    }
     if (residual)
-      k_apply<DIM, NL, true><<<g, 256, 0, st>>>(u, f, y, t, L.sp.n1, L.sp.nx, L.sp.h, L.n_t,
-                                                 L.first_global);
+      k_apply<DIM, NL, true><<<g, T::THREADS, smem, st>>>(u, f, y, t, n1, L.sp.nx, L.sp.h, L.n_t,
+                                                           int(C), L.first_global, ab);
     else
-      k_apply<DIM, NL, false><<<g, 256, 0, st>>>(u, f, y, t, L.sp.n1, L.sp.nx, L.sp.h, L.n_t,
-                                                  L.first_global);
+      k_apply<DIM, NL, false><<<g, T::THREADS, smem, st>>>(u, f, y, t, n1, L.sp.nx, L.sp.h,
+                                                            L.n_t, int(C), L.first_global, ab);
   });
   return cudaGetLastError();
 }

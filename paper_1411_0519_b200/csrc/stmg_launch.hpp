@@ -44,8 +44,9 @@ struct LevelView {
 };
 
 // ---- physical-space operators (nodal values) ------------------------------
+// ab: device array [a_0..a_{kMaxNL}), [b_0..) with N_tau = a b^T.
 cudaError_t launch_apply(const LevelView& L, const double* u, const double* f,
-                         double* y, bool residual, cudaStream_t st);
+                         double* y, bool residual, const double* ab, cudaStream_t st);
 cudaError_t launch_restrict(const LevelView& F, int mode, int64_t n1c,
                             const double* fine, double* coarse, cudaStream_t st);
 cudaError_t launch_prolong(const LevelView& F, int mode, int64_t n1c,
