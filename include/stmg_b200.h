@@ -62,6 +62,8 @@ typedef struct {
   int policy;       /* STMG_POLICY_* */
   int two_grid;     /* 0: full ladder; STMG_COARSEN_SEMI/FULL: build_two_grid */
   int device;       /* CUDA device ordinal */
+  int shards;       /* >1: time-slab sharding emulated on this device (same
+                       halo/gather/scatter logic as the multi-GPU path) */
 } stmg_hierarchy_params;
 
 /* CycleConfig + SmootherConfig (mg.hpp:66-71, smoother.hpp:15-24). */
@@ -162,6 +164,23 @@ int stmg_solve(stmg_ctx* ctx, const double* f, double* u,
 int stmg_solve_host(stmg_ctx* ctx, const double* f_host, double* u_host,
                     const stmg_cycle_config* cfg, double eps, int max_iter,
                     double* history, int history_cap, stmg_solve_report* report);
+
+/* ---- multi-GPU: time slabs over ranks (one process per GPU, NCCL) ------- */
+/* 128-byte NCCL unique id, created on rank 0 and broadcast by the caller. */
+int stmg_nccl_unique_id(void* out, size_t len);
+/* Context owning time steps [rank*n_t/world, (rank+1)*n_t/world) of the finest
+ * level; stmg_solve / stmg_solve_host then take this rank's slabs of f and u.
+ * Coarse levels with fewer than 2 steps per rank run on rank 0. */
+int stmg_create_distributed(const stmg_hierarchy_params* params, int rank,
+                            int world, const void* nccl_id, size_t id_len,
+                            stmg_ctx** out);
+/* Sharding plan (host only, no GPU needed): first level gathered onto rank 0
+ * and finest-level steps per shard. */
+int stmg_shard_plan(const stmg_hierarchy_params* params, int shards,
+                    int* gather_level, int64_t* steps_per_shard);
+/* Finest-level time steps owned by this context. */
+int stmg_local_steps(const stmg_ctx* ctx, int64_t* first_step,
+                     int64_t* n_steps);
 
 /* ---- live per-kernel timing (CUDA events inside the cycle) --------------- */
 /* Kernel ids: 0 = fused pre-smooth+residual+restrict on the finest level,

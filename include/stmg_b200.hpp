@@ -88,6 +88,7 @@ struct HierarchyParams {
   CoarseningPolicy policy = CoarseningPolicy::mu_driven;
   BlockSolverKind block_solver = BlockSolverKind::exact;
   int device = 0;
+  int shards = 0;  // >1: time-slab sharding emulated on one device
 };
 
 // smoother.hpp:15-24
@@ -167,6 +168,7 @@ inline stmg_hierarchy_params to_c(const HierarchyParams& p, int two_grid) {
   c.policy = int(p.policy);
   c.two_grid = two_grid;
   c.device = p.device;
+  c.shards = p.shards;
   return c;
 }
 

@@ -23,7 +23,8 @@ VP = C.c_void_p
 class HierarchyParams(C.Structure):
     _fields_ = [("p_t", C.c_int), ("dim", C.c_int), ("space_level", C.c_int),
                 ("time_level", C.c_int), ("t_final", D), ("mu_star", D),
-                ("policy", C.c_int), ("two_grid", C.c_int), ("device", C.c_int)]
+                ("policy", C.c_int), ("two_grid", C.c_int), ("device", C.c_int),
+                ("shards", C.c_int)]
 
 
 class CycleConfig(C.Structure):
@@ -77,6 +78,12 @@ SIGNATURES = [
                              C.POINTER(SolveReport)]),
     ("stmg_solve_host", C.c_int, [VP, VP, VP, C.POINTER(CycleConfig), D, C.c_int, PD, C.c_int,
                                   C.POINTER(SolveReport)]),
+    ("stmg_nccl_unique_id", C.c_int, [VP, C.c_size_t]),
+    ("stmg_create_distributed", C.c_int, [C.POINTER(HierarchyParams), C.c_int, C.c_int, VP,
+                                          C.c_size_t, C.POINTER(VP)]),
+    ("stmg_shard_plan", C.c_int, [C.POINTER(HierarchyParams), C.c_int, C.POINTER(C.c_int),
+                                  C.POINTER(C.c_int64)]),
+    ("stmg_local_steps", C.c_int, [VP, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("stmg_profile_enable", C.c_int, [VP, C.c_int]),
     ("stmg_profile_read", C.c_int, [VP, C.c_int, PD, C.POINTER(C.c_int64), PD]),
     ("stmg_profile_reset", C.c_int, [VP]),

@@ -13,6 +13,8 @@
 // values, one kernel family per reference entry point; used for the operator
 // API and as a second GPU implementation in the parity tests.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <chrono>
 #include <cmath>
@@ -103,8 +105,13 @@ struct ProfSlot {
 
 }  // namespace
 
+namespace {
+struct ShardSet;
+}
+
 struct stmg_ctx {
   int device = 0;
+  std::unique_ptr<ShardSet> shards;  // time-slab sharding (virtual or NCCL)
   cudaStream_t stream = nullptr;
   std::vector<Level> levels;
   int p_t = 0, dim = 1;
@@ -423,24 +430,59 @@ void ensure_spectral(stmg_ctx* c, int from_level) {
 // memory runs inside the single-CTA tail kernel.
 constexpr i64 kTailSmemBytes = 184 * 1024;
 
-void ensure_tail(stmg_ctx* c) {
-  if (c->tail_table || c->tail_start == 0) return;
-  const int nl = int(c->levels.size());
-  int start = nl;  // first level of the small suffix
+// First level of the small suffix that runs in the tail kernel (0: none),
+// from the level vector sizes (doubles).
+int tail_start_from(const std::vector<i64>& sizes, i64* bytes_out) {
+  const int nl = int(sizes.size());
+  int start = nl;
   i64 bytes = 0;
   while (start - 1 >= 1) {
-    const i64 b = 24 * c->levels[start - 1].view.size();
+    const i64 b = 24 * sizes[start - 1];
     if (bytes + b > kTailSmemBytes || nl - (start - 1) > 24) break;
     bytes += b;
     --start;
   }
-  if (start >= nl) {
+  if (bytes_out) *bytes_out = bytes;
+  return start >= nl ? 0 : start;
+}
+
+int tail_start_of(const stmg_ctx* c, i64* bytes_out) {
+  std::vector<i64> sizes;
+  for (const Level& L : c->levels) sizes.push_back(L.view.size());
+  return tail_start_from(sizes, bytes_out);
+}
+
+// Gather level of a ladder for S shards: first level with fewer than 2 steps
+// per shard, or the first tail level if that comes earlier.
+int gather_level_of(const std::vector<stmg::LevelSpec>& specs, int S) {
+  const int nl = int(specs.size());
+  int lg = nl - 1;
+  for (int l = 0; l < nl; ++l)
+    if (specs[l].n_t < 2 * S) {
+      lg = l;
+      break;
+    }
+  std::vector<i64> sizes;
+  for (const auto& L : specs) sizes.push_back(L.size());
+  const int ts = tail_start_from(sizes, nullptr);
+  if (ts > 0) lg = std::min(lg, ts);
+  return lg;
+}
+
+// Build the tail's device table (the buffers of levels >= start must exist).
+void ensure_tail(stmg_ctx* c) {
+  if (c->tail_table || c->tail_start == 0) return;
+  const int nl = int(c->levels.size());
+  i64 bytes = 0;
+  const int start = tail_start_of(c, &bytes);
+  if (start == 0) {
     c->tail_start = 0;  // not even the coarsest fits: per-level path
     return;
   }
   std::vector<stmg::TailSpec> spec(nl - start);
   for (int l = start; l < nl; ++l) {
     Level& L = c->levels[l];
+    require(L.F.base != nullptr, "internal: tail buffers not allocated");
     stmg::TailSpec& t = spec[l - start];
     t.view = L.view;
     t.mode = L.spec.coarsen;
@@ -678,6 +720,494 @@ void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config
   if (rep) *rep = r;
 }
 
+// ======================================================= time-slab sharding
+// Level l < lg of the hierarchy is split into S contiguous time slabs (one per
+// shard); the rest (l >= lg, small) is gathered onto shard 0 ("root").  Each
+// fused kernel on a sharded level needs the end-of-slab halo of its left
+// neighbour (2 u slabs, 1 f slab, 1 coarse e slab), which lands in the halo
+// slabs in front of every buffer.  Norm partials are concatenated in global
+// chunk order, so iterates AND norms are bitwise identical for any S.
+// Transports: virtual shards on one device (D2D copies on the ctx stream) or
+// one rank per GPU over NCCL (send/recv, all-gather; dlopen'ed, graph-capturable).
+struct NcclApi {
+  void* h = nullptr;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
+  decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclGetErrorString) ErrStr = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  if (api.h) return api;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) throw std::runtime_error(std::string("cannot load NCCL: ") + dlerror());
+  auto sym = [&](const char* n) {
+    void* p = dlsym(h, n);
+    if (!p) throw std::runtime_error(std::string("NCCL symbol missing: ") + n);
+    return p;
+  };
+  api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+  api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+  api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+  api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+  api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+  api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+  api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+  api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+  api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+  api.ErrStr = reinterpret_cast<decltype(api.ErrStr)>(sym("ncclGetErrorString"));
+  api.h = h;
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw std::runtime_error(std::string("NCCL error in ") + what + ": " + nccl().ErrStr(r));
+}
+
+struct ShardLevel {
+  stmg::LevelView view;  // local n_t, first_global
+  DevBuf F, U[2];
+};
+
+struct Shard {
+  int g = 0;  // global shard index
+  std::vector<ShardLevel> lv;  // sharded levels 0..lg-1
+  std::vector<int> cur;
+  DevBuf Fg;  // local part of F_lg (written by down(lg-1))
+  DevBuf Eg;  // local part of the coarse correction at lg (+1 halo slab)
+};
+
+struct ShardSet {
+  int S = 1;
+  int lg = 0;  // first gathered level
+  bool nccl = false;
+  ncclComm_t comm = nullptr;
+  std::vector<Shard> local;  // virtual: all S shards; nccl: this rank's
+  DevBuf partials;           // S * P partial sums (global chunk order)
+  i64 P = 0;                 // partials per shard (level-0 residual)
+  i64 m = 0;                 // coarse steps per shard at lg
+  bool built = false;
+};
+
+bool is_root(const ShardSet& ss, const Shard& sh) { return sh.g == 0; }
+
+int gather_level(stmg_ctx* c, int S) {
+  std::vector<stmg::LevelSpec> specs;
+  for (const Level& L : c->levels) specs.push_back(L.spec);
+  return gather_level_of(specs, S);
+}
+
+// Chunk of a sharded level: the single-shard choice, so partial sums line up.
+int shard_chunk(const Level& G, const stmg::LevelView& local, bool grouped) {
+  int ch = stmg::pick_chunk(G.view, grouped);
+  while (ch > 2 && (local.n_t % ch) != 0) ch /= 2;
+  return int(std::min<i64>(ch, local.n_t));
+}
+
+void build_shards(stmg_ctx* c) {
+  ShardSet& ss = *c->shards;
+  if (ss.built) return;
+  ss.lg = gather_level(c, ss.S);
+  require(ss.lg >= 1, "too few time steps for this many shards (need >= 2 per shard)");
+  const int lg = ss.lg;
+  ss.m = c->levels[lg].spec.n_t / ss.S;
+  require(ss.m >= 1 && ss.m * ss.S == c->levels[lg].spec.n_t, "time steps do not split evenly");
+  for (Shard& sh : ss.local) {
+    sh.lv.resize(lg);
+    sh.cur.assign(lg, 0);
+    for (int l = 0; l < lg; ++l) {
+      ShardLevel& s = sh.lv[l];
+      s.view = c->levels[l].view;
+      s.view.n_t = c->levels[l].spec.n_t / ss.S;
+      s.view.first_global = sh.g == 0;
+      const i64 n = s.view.size(), halo = 2 * s.view.slab();
+      s.F.alloc(n, halo);
+      s.U[0].alloc(n, halo);
+      s.U[1].alloc(n, halo);
+    }
+    const i64 cslab = c->levels[lg].view.slab();
+    sh.Fg.alloc(ss.m * cslab, 2 * cslab);
+    sh.Eg.alloc(ss.m * cslab, 2 * cslab);
+  }
+  // root holds the gathered levels (full size)
+  bool have_root = false;
+  for (Shard& sh : ss.local) have_root |= sh.g == 0;
+  if (have_root) {
+    ensure_spectral(c, lg);
+    ensure_tail(c);
+  }
+  if (int(c->cur.size()) != int(c->levels.size())) c->cur.assign(c->levels.size(), 0);
+  // level-0 residual partials per shard
+  {
+    const stmg::LevelView& v = ss.local[0].lv[0].view;
+    const i64 G = (v.sp.n1 + 1) / 2;
+    i64 lanes = 1;
+    for (int a = 0; a < v.sp.dim; ++a) lanes *= 2 * G;
+    const i64 bx = (std::max(lanes, v.sp.nx) + 127) / 128;
+    const int ch = std::min(shard_chunk(c->levels[0], v, true), shard_chunk(c->levels[0], v, false));
+    ss.P = bx * ((v.n_t + ch - 1) / ch);
+  }
+  ss.partials.alloc(ss.S * ss.P + 16, 0);
+  ss.built = true;
+}
+
+// Copy the last `ns` slabs of every shard's buffer into its right
+// neighbour's halo.  get(sh) -> the buffer base of that shard.
+template <class Get>
+void halo(stmg_ctx* c, i64 n_loc, i64 slab, int ns, Get get) {
+  ShardSet& ss = *c->shards;
+  const size_t bytes = size_t(ns) * size_t(slab) * sizeof(double);
+  if (!ss.nccl) {
+    for (size_t i = 1; i < ss.local.size(); ++i) {
+      double* dst = get(ss.local[i]) - ns * slab;
+      const double* src = get(ss.local[i - 1]) + (n_loc - ns) * slab;
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    return;
+  }
+  Shard& sh = ss.local[0];
+  NcclApi& N = nccl();
+  nccl_check(N.GroupStart(), "group start");
+  if (sh.g + 1 < ss.S)
+    nccl_check(N.Send(get(sh) + (n_loc - ns) * slab, size_t(ns) * slab, ncclDouble, sh.g + 1,
+                      ss.comm, c->stream), "halo send");
+  if (sh.g > 0)
+    nccl_check(N.Recv(get(sh) - ns * slab, size_t(ns) * slab, ncclDouble, sh.g - 1, ss.comm,
+                      c->stream), "halo recv");
+  nccl_check(N.GroupEnd(), "group end");
+}
+
+// Fg of every shard -> root's full F at lg.
+void gather_rhs(stmg_ctx* c) {
+  ShardSet& ss = *c->shards;
+  const i64 cslab = c->levels[ss.lg].view.slab();
+  const size_t bytes = size_t(ss.m * cslab) * sizeof(double);
+  if (!ss.nccl) {
+    double* F = c->levels[ss.lg].F.base;
+    for (Shard& sh : ss.local)
+      CK(cudaMemcpyAsync(F + sh.g * ss.m * cslab, sh.Fg.base, bytes, cudaMemcpyDeviceToDevice,
+                         c->stream));
+    return;
+  }
+  Shard& sh = ss.local[0];
+  NcclApi& N = nccl();
+  nccl_check(N.GroupStart(), "group start");
+  if (sh.g == 0) {
+    double* F = c->levels[ss.lg].F.base;
+    CK(cudaMemcpyAsync(F, sh.Fg.base, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    for (int g = 1; g < ss.S; ++g)
+      nccl_check(N.Recv(F + g * ss.m * cslab, size_t(ss.m * cslab), ncclDouble, g, ss.comm,
+                        c->stream), "gather recv");
+  } else {
+    nccl_check(N.Send(sh.Fg.base, size_t(ss.m * cslab), ncclDouble, 0, ss.comm, c->stream),
+               "gather send");
+  }
+  nccl_check(N.GroupEnd(), "group end");
+}
+
+// root's coarse correction at lg -> every shard's Eg (+ the step before).
+void scatter_corr(stmg_ctx* c) {
+  ShardSet& ss = *c->shards;
+  const i64 cslab = c->levels[ss.lg].view.slab();
+  auto src_of = [&](int g) {
+    const double* E = c->levels[ss.lg].U[c->cur[ss.lg]].base;
+    return E + (g * ss.m - (g > 0 ? 1 : 0)) * cslab;
+  };
+  auto count_of = [&](int g) { return size_t((ss.m + (g > 0 ? 1 : 0)) * cslab); };
+  auto dst_of = [&](Shard& sh) { return sh.Eg.base - (sh.g > 0 ? cslab : 0); };
+  if (!ss.nccl) {
+    for (Shard& sh : ss.local)
+      CK(cudaMemcpyAsync(dst_of(sh), src_of(sh.g), count_of(sh.g) * sizeof(double),
+                         cudaMemcpyDeviceToDevice, c->stream));
+    return;
+  }
+  Shard& sh = ss.local[0];
+  NcclApi& N = nccl();
+  nccl_check(N.GroupStart(), "group start");
+  if (sh.g == 0) {
+    CK(cudaMemcpyAsync(dst_of(sh), src_of(0), count_of(0) * sizeof(double),
+                       cudaMemcpyDeviceToDevice, c->stream));
+    for (int g = 1; g < ss.S; ++g)
+      nccl_check(N.Send(src_of(g), count_of(g), ncclDouble, g, ss.comm, c->stream),
+                 "scatter send");
+  } else {
+    nccl_check(N.Recv(dst_of(sh), count_of(sh.g), ncclDouble, 0, ss.comm, c->stream),
+               "scatter recv");
+  }
+  nccl_check(N.GroupEnd(), "group end");
+}
+
+void allgather_partials(stmg_ctx* c) {
+  ShardSet& ss = *c->shards;
+  if (!ss.nccl) return;  // virtual shards write their segments in place
+  NcclApi& N = nccl();
+  const Shard& sh = ss.local[0];
+  nccl_check(N.AllGather(ss.partials.base + sh.g * ss.P, ss.partials.base, size_t(ss.P),
+                         ncclDouble, ss.comm, c->stream), "partials all-gather");
+}
+
+stmg::ModalArgs shard_args(stmg_ctx* c, int l, const ShardLevel& s, double omega, bool grouped) {
+  stmg::ModalArgs a;
+  a.omega = omega;
+  a.chunk = shard_chunk(c->levels[l], s.view, grouped);
+  a.mode = c->levels[l].spec.coarsen ? c->levels[l].spec.coarsen : 1;
+  a.n1c = c->levels[l + 1].spec.n1();
+  return a;
+}
+
+// One V-cycle (gamma = 1) over the sharded levels + the root's tail, plus the
+// residual norm into d_norm (and h_norm).
+void sharded_cycle(stmg_ctx* c, const stmg_cycle_config& cfg) {
+  ShardSet& ss = *c->shards;
+  const int lg = ss.lg;
+  const int nu1 = cfg.nu1, nu2 = cfg.nu2;
+  for (int l = 0; l < lg; ++l) {
+    const stmg::LevelView& v = ss.local[0].lv[l].view;
+    const i64 n_loc = v.n_t, slab = v.slab();
+    bool zero = l > 0;
+    if (zero)
+      for (Shard& sh : ss.local) sh.cur[l] = 0;
+    if (l > 0) halo(c, n_loc, slab, 1, [&](Shard& sh) { return sh.lv[l].F.base; });
+    for (int s = 0; s + 1 < nu1; ++s) {
+      if (!zero) halo(c, n_loc, slab, 1, [&](Shard& sh) { return sh.lv[l].U[sh.cur[l]].base; });
+      for (Shard& sh : ss.local) {
+        ShardLevel& L = sh.lv[l];
+        stmg::ModalArgs a = shard_args(c, l, L, cfg.omega_t, false);
+        CK(stmg::launch_smooth(L.view, a, zero, L.F.base, L.U[sh.cur[l]].base,
+                               L.U[1 - sh.cur[l]].base, c->stream));
+        count(c);
+        sh.cur[l] ^= 1;
+      }
+      zero = false;
+    }
+    if (!zero) halo(c, n_loc, slab, 2, [&](Shard& sh) { return sh.lv[l].U[sh.cur[l]].base; });
+    for (Shard& sh : ss.local) {
+      ShardLevel& L = sh.lv[l];
+      stmg::ModalArgs a = shard_args(c, l, L, cfg.omega_t, true);
+      double* fc = (l + 1 < lg) ? sh.lv[l + 1].F.base : sh.Fg.base;
+      const bool p = l == 0 && sh.g == 0;
+      if (p) prof_begin(c, 0);
+      CK(stmg::launch_down(L.view, a, zero, L.F.base, L.U[sh.cur[l]].base, L.U[1 - sh.cur[l]].base,
+                           fc, c->stream));
+      if (p) prof_end(c, 0, 8.0 * double((zero ? 2 : 3) * L.view.size() + L.view.size() / 8));
+      count(c);
+      sh.cur[l] ^= 1;
+    }
+  }
+  gather_rhs(c);
+  bool have_root = false;
+  for (Shard& sh : ss.local) have_root |= sh.g == 0;
+  if (have_root) {
+    if (c->tail_table && lg == c->tail_start) {
+      CK(stmg::launch_tail(c->dim, c->p_t + 1, c->tail_table, int(c->levels.size()) - lg,
+                           cfg.omega_t, c->tail_smem, c->stream));
+      count(c);
+      for (int l = lg; l < int(c->levels.size()); ++l) c->cur[l] = 0;
+    } else {
+      spectral_cycle(c, lg, true, cfg, false, nullptr);
+    }
+  }
+  scatter_corr(c);
+  for (int l = lg - 1; l >= 0; --l) {
+    const stmg::LevelView& v = ss.local[0].lv[l].view;
+    const i64 n_loc = v.n_t, slab = v.slab();
+    if (l + 1 < lg) {
+      const stmg::LevelView& vc = ss.local[0].lv[l + 1].view;
+      halo(c, vc.n_t, vc.slab(), 1,
+           [&](Shard& sh) { return sh.lv[l + 1].U[sh.cur[l + 1]].base; });
+    }
+    halo(c, n_loc, slab, 2, [&](Shard& sh) { return sh.lv[l].U[sh.cur[l]].base; });
+    const bool resid = l == 0 && nu2 == 1;
+    for (Shard& sh : ss.local) {
+      ShardLevel& L = sh.lv[l];
+      stmg::ModalArgs a = shard_args(c, l, L, cfg.omega_t, true);
+      const double* ec = (l + 1 < lg) ? sh.lv[l + 1].U[sh.cur[l + 1]].base : sh.Eg.base;
+      const bool p = l == 0 && sh.g == 0;
+      if (p) prof_begin(c, 1);
+      CK(stmg::launch_up(L.view, a, ec, L.U[sh.cur[l]].base, L.F.base, L.U[1 - sh.cur[l]].base,
+                         resid ? ss.partials.base + sh.g * ss.P : nullptr, c->stream));
+      if (p) prof_end(c, 1, 8.0 * double(3 * L.view.size() + L.view.size() / 8));
+      count(c);
+      if (resid) require(a.n_partials == ss.P, "partial count mismatch");
+      sh.cur[l] ^= 1;
+    }
+    for (int s = 1; s < nu2; ++s) {
+      halo(c, n_loc, slab, 1, [&](Shard& sh) { return sh.lv[l].U[sh.cur[l]].base; });
+      for (Shard& sh : ss.local) {
+        ShardLevel& L = sh.lv[l];
+        stmg::ModalArgs a = shard_args(c, l, L, cfg.omega_t, false);
+        CK(stmg::launch_smooth(L.view, a, false, L.F.base, L.U[sh.cur[l]].base,
+                               L.U[1 - sh.cur[l]].base, c->stream));
+        count(c);
+        sh.cur[l] ^= 1;
+      }
+    }
+    if (l == 0 && !resid) {
+      halo(c, n_loc, slab, 1, [&](Shard& sh) { return sh.lv[0].U[sh.cur[0]].base; });
+      for (Shard& sh : ss.local) {
+        ShardLevel& L = sh.lv[0];
+        stmg::ModalArgs a = shard_args(c, 0, L, cfg.omega_t, false);
+        CK(stmg::launch_resnorm(L.view, a, L.U[sh.cur[0]].base, L.F.base,
+                                ss.partials.base + sh.g * ss.P, c->stream));
+        count(c);
+        require(a.n_partials == ss.P, "partial count mismatch");
+      }
+    }
+  }
+  allgather_partials(c);
+  CK(stmg::launch_norm_final(ss.partials.base, ss.S * ss.P, c->d_norm, nullptr, 0, c->stream));
+  count(c);
+  CK(cudaMemcpyAsync(c->h_norm, c->d_norm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+}
+
+// Sharded solve: f, u are this process's time slabs (virtual shards: the whole
+// vectors, split here).
+void solve_sharded(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config& cfg,
+                   double eps, int max_iter, double* history, int history_cap,
+                   stmg_solve_report* rep) {
+  require(eps > 0.0, "eps_mg must be positive");
+  require(f != nullptr && u != nullptr, "null vector");
+  require(max_iter >= 0, "max_iter must be >= 0");
+  require(cfg.path == STMG_PATH_SPECTRAL, "sharded solves run on the spectral path");
+  require(cfg.gamma == 1 && cfg.nu1 >= 1 && cfg.nu2 >= 1,
+          "sharded solves support V(nu1, nu2) cycles with nu1, nu2 >= 1");
+  build_shards(c);
+  ShardSet& ss = *c->shards;
+  stmg_solve_report r{};
+  int nh = 0;
+  auto push = [&](double v) {
+    if (history && nh < history_cap) history[nh] = v;
+    ++nh;
+  };
+  CK(cudaStreamSynchronize(c->stream));
+  const auto t0 = std::chrono::steady_clock::now();
+  CK(cudaEventRecord(c->ev_solve[0], c->stream));
+  const i64 nloc0 = ss.local[0].lv[0].view.size();
+  auto part = [&](const Shard& sh) { return ss.nccl ? 0 : sh.g * nloc0; };
+  // zero initial guess detection (OR over shards)
+  CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+  for (Shard& sh : ss.local) {
+    CK(stmg::launch_nonzero(u + part(sh), nloc0, c->d_flag, c->stream));
+    count(c);
+  }
+  if (ss.nccl)
+    nccl_check(nccl().AllReduce(c->d_flag, c->d_flag, 1, ncclInt32, ncclMax, ss.comm, c->stream),
+               "flag all-reduce");
+  CK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  for (Shard& sh : ss.local) {
+    ShardLevel& L = sh.lv[0];
+    for (int a = 0; a < c->dim; ++a) {
+      CK(stmg::launch_dst_axis(L.view, a, a == 0 ? f + part(sh) : L.F.base, L.F.base, false, 1.0,
+                               c->levels[0].d_twiddle, c->stream));
+      count(c);
+    }
+    sh.cur[0] = 0;
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  const bool u_nonzero = *c->h_flag != 0;
+  for (Shard& sh : ss.local) {
+    ShardLevel& L = sh.lv[0];
+    if (u_nonzero) {
+      for (int a = 0; a < c->dim; ++a) {
+        CK(stmg::launch_dst_axis(L.view, a, a == 0 ? u + part(sh) : L.U[0].base, L.U[0].base,
+                                 false, 1.0, c->levels[0].d_twiddle, c->stream));
+        count(c);
+      }
+    } else {
+      CK(cudaMemsetAsync(L.U[0].base, 0, size_t(nloc0) * sizeof(double), c->stream));
+    }
+  }
+  const stmg::LevelView& v0 = ss.local[0].lv[0].view;
+  halo(c, v0.n_t, v0.slab(), 1, [&](Shard& sh) { return sh.lv[0].F.base; });
+  halo(c, v0.n_t, v0.slab(), 1, [&](Shard& sh) { return sh.lv[0].U[0].base; });
+  for (Shard& sh : ss.local) {
+    ShardLevel& L = sh.lv[0];
+    stmg::ModalArgs a = shard_args(c, 0, L, cfg.omega_t, false);
+    CK(stmg::launch_resnorm(L.view, a, L.U[0].base, L.F.base, ss.partials.base + sh.g * ss.P,
+                            c->stream));
+    count(c);
+    require(a.n_partials == ss.P, "partial count mismatch");
+  }
+  allgather_partials(c);
+  CK(stmg::launch_norm_final(ss.partials.base, ss.S * ss.P, c->d_norm, nullptr, 0, c->stream));
+  count(c);
+  CK(cudaMemcpyAsync(c->h_norm, c->d_norm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  const double r0 = *c->h_norm;
+  r.r0 = r.r_final = r0;
+  push(r0);
+  if (r0 == 0.0) r.converged = 1;
+  for (int k = 0; k < max_iter && !r.converged; ++k) {
+    // the cycle's buffer parity pattern is the same every iteration (coarse
+    // levels restart at buffer 0) except the finest level's, so at most two
+    // graphs; key on shard 0's finest parity
+    stmg_ctx::GraphKey key{cfg.nu1, cfg.nu2, -1 - ss.local[0].cur[0], 0, cfg.omega_t};
+    auto it = c->graphs.find(key);
+    if (it == c->graphs.end()) {
+      std::vector<int> cur0(ss.local.size());
+      for (size_t i = 0; i < ss.local.size(); ++i) cur0[i] = ss.local[i].cur[0];
+      cudaGraph_t graph;
+      c->capturing = true;
+      c->captured_kernels = 0;
+      CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        sharded_cycle(c, cfg);
+      } catch (...) {
+        cudaStreamEndCapture(c->stream, &graph);
+        c->capturing = false;
+        throw;
+      }
+      CK(cudaStreamEndCapture(c->stream, &graph));
+      c->capturing = false;
+      stmg_ctx::GraphEntry e;
+      CK(cudaGraphInstantiate(&e.exec, graph, 0));
+      CK(cudaGraphDestroy(graph));
+      e.cur0_after = ss.local[0].cur[0];
+      e.kernels = c->captured_kernels;
+      for (size_t i = 0; i < ss.local.size(); ++i) ss.local[i].cur[0] = cur0[i];
+      it = c->graphs.emplace(key, e).first;
+    }
+    CK(cudaGraphLaunch(it->second.exec, c->stream));
+    c->launches += it->second.kernels;
+    CK(cudaStreamSynchronize(c->stream));
+    prof_collect_graph(c);
+    for (Shard& sh : ss.local) sh.cur[0] = it->second.cur0_after;
+    const double rk = *c->h_norm;
+    push(rk);
+    r.r_final = rk;
+    ++r.iterations;
+    if (rk <= eps * r0) r.converged = 1;
+  }
+  for (Shard& sh : ss.local) {
+    ShardLevel& L = sh.lv[0];
+    for (int a = 0; a < c->dim; ++a) {
+      CK(stmg::launch_dst_axis(L.view, a, a == 0 ? L.U[sh.cur[0]].base : u + part(sh),
+                               u + part(sh), false, 1.0, c->levels[0].d_twiddle, c->stream));
+      count(c);
+    }
+  }
+  CK(cudaEventRecord(c->ev_solve[1], c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  prof_collect(c);
+  {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev_solve[0], c->ev_solve[1]));
+    r.device_time_seconds = 1e-3 * double(ms);
+  }
+  r.wall_time_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (rep) *rep = r;
+}
+
 }  // namespace
 
 // =================================================================== C ABI
@@ -714,6 +1244,7 @@ int stmg_time_transfer(int p_t, double tau, double* R1, double* R2) {
 int stmg_create(const stmg_hierarchy_params* p, stmg_ctx** out) {
   return guard([&] {
     require(p != nullptr && out != nullptr, "null argument");
+    require(p->shards >= 0 && p->shards <= 4096, "shard count out of range");
     *out = nullptr;
     auto specs = stmg::build_ladder(p->p_t, p->dim, p->space_level, p->time_level, p->t_final,
                                     p->mu_star, p->policy, p->two_grid);
@@ -734,6 +1265,12 @@ int stmg_create(const stmg_hierarchy_params* p, stmg_ctx** out) {
     for (size_t i = 0; i < specs.size(); ++i) {
       c->levels[i].spec = specs[i];
       build_level_tables(c->levels[i]);
+    }
+    if (p->shards > 1) {
+      c->shards = std::make_unique<ShardSet>();
+      c->shards->S = p->shards;
+      c->shards->local.resize(p->shards);
+      for (int g = 0; g < p->shards; ++g) c->shards->local[g].g = g;
     }
     CK(cudaMalloc(&c->d_norm, sizeof(double)));
     CK(cudaMallocHost(&c->h_norm, sizeof(double)));
@@ -756,6 +1293,17 @@ int stmg_destroy(stmg_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
+    if (c->shards) {
+      for (Shard& sh : c->shards->local) {
+        for (ShardLevel& L : sh.lv)
+          for (DevBuf* b : {&L.F, &L.U[0], &L.U[1]}) b->release();
+        sh.Fg.release();
+        sh.Eg.release();
+      }
+      c->shards->partials.release();
+      if (c->shards->comm) nccl().CommDestroy(c->shards->comm);
+      c->shards.reset();
+    }
     for (auto& L : c->levels) {
       cudaFree(L.d_tables);
       cudaFree(L.d_twiddle);
@@ -992,7 +1540,8 @@ int stmg_solve(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config*
   return guard([&] {
     require(c != nullptr, "null context");
     check_cfg(cfg);
-    solve_impl(c, f, u, *cfg, eps, max_iter, history, history_cap, report);
+    if (c->shards) solve_sharded(c, f, u, *cfg, eps, max_iter, history, history_cap, report);
+    else solve_impl(c, f, u, *cfg, eps, max_iter, history, history_cap, report);
   });
 }
 
@@ -1004,7 +1553,7 @@ int stmg_solve_host(stmg_ctx* c, const double* f_host, double* u_host,
     check_cfg(cfg);
     require(f_host && u_host, "null vector");
     Level& L0 = c->levels[0];
-    const i64 n = L0.view.size();
+    const i64 n = (c->shards && c->shards->nccl) ? L0.view.size() / c->shards->S : L0.view.size();
     ensure(c->user_f, n);
     ensure(c->user_u, n);
     const auto t0 = std::chrono::steady_clock::now();
@@ -1013,13 +1562,86 @@ int stmg_solve_host(stmg_ctx* c, const double* f_host, double* u_host,
     CK(cudaMemcpyAsync(c->user_u.base, u_host, size_t(n) * sizeof(double), cudaMemcpyHostToDevice,
                        c->stream));
     stmg_solve_report r{};
-    solve_impl(c, c->user_f.base, c->user_u.base, *cfg, eps, max_iter, history, history_cap, &r);
+    if (c->shards)
+      solve_sharded(c, c->user_f.base, c->user_u.base, *cfg, eps, max_iter, history, history_cap,
+                    &r);
+    else
+      solve_impl(c, c->user_f.base, c->user_u.base, *cfg, eps, max_iter, history, history_cap, &r);
     CK(cudaMemcpyAsync(u_host, c->user_u.base, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
                        c->stream));
     CK(cudaStreamSynchronize(c->stream));
     r.wall_time_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (report) *report = r;
+  });
+}
+
+int stmg_nccl_unique_id(void* out, size_t len) {
+  return guard([&] {
+    require(out != nullptr && len >= sizeof(ncclUniqueId), "buffer too small for an NCCL id");
+    ncclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id), "get unique id");
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+int stmg_create_distributed(const stmg_hierarchy_params* p, int rank, int world,
+                            const void* nccl_id, size_t id_len, stmg_ctx** out) {
+  return guard([&] {
+    require(p && out && nccl_id, "null argument");
+    require(world >= 1 && rank >= 0 && rank < world, "rank/world out of range");
+    require(id_len >= sizeof(ncclUniqueId), "NCCL id too short");
+    stmg_hierarchy_params q = *p;
+    q.shards = 0;
+    stmg_ctx* c = nullptr;
+    const int rc = stmg_create(&q, &c);
+    if (rc != STMG_OK) {
+      if (rc == STMG_EINVAL) throw std::invalid_argument(g_err);
+      throw std::runtime_error(g_err);
+    }
+    std::unique_ptr<stmg_ctx, int (*)(stmg_ctx*)> hold(c, stmg_destroy);
+    if (world > 1) {
+      c->shards = std::make_unique<ShardSet>();
+      c->shards->S = world;
+      c->shards->nccl = true;
+      c->shards->local.resize(1);
+      c->shards->local[0].g = rank;
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      CK(cudaSetDevice(c->device));
+      nccl_check(nccl().CommInitRank(&c->shards->comm, world, id, rank), "comm init");
+      build_shards(c);
+    }
+    *out = hold.release();
+  });
+}
+
+int stmg_shard_plan(const stmg_hierarchy_params* p, int shards, int* gather_level,
+                    int64_t* steps_per_shard) {
+  return guard([&] {
+    require(p && gather_level && steps_per_shard, "null argument");
+    require(shards >= 1, "shard count must be >= 1");
+    const auto specs = stmg::build_ladder(p->p_t, p->dim, p->space_level, p->time_level,
+                                          p->t_final, p->mu_star, p->policy, p->two_grid);
+    const int lg = gather_level_of(specs, shards);
+    require(shards == 1 || lg >= 1, "too few time steps for this many shards (need >= 2 per shard)");
+    *gather_level = lg;
+    *steps_per_shard = specs[0].n_t / shards;
+  });
+}
+
+int stmg_local_steps(const stmg_ctx* c, int64_t* first_step, int64_t* n_steps) {
+  return guard([&] {
+    require(c && first_step && n_steps, "null argument");
+    const i64 nt = c->levels[0].spec.n_t;
+    if (c->shards && c->shards->nccl) {
+      const i64 loc = nt / c->shards->S;
+      *first_step = c->shards->local[0].g * loc;
+      *n_steps = loc;
+    } else {
+      *first_step = 0;
+      *n_steps = nt;
+    }
   });
 }
 

@@ -50,6 +50,15 @@ def build_time_transfer(p_t: int, tau: float):
     return R1, R2
 
 
+def shard_plan(p_t: int, dim: int, space_level: int, time_level: int, shards: int,
+               t_final: float = 1.0, mu_star: float = 0.0, policy: int = POLICY_MU_DRIVEN):
+    """(gather level, finest steps per shard) of the time-slab decomposition."""
+    prm = A.HierarchyParams(p_t, dim, space_level, time_level, t_final, mu_star, policy, 0, 0, 0)
+    lg, n = C.c_int(), C.c_int64()
+    check(A.lib().stmg_shard_plan(C.byref(prm), shards, C.byref(lg), C.byref(n)))
+    return lg.value, n.value
+
+
 @dataclass
 class CycleConfig:
     """CycleConfig + SmootherConfig (mg.hpp:66-71, smoother.hpp:15-24)."""
@@ -114,13 +123,23 @@ class Hierarchy:
 
     def __init__(self, p_t: int, dim: int, space_level: int, time_level: int,
                  t_final: float = 1.0, mu_star: float = 0.0, policy: int = POLICY_MU_DRIVEN,
-                 two_grid: int = 0, device: int = 0):
+                 two_grid: int = 0, device: int = 0, shards: int = 0,
+                 rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None):
+        """shards > 1: time-slab sharding emulated on one device; world > 1:
+        one rank per GPU over NCCL (nccl_id from unique_id() on rank 0)."""
         self._ctx = None
         prm = A.HierarchyParams(p_t, dim, space_level, time_level, t_final, mu_star, policy,
-                                two_grid, device)
+                                two_grid, device, shards)
         ctx = C.c_void_p()
-        check(A.lib().stmg_create(C.byref(prm), C.byref(ctx)))
+        if world > 1:
+            if nccl_id is None:
+                raise ValueError("world > 1 needs the NCCL id of rank 0")
+            check(A.lib().stmg_create_distributed(C.byref(prm), rank, world, nccl_id,
+                                                  len(nccl_id), C.byref(ctx)))
+        else:
+            check(A.lib().stmg_create(C.byref(prm), C.byref(ctx)))
         self._ctx = ctx
+        self.rank, self.world = rank, world
         n = C.c_int()
         check(A.lib().stmg_num_levels(ctx, C.byref(n)))
         self.levels = []
@@ -140,6 +159,24 @@ class Hierarchy:
             self.close()
         except Exception:
             pass
+
+    @staticmethod
+    def unique_id() -> bytes:
+        """NCCL unique id for stmg_create_distributed (call on rank 0)."""
+        buf = C.create_string_buffer(128)
+        check(A.lib().stmg_nccl_unique_id(buf, 128))
+        return buf.raw
+
+    def local_steps(self):
+        a, b = C.c_int64(), C.c_int64()
+        check(A.lib().stmg_local_steps(self._ctx, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def local_vector(self) -> "BlockVector":
+        """This rank's finest-level time slabs (whole vector if not distributed)."""
+        L = self.levels[0]
+        _, n = self.local_steps()
+        return BlockVector(self, n * L["n_loc"] * L["n_x"], (n, L["n_loc"], L["n_x"]))
 
     # ---- vectors ----------------------------------------------------------
     def _lev(self, level: int) -> dict:
