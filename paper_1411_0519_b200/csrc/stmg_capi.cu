@@ -846,15 +846,11 @@ void build_shards(stmg_ctx* c) {
     ensure_tail(c);
   }
   if (int(c->cur.size()) != int(c->levels.size())) c->cur.assign(c->levels.size(), 0);
-  // level-0 residual partials per shard
+  // level-0 residual partials per shard (k_up grouped, k_resnorm per mode)
   {
     const stmg::LevelView& v = ss.local[0].lv[0].view;
-    const i64 G = (v.sp.n1 + 1) / 2;
-    i64 lanes = 1;
-    for (int a = 0; a < v.sp.dim; ++a) lanes *= 2 * G;
-    const i64 bx = (std::max(lanes, v.sp.nx) + 127) / 128;
-    const int ch = std::min(shard_chunk(c->levels[0], v, true), shard_chunk(c->levels[0], v, false));
-    ss.P = bx * ((v.n_t + ch - 1) / ch);
+    ss.P = std::max(stmg::partial_count(v, shard_chunk(c->levels[0], v, true), true),
+                    stmg::partial_count(v, shard_chunk(c->levels[0], v, false), false));
   }
   ss.partials.alloc(ss.S * ss.P + 16, 0);
   ss.built = true;
@@ -946,13 +942,19 @@ void scatter_corr(stmg_ctx* c) {
   nccl_check(N.GroupEnd(), "group end");
 }
 
-void allgather_partials(stmg_ctx* c) {
+void allgather_partials(stmg_ctx* c, i64 np) {
   ShardSet& ss = *c->shards;
   if (!ss.nccl) return;  // virtual shards write their segments in place
   NcclApi& N = nccl();
   const Shard& sh = ss.local[0];
-  nccl_check(N.AllGather(ss.partials.base + sh.g * ss.P, ss.partials.base, size_t(ss.P),
-                         ncclDouble, ss.comm, c->stream), "partials all-gather");
+  nccl_check(N.AllGather(ss.partials.base + sh.g * np, ss.partials.base, size_t(np), ncclDouble,
+                         ss.comm, c->stream), "partials all-gather");
+}
+
+// Partial sums of one shard's level-0 residual kernel (same on every shard).
+i64 shard_np(stmg_ctx* c, bool grouped) {
+  const stmg::LevelView& v = c->shards->local[0].lv[0].view;
+  return stmg::partial_count(v, shard_chunk(c->levels[0], v, grouped), grouped);
 }
 
 stmg::ModalArgs shard_args(stmg_ctx* c, int l, const ShardLevel& s, double omega, bool grouped) {
@@ -1007,7 +1009,7 @@ void sharded_cycle(stmg_ctx* c, const stmg_cycle_config& cfg) {
   bool have_root = false;
   for (Shard& sh : ss.local) have_root |= sh.g == 0;
   if (have_root) {
-    if (c->tail_table && lg == c->tail_start) {
+    if (c->tail_table && lg == c->tail_start && nu1 == 1 && nu2 == 1) {  // tail = V(1,1)
       CK(stmg::launch_tail(c->dim, c->p_t + 1, c->tail_table, int(c->levels.size()) - lg,
                            cfg.omega_t, c->tail_smem, c->stream));
       count(c);
@@ -1027,6 +1029,7 @@ void sharded_cycle(stmg_ctx* c, const stmg_cycle_config& cfg) {
     }
     halo(c, n_loc, slab, 2, [&](Shard& sh) { return sh.lv[l].U[sh.cur[l]].base; });
     const bool resid = l == 0 && nu2 == 1;
+    const i64 npu = shard_np(c, true);
     for (Shard& sh : ss.local) {
       ShardLevel& L = sh.lv[l];
       stmg::ModalArgs a = shard_args(c, l, L, cfg.omega_t, true);
@@ -1034,10 +1037,10 @@ void sharded_cycle(stmg_ctx* c, const stmg_cycle_config& cfg) {
       const bool p = l == 0 && sh.g == 0;
       if (p) prof_begin(c, 1);
       CK(stmg::launch_up(L.view, a, ec, L.U[sh.cur[l]].base, L.F.base, L.U[1 - sh.cur[l]].base,
-                         resid ? ss.partials.base + sh.g * ss.P : nullptr, c->stream));
+                         resid ? ss.partials.base + sh.g * npu : nullptr, c->stream));
       if (p) prof_end(c, 1, 8.0 * double(3 * L.view.size() + L.view.size() / 8));
       count(c);
-      if (resid) require(a.n_partials == ss.P, "partial count mismatch");
+      if (resid) require(a.n_partials == npu, "partial count mismatch");
       sh.cur[l] ^= 1;
     }
     for (int s = 1; s < nu2; ++s) {
@@ -1053,18 +1056,20 @@ void sharded_cycle(stmg_ctx* c, const stmg_cycle_config& cfg) {
     }
     if (l == 0 && !resid) {
       halo(c, n_loc, slab, 1, [&](Shard& sh) { return sh.lv[0].U[sh.cur[0]].base; });
+      const i64 npr = shard_np(c, false);
       for (Shard& sh : ss.local) {
         ShardLevel& L = sh.lv[0];
         stmg::ModalArgs a = shard_args(c, 0, L, cfg.omega_t, false);
         CK(stmg::launch_resnorm(L.view, a, L.U[sh.cur[0]].base, L.F.base,
-                                ss.partials.base + sh.g * ss.P, c->stream));
+                                ss.partials.base + sh.g * npr, c->stream));
         count(c);
-        require(a.n_partials == ss.P, "partial count mismatch");
+        require(a.n_partials == npr, "partial count mismatch");
       }
     }
   }
-  allgather_partials(c);
-  CK(stmg::launch_norm_final(ss.partials.base, ss.S * ss.P, c->d_norm, nullptr, 0, c->stream));
+  const i64 np = shard_np(c, nu2 == 1);
+  allgather_partials(c, np);
+  CK(stmg::launch_norm_final(ss.partials.base, ss.S * np, c->d_norm, nullptr, 0, c->stream));
   count(c);
   CK(cudaMemcpyAsync(c->h_norm, c->d_norm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
 }
@@ -1129,16 +1134,17 @@ void solve_sharded(stmg_ctx* c, const double* f, double* u, const stmg_cycle_con
   const stmg::LevelView& v0 = ss.local[0].lv[0].view;
   halo(c, v0.n_t, v0.slab(), 1, [&](Shard& sh) { return sh.lv[0].F.base; });
   halo(c, v0.n_t, v0.slab(), 1, [&](Shard& sh) { return sh.lv[0].U[0].base; });
+  const i64 npr = shard_np(c, false);
   for (Shard& sh : ss.local) {
     ShardLevel& L = sh.lv[0];
     stmg::ModalArgs a = shard_args(c, 0, L, cfg.omega_t, false);
-    CK(stmg::launch_resnorm(L.view, a, L.U[0].base, L.F.base, ss.partials.base + sh.g * ss.P,
+    CK(stmg::launch_resnorm(L.view, a, L.U[0].base, L.F.base, ss.partials.base + sh.g * npr,
                             c->stream));
     count(c);
-    require(a.n_partials == ss.P, "partial count mismatch");
+    require(a.n_partials == npr, "partial count mismatch");
   }
-  allgather_partials(c);
-  CK(stmg::launch_norm_final(ss.partials.base, ss.S * ss.P, c->d_norm, nullptr, 0, c->stream));
+  allgather_partials(c, npr);
+  CK(stmg::launch_norm_final(ss.partials.base, ss.S * npr, c->d_norm, nullptr, 0, c->stream));
   count(c);
   CK(cudaMemcpyAsync(c->h_norm, c->d_norm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));

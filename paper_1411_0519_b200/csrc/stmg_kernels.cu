@@ -1679,6 +1679,12 @@ cudaError_t launch_tail(int dim, int nl, const void* dev_table, int nlev, double
   return cudaGetLastError();
 }
 
+int64_t partial_count(const LevelView& L, int chunk, bool grouped) {
+  const i64 G = (L.sp.n1 + 1) / 2;
+  const i64 units = grouped ? (ipow(G, L.sp.dim) << L.sp.dim) : L.sp.nx;
+  return i64(grid1(units, 128)) * ((L.n_t + chunk - 1) / chunk);
+}
+
 int pick_chunk(const LevelView& L, bool grouped) {
   const i64 G = (L.sp.n1 + 1) / 2;
   const i64 units = grouped ? (ipow(G, L.sp.dim) << L.sp.dim) : L.sp.nx;

@@ -101,6 +101,8 @@ cudaError_t launch_resnorm(const LevelView& L, ModalArgs& a, const double* u,
 
 // Chunk length heuristic for the modal kernels at a level.
 int pick_chunk(const LevelView& L, bool grouped);
+// Number of partial sums written by launch_up (grouped) / launch_resnorm.
+int64_t partial_count(const LevelView& L, int chunk, bool grouped);
 
 // Single-CTA coarse tail (levels[0..nlev) = the small levels down to the
 // coarsest).  The device table is built once (outside graph capture).
