@@ -264,7 +264,10 @@ class Hierarchy:
                    max_iter: int = 250) -> SolveReport:
         """solve() on HOST arrays (u updated in place); H2D/D2H inside."""
         assert f.dtype == np.float64 and u.dtype == np.float64
-        assert f.size == self.size(0) and u.size == self.size(0)
+        _, n = self.local_steps()
+        local = n * self.levels[0]["n_loc"] * self.levels[0]["n_x"]
+        if f.size != local or u.size != local:
+            raise ValueError("space-time vector shape mismatch")
         c = cfg.c()
         hist = np.zeros(max_iter + 1)
         rep = A.SolveReport()
