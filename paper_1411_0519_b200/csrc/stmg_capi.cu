@@ -18,6 +18,8 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -116,7 +118,8 @@ struct stmg_ctx {
   std::vector<Level> levels;
   int p_t = 0, dim = 1;
   // scratch
-  DevBuf partials;   // norm partial sums
+  DevBuf partials;       // norm partial sums of the spectral cycle (graph-resident)
+  DevBuf partials_phys;  // per-step partials of stmg_norm
   double* d_norm = nullptr;
   double* d_hist = nullptr;
   int hist_cap = 0;
@@ -154,6 +157,11 @@ struct stmg_ctx {
   size_t tail_smem = 0;
   int* d_flag = nullptr;
   int* h_flag = nullptr;  // pinned
+  // device-side solve loop (conditional while node): cached per configuration
+  std::map<std::string, cudaGraphExec_t> loops;
+  int* d_iter = nullptr;
+  double* d_r0 = nullptr;
+  bool use_device_loop = true;
 };
 
 namespace {
@@ -393,9 +401,10 @@ void phys_cycle(stmg_ctx* c, int level, double* u, const double* f, const stmg_c
 }
 
 double norm_phys(stmg_ctx* c, Level& L, const double* v) {
-  ensure(c->partials, std::max<i64>(L.view.n_t, 1));
-  CK(stmg::launch_step_sumsq(L.view, v, c->partials.base, c->stream));
-  CK(stmg::launch_norm_final(c->partials.base, L.view.n_t, c->d_norm, nullptr, 0, c->stream));
+  // own buffer: the spectral partials are baked into cached graphs
+  ensure(c->partials_phys, std::max<i64>(L.view.n_t, 1));
+  CK(stmg::launch_step_sumsq(L.view, v, c->partials_phys.base, c->stream));
+  CK(stmg::launch_norm_final(c->partials_phys.base, L.view.n_t, c->d_norm, nullptr, 0, c->stream));
   count(c, 2);
   CK(cudaMemcpyAsync(c->h_norm, c->d_norm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -423,7 +432,13 @@ void ensure_spectral(stmg_ctx* c, int from_level) {
     const int ch = std::min(stmg::pick_chunk(L.view, true), stmg::pick_chunk(L.view, false));
     need = std::max<i64>(need, bx * ((L.view.n_t + ch - 1) / ch));
   }
-  ensure(c->partials, need);
+  if (c->partials.count < need) {  // grow only; cached graphs bake the pointer in
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
+    c->graphs.clear();
+    for (auto& kv : c->loops) cudaGraphExecDestroy(kv.second);
+    c->loops.clear();
+    c->partials.alloc(need, 0);
+  }
 }
 
 // The suffix of levels whose vectors (f, u, u') fit in one SM's shared
@@ -593,6 +608,9 @@ void check_cfg(const stmg_cycle_config* cfg) {
 
 void ensure_hist(stmg_ctx* c, int n) {
   if (c->hist_cap >= n) return;
+  n = std::max(n, 1024);
+  for (auto& kv : c->loops) cudaGraphExecDestroy(kv.second);  // they bake d_hist in
+  c->loops.clear();
   if (c->d_hist) cudaFree(c->d_hist);
   CK(cudaMalloc(&c->d_hist, size_t(n) * sizeof(double)));
   c->hist_cap = n;
@@ -644,6 +662,81 @@ stmg_ctx::GraphEntry& cycle_graph(stmg_ctx* c, const stmg_cycle_config& cfg) {
   return c->graphs[key] = e;
 }
 
+// The whole iteration as one graph: a conditional WHILE node whose body is a
+// V-cycle + residual norm + the device-side stop test (k_decide), so the host
+// does not synchronise per cycle.  Requires the cycle to leave the finest
+// iterate in the buffer it started from (true for V(1,1), any nu1 + nu2 even).
+template <class Body>
+cudaGraphExec_t device_loop(stmg_ctx* c, const std::string& key, double eps, int max_iter,
+                            Body&& body) {
+  auto it = c->loops.find(key);
+  if (it != c->loops.end()) return it->second;
+  cudaGraph_t g;
+  CK(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np{};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+  cudaGraph_t bodyg = np.conditional.phGraph_out[0];
+  c->capturing = true;
+  c->captured_kernels = 0;
+  CK(cudaStreamBeginCaptureToGraph(c->stream, bodyg, nullptr, nullptr, 0,
+                                   cudaStreamCaptureModeThreadLocal));
+  try {
+    body();
+    CK(stmg::launch_decide(h, c->d_norm, c->d_r0, c->d_hist, c->d_iter, eps, max_iter,
+                           c->stream));
+    count(c);
+  } catch (...) {
+    cudaGraph_t dummy;
+    cudaStreamEndCapture(c->stream, &dummy);
+    c->capturing = false;
+    cudaGraphDestroy(g);
+    throw;
+  }
+  cudaGraph_t captured;
+  CK(cudaStreamEndCapture(c->stream, &captured));
+  c->capturing = false;
+  cudaGraphExec_t exec;
+  CK(cudaGraphInstantiate(&exec, g, 0));
+  CK(cudaGraphDestroy(g));
+  c->loops[key] = exec;
+  return exec;
+}
+
+std::string loop_key(const char* kind, const stmg_cycle_config& cfg, int cur0, double eps,
+                     int max_iter) {
+  char b[160];
+  std::snprintf(b, sizeof(b), "%s/%d/%d/%d/%.17g/%d/%.17g/%d", kind, cfg.nu1, cfg.nu2, cfg.gamma,
+                cfg.omega_t, cur0, eps, max_iter);
+  return b;
+}
+
+// Run the remaining cycles on the device; fills r and history from the device.
+void run_device_loop(stmg_ctx* c, cudaGraphExec_t exec, int max_iter, double* history,
+                     int history_cap, int* nh, stmg_solve_report& r, double eps) {
+  CK(cudaMemsetAsync(c->d_iter, 0, sizeof(int), c->stream));
+  CK(cudaGraphLaunch(exec, c->stream));
+  int it = 0;
+  CK(cudaMemcpyAsync(&it, c->d_iter, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  std::vector<double> h(size_t(it) + 1);
+  CK(cudaMemcpy(h.data(), c->d_hist, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  for (int k = 1; k <= it; ++k) {
+    if (history && *nh < history_cap) history[*nh] = h[k];
+    ++*nh;
+  }
+  r.iterations = it;
+  r.r_final = it > 0 ? h[it] : r.r0;
+  r.converged = (it > 0 && h[it] <= eps * r.r0) ? 1 : 0;
+  (void)max_iter;
+}
+
 void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config& cfg, double eps,
                 int max_iter, double* history, int history_cap, stmg_solve_report* rep) {
   require(eps > 0.0, "eps_mg must be positive");
@@ -692,7 +785,29 @@ void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config
     r.r0 = r.r_final = r0;
     push(r0);
     if (r0 == 0.0) r.converged = 1;
-    for (int k = 0; k < max_iter && !r.converged; ++k) {
+    // the device-side loop needs the finest iterate back in its buffer after
+    // a cycle; the per-cycle graph (kept for profiling) reports where it ends
+    const stmg_ctx::GraphEntry& probe = cycle_graph(c, cfg);
+    const bool loop_ok = c->use_device_loop && !c->profile && probe.cur0_after == c->cur[0];
+    if (loop_ok && !r.converged && max_iter > 0) {
+      ensure_hist(c, max_iter + 1);
+      CK(cudaMemcpyAsync(c->d_r0, c->d_norm, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaMemcpyAsync(c->d_hist, c->d_norm, sizeof(double), cudaMemcpyDeviceToDevice,
+                         c->stream));
+      const int cur0 = c->cur[0];
+      cudaGraphExec_t ex = device_loop(c, loop_key("single", cfg, cur0, eps, max_iter), eps,
+                                       max_iter, [&] {
+                                         i64 np = 0;
+                                         spectral_cycle(c, 0, false, cfg, true, &np);
+                                         CK(stmg::launch_norm_final(c->partials.base, np, c->d_norm,
+                                                                    nullptr, 0, c->stream));
+                                         count(c);
+                                       });
+      c->cur[0] = cur0;
+      run_device_loop(c, ex, max_iter, history, history_cap, &nh, r, eps);
+      c->launches += r.iterations * (probe.kernels + 1);
+    }
+    for (int k = 0; k < max_iter && !r.converged && !loop_ok; ++k) {
       stmg_ctx::GraphEntry& g = cycle_graph(c, cfg);
       CK(cudaGraphLaunch(g.exec, c->stream));
       c->launches += g.kernels;
@@ -1281,6 +1396,9 @@ int stmg_create(const stmg_hierarchy_params* p, stmg_ctx** out) {
     CK(cudaMalloc(&c->d_norm, sizeof(double)));
     CK(cudaMallocHost(&c->h_norm, sizeof(double)));
     CK(cudaMalloc(&c->d_flag, sizeof(int)));
+    CK(cudaMalloc(&c->d_iter, sizeof(int)));
+    CK(cudaMalloc(&c->d_r0, sizeof(double)));
+    if (const char* e = std::getenv("STMG_DEVICE_LOOP")) c->use_device_loop = std::atoi(e) != 0;
     CK(cudaMallocHost(&c->h_flag, sizeof(int)));
     CK(cudaEventCreate(&c->ev_solve[0]));
     CK(cudaEventCreate(&c->ev_solve[1]));
@@ -1316,6 +1434,7 @@ int stmg_destroy(stmg_ctx* c) {
       for (DevBuf* b : {&L.F, &L.U[0], &L.U[1], &L.R, &L.RC, &L.EC, &L.CORR}) b->release();
     }
     c->partials.release();
+    c->partials_phys.release();
     c->user_f.release();
     c->user_u.release();
     for (auto& s : c->prof) {
@@ -1331,6 +1450,9 @@ int stmg_destroy(stmg_ctx* c) {
     cudaFree(c->d_norm);
     cudaFree(c->d_hist);
     cudaFree(c->d_flag);
+    cudaFree(c->d_iter);
+    cudaFree(c->d_r0);
+    for (auto& kv : c->loops) cudaGraphExecDestroy(kv.second);
     cudaFreeHost(c->h_flag);
     if (c->tail_table) cudaFree(c->tail_table);
     cudaFreeHost(c->h_norm);

@@ -1432,6 +1432,19 @@ __global__ void k_nonzero(const double* __restrict__ v, const i64 n, int* __rest
   if (__syncthreads_or(nz) && threadIdx.x == 0) *flag = 1;
 }
 
+// Stop test on the device (mg.cpp:156-160): record ||r_k||, count the cycle
+// and set the while-loop condition of the solve graph.
+__global__ void k_decide(cudaGraphConditionalHandle h, const double* __restrict__ norm,
+                         const double* __restrict__ r0, double* __restrict__ hist,
+                         int* __restrict__ iter, const double eps, const int max_iter) {
+  const int k = *iter + 1;
+  *iter = k;
+  const double rk = *norm;
+  hist[k] = rk;
+  const bool more = !(rk <= eps * (*r0)) && k < max_iter;
+  cudaGraphSetConditional(h, more ? 1u : 0u);
+}
+
 __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, const double a,
                        const i64 n) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1623,6 +1636,12 @@ cudaError_t launch_fill_uniform(double* v, int64_t n, uint64_t seed, uint64_t st
                                 int64_t offset, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   k_fill_uniform<<<grid1(n, 256), 256, 0, st>>>(v, n, seed, stream, offset);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decide(cudaGraphConditionalHandle h, const double* norm, const double* r0,
+                          double* hist, int* iter, double eps, int max_iter, cudaStream_t st) {
+  k_decide<<<1, 1, 0, st>>>(h, norm, r0, hist, iter, eps, max_iter);
   return cudaGetLastError();
 }
 

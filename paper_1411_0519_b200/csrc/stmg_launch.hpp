@@ -73,6 +73,10 @@ cudaError_t launch_fill_uniform(double* v, int64_t n, uint64_t seed,
                                 uint64_t stream, int64_t offset, cudaStream_t st);
 cudaError_t launch_axpy(double* y, const double* x, double a, int64_t n,
                         cudaStream_t st);
+// Device-side stop test: hist[++iter] = norm; loop while norm > eps*r0 and
+// iter < max_iter (sets the conditional handle of the solve graph).
+cudaError_t launch_decide(cudaGraphConditionalHandle h, const double* norm, const double* r0,
+                          double* hist, int* iter, double eps, int max_iter, cudaStream_t st);
 
 // ---- fused spectral V-cycle kernels (sine coefficients) -------------------
 struct ModalArgs {
