@@ -662,6 +662,9 @@ stmg_ctx::GraphEntry& cycle_graph(stmg_ctx* c, const stmg_cycle_config& cfg) {
   return c->graphs[key] = e;
 }
 
+// Buffer flips of the finest level per V-cycle (each sweep ping-pongs).
+int nu_flips(const stmg_cycle_config& cfg) { return std::max(cfg.nu1, 1) + std::max(cfg.nu2, 1); }
+
 // The whole iteration as one graph: a conditional WHILE node whose body is a
 // V-cycle + residual norm + the device-side stop test (k_decide), so the host
 // does not synchronise per cycle.  Requires the cycle to leave the finest
@@ -1083,7 +1086,7 @@ stmg::ModalArgs shard_args(stmg_ctx* c, int l, const ShardLevel& s, double omega
 
 // One V-cycle (gamma = 1) over the sharded levels + the root's tail, plus the
 // residual norm into d_norm (and h_norm).
-void sharded_cycle(stmg_ctx* c, const stmg_cycle_config& cfg) {
+void sharded_cycle(stmg_ctx* c, const stmg_cycle_config& cfg, bool copy_norm = true) {
   ShardSet& ss = *c->shards;
   const int lg = ss.lg;
   const int nu1 = cfg.nu1, nu2 = cfg.nu2;
@@ -1186,7 +1189,8 @@ void sharded_cycle(stmg_ctx* c, const stmg_cycle_config& cfg) {
   allgather_partials(c, np);
   CK(stmg::launch_norm_final(ss.partials.base, ss.S * np, c->d_norm, nullptr, 0, c->stream));
   count(c);
-  CK(cudaMemcpyAsync(c->h_norm, c->d_norm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  if (copy_norm)
+    CK(cudaMemcpyAsync(c->h_norm, c->d_norm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
 }
 
 // Sharded solve: f, u are this process's time slabs (virtual shards: the whole
@@ -1267,7 +1271,21 @@ void solve_sharded(stmg_ctx* c, const double* f, double* u, const stmg_cycle_con
   r.r0 = r.r_final = r0;
   push(r0);
   if (r0 == 0.0) r.converged = 1;
-  for (int k = 0; k < max_iter && !r.converged; ++k) {
+  // virtual shards: all cycles in one graph (device-side stop test); the
+  // finest parity is preserved when nu1 + nu2 is even
+  const bool loop_ok = !ss.nccl && c->use_device_loop && !c->profile && (nu_flips(cfg) % 2 == 0);
+  if (loop_ok && !r.converged && max_iter > 0) {
+    ensure_hist(c, max_iter + 1);
+    CK(cudaMemcpyAsync(c->d_r0, c->d_norm, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_hist, c->d_norm, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    std::vector<int> cur0(ss.local.size());
+    for (size_t i = 0; i < ss.local.size(); ++i) cur0[i] = ss.local[i].cur[0];
+    cudaGraphExec_t ex = device_loop(c, loop_key("sharded", cfg, cur0[0], eps, max_iter), eps,
+                                     max_iter, [&] { sharded_cycle(c, cfg, false); });
+    for (size_t i = 0; i < ss.local.size(); ++i) ss.local[i].cur[0] = cur0[i];
+    run_device_loop(c, ex, max_iter, history, history_cap, &nh, r, eps);
+  }
+  for (int k = 0; k < max_iter && !r.converged && !loop_ok; ++k) {
     // the cycle's buffer parity pattern is the same every iteration (coarse
     // levels restart at buffer 0) except the finest level's, so at most two
     // graphs; key on shard 0's finest parity
