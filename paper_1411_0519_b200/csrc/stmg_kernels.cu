@@ -339,21 +339,34 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
     }
   }
 
+  // software pipeline: the loads of step pair n+2 are in flight while pair
+  // n is computed (memory-level parallelism; the kernel is latency bound)
+  double f2[2][NL], u2[2][NL];
+#pragma unroll
+  for (int e = 0; e < 2; ++e)
+#pragma unroll
+    for (int l = 0; l < NL; ++l) f2[e][l] = u2[e][l] = 0.0;
+  if (me.ok && n0 < nend) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      ld_st<COH, NL>(fp + (n0 + e) * slab, nx, f2[e]);
+      if (!ZERO) ld_st<COH, NL>(up + (n0 + e) * slab, nx, u2[e]);
+    }
+  }
   for (i64 n = n0; n < nend; n += 2) {
     double acc[NL];
 #pragma unroll
     for (int l = 0; l < NL; ++l) acc[l] = 0.0;
-    // issue all loads of the step pair up front (memory-level parallelism)
-    double f2[2][NL], u2[2][NL];
+    double fn[2][NL], un2[2][NL];
 #pragma unroll
     for (int e = 0; e < 2; ++e)
 #pragma unroll
-      for (int l = 0; l < NL; ++l) f2[e][l] = u2[e][l] = 0.0;
-    if (me.ok) {
+      for (int l = 0; l < NL; ++l) fn[e][l] = un2[e][l] = 0.0;
+    if (me.ok && n + 2 < nend) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        ld_st<COH, NL>(fp + (n + e) * slab, nx, f2[e]);
-        if (!ZERO) ld_st<COH, NL>(up + (n + e) * slab, nx, u2[e]);
+        ld_st<COH, NL>(fp + (n + 2 + e) * slab, nx, fn[e]);
+        if (!ZERO) ld_st<COH, NL>(up + (n + 2 + e) * slab, nx, un2[e]);
       }
     }
 #pragma unroll
@@ -387,6 +400,13 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
         un[l] = w[l];
       }
     }
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        f2[e][l] = fn[e][l];
+        u2[e][l] = un2[e][l];
+      }
     const i64 nc = n >> 1;
     if (CO == 2) {
 #pragma unroll
@@ -453,13 +473,39 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
     }
   }
 
-  for (i64 n = n0; n < nend; n += 2) {
-    if (has_c) ld_ro<COH, NL>(ep + (n >> 1) * cslab, nxc, ev);
-    double u2[2][NL], f2[2][NL];
+  // software pipeline (see down_body); off for NL > 2, where the extra
+  // registers cost more occupancy than the prefetch gains (C3: -20 %)
+  constexpr bool PF = NL <= 2;
+  double u2[2][NL], f2[2][NL], en[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) en[l] = 0.0;
+  if (n0 < nend) {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      ld_st<COH, NL>(up + (n + e) * slab, nx, u2[e]);
-      ld_st<COH, NL>(fp + (n + e) * slab, nx, f2[e]);
+      ld_st<COH, NL>(up + (n0 + e) * slab, nx, u2[e]);
+      ld_st<COH, NL>(fp + (n0 + e) * slab, nx, f2[e]);
+    }
+    if (has_c) ld_ro<COH, NL>(ep + (n0 >> 1) * cslab, nxc, en);
+  }
+  for (i64 n = n0; n < nend; n += 2) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l) ev[l] = en[l];
+    double un2[2][NL], fn[2][NL];
+    if (PF && n + 2 < nend) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        ld_st<COH, NL>(up + (n + 2 + e) * slab, nx, un2[e]);
+        ld_st<COH, NL>(fp + (n + 2 + e) * slab, nx, fn[e]);
+      }
+      if (has_c) ld_ro<COH, NL>(ep + ((n + 2) >> 1) * cslab, nxc, en);
+    }
+    if (!PF && n > n0) {  // plain: load this pair now
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        ld_st<COH, NL>(up + (n + e) * slab, nx, u2[e]);
+        ld_st<COH, NL>(fp + (n + e) * slab, nx, f2[e]);
+      }
+      if (has_c) ld_ro<COH, NL>(ep + (n >> 1) * cslab, nxc, ev);
     }
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -491,6 +537,15 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
         vo[l] = v[l];
         wp[l] = w[l];
       }
+    }
+    if (PF && n + 2 < nend) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          u2[e][l] = un2[e][l];
+          f2[e][l] = fn[e][l];
+        }
     }
   }
   return sumsq;
@@ -546,15 +601,16 @@ __global__ void __launch_bounds__(256) k_up(const double* __restrict__ ec,
                                             const i64 n1c, const double omega,
                                             const bool first_global) {
   __shared__ double sh[32];
-  const i64 tid = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  const i64 n0 = i64(blockIdx.y) * C;
+  const unsigned bx = blockIdx.x, by = blockIdx.y;
+  const i64 tid = i64(bx) * blockDim.x + threadIdx.x;
+  const i64 n0 = i64(by) * C;
   const i64 nend = min(n0 + i64(C), n_t);
   const double sumsq = up_body<DIM, NL, CO, RESID, false>(
       tid, n0, nend, ec, uin, f, uout, t, s, n1c, omega, n0 > 0 || !first_global,
       n0 - 1 > 0 || !first_global);
   if (RESID) {
     const double tot = block_sum(sumsq, sh);
-    if (threadIdx.x == 0) partials[i64(blockIdx.y) * gridDim.x + blockIdx.x] = tot;
+    if (threadIdx.x == 0) partials[i64(by) * gridDim.x + bx] = tot;
   }
 }
 
