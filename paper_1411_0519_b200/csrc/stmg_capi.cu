@@ -261,9 +261,10 @@ void build_level_tables(Level& L) {
   }
   CK(cudaMalloc(&L.d_tables, tab.size() * sizeof(double)));
   CK(cudaMemcpy(L.d_tables, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
-  // twiddles exp(-2 pi i k / (2N)), k < N
-  std::vector<double> tw(2 * (n1 + 1));
-  for (i64 k = 0; k <= n1; ++k) {
+  // twiddles exp(-2 pi i k / L), L = 2N, full circle (k < L; indices in the
+  // Stockham passes stay below L)
+  std::vector<double> tw(4 * (n1 + 1));
+  for (i64 k = 0; k < 2 * (n1 + 1); ++k) {
     const long double a = -pi * (long double)k / (long double)N;
     tw[2 * k] = double(std::cos(a));
     tw[2 * k + 1] = double(std::sin(a));

@@ -1289,7 +1289,9 @@ struct DSTShape {
   static constexpr int BLOCK = TS > 128 ? TS : 128;
   static constexpr int F = BLOCK / TS;  // FFTs per block
   static constexpr int TL = 2 * F;      // lines per block
-  static constexpr int BUF = L + L / 16;
+  // padded FFT buffer; +4 double2 puts consecutive FFTs 64 B apart in the
+  // bank space, so the line-pair scatter of a warp is conflict-free
+  static constexpr int BUF = L + L / 16 + 4;
   static constexpr size_t smem = size_t(F) * BUF * sizeof(double2);
 };
 
@@ -1299,26 +1301,22 @@ __device__ __forceinline__ void team_sync() {
   else __syncthreads();
 }
 
-template <int L, int TS, int R>
-__device__ __forceinline__ void stockham_pass(double2* __restrict__ X, const int tt, const int Ns,
+template <int L, int TS, int R, int NS>
+__device__ __forceinline__ void stockham_pass(double2* __restrict__ X, const int tt,
                                               const double2* __restrict__ tw) {
-  constexpr int NJ = L / R;        // butterflies per FFT
-  constexpr int IPT = NJ / TS;     // butterflies per thread
+  constexpr int NJ = L / R;     // butterflies per FFT
+  constexpr int IPT = NJ / TS;  // butterflies per thread
+  constexpr int TSTEP = L / (NS * R);
   double2 v[IPT][R];
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     const int j = tt + i * TS;
 #pragma unroll
     for (int r = 0; r < R; ++r) v[i][r] = X[dst_pad(j + r * NJ)];
-    if (Ns > 1) {
-      const int step = (j % Ns) * (L / (Ns * R));
+    if (NS > 1) {
+      const int step = (j % NS) * TSTEP;  // NS, TSTEP: powers of two, compile time
 #pragma unroll
-      for (int r = 1; r < R; ++r) {
-        const int idx = (r * step) & (L - 1);
-        double2 w = __ldg(tw + (idx & (L / 2 - 1)));
-        if (idx >= L / 2) w = make_double2(-w.x, -w.y);
-        v[i][r] = cmul(v[i][r], w);
-      }
+      for (int r = 1; r < R; ++r) v[i][r] = cmul(v[i][r], __ldg(tw + r * step));
     }
     RegFFT<R>::run(v[i]);
   }
@@ -1326,108 +1324,113 @@ __device__ __forceinline__ void stockham_pass(double2* __restrict__ X, const int
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     const int j = tt + i * TS;
-    const int idxD = (j / Ns) * Ns * R + (j % Ns);
+    const int idxD = (j / NS) * NS * R + (j % NS);
 #pragma unroll
-    for (int r = 0; r < R; ++r) X[dst_pad(idxD + r * Ns)] = v[i][r];
+    for (int r = 0; r < R; ++r) X[dst_pad(idxD + r * NS)] = v[i][r];
   }
   team_sync<TS>();
 }
 
-template <int LOG2N, int P>
-__device__ __forceinline__ void dst_passes(double2* X, const int tt, const int Ns,
+template <int LOG2N, int P, int NS>
+__device__ __forceinline__ void dst_passes(double2* X, const int tt,
                                            const double2* __restrict__ tw) {
   using S = DSTShape<LOG2N>;
   if constexpr (P < dst_num_passes(S::M)) {
     constexpr int R = dst_pass_radix(S::M, P);
-    stockham_pass<S::L, S::TS, R>(X, tt, Ns, tw);
-    dst_passes<LOG2N, P + 1>(X, tt, Ns * R, tw);
+    stockham_pass<S::L, S::TS, R, NS>(X, tt, tw);
+    dst_passes<LOG2N, P + 1, NS * R>(X, tt, tw);
   }
 }
 
 template <int LOG2N>
-__global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK) k_dst_lines(
+__global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK, (LOG2N >= 3 ? 5 : 1)) k_dst_lines(
     const double* __restrict__ in, double* __restrict__ out, const i64 n_lines, const i64 stride,
     const double scale, const double alpha, const int accumulate,
     const double2* __restrict__ tw) {
   using S = DSTShape<LOG2N>;
   constexpr int L = S::L, F = S::F, TL = S::TL, n1 = S::n1, N = S::N, BUF = S::BUF;
   constexpr int TS = S::TS;
+  constexpr int BLK = S::BLOCK;
   extern __shared__ double2 sm[];
-  double* smd = reinterpret_cast<double*>(sm);
-
   __shared__ i64 lbase[TL];  // global offset of element 0 of each tile line
+
   const i64 line0 = i64(blockIdx.x) * TL;
   const int nt = int(min(i64(TL), n_lines - line0));
-  for (int li = threadIdx.x; li < nt; li += blockDim.x) {
-    const i64 line = line0 + li;
+  for (int li = threadIdx.x; li < TL; li += BLK) {
+    const i64 line = line0 + min(li, nt - 1);
     const i64 o = line / stride;
     lbase[li] = o * stride * n1 + (line - o * stride);
   }
-  if (nt < TL)
-    for (int k = threadIdx.x; k < F * BUF; k += blockDim.x) sm[k] = make_double2(0.0, 0.0);
-  else
-    for (int f = threadIdx.x; f < F; f += blockDim.x) {
-      sm[f * BUF + dst_pad(0)] = make_double2(0.0, 0.0);
-      sm[f * BUF + dst_pad(N)] = make_double2(0.0, 0.0);
-    }
+  for (int f = threadIdx.x; f < F; f += BLK) {
+    sm[f * BUF + dst_pad(0)] = make_double2(0.0, 0.0);
+    sm[f * BUF + dst_pad(N)] = make_double2(0.0, 0.0);
+  }
   __syncthreads();
-  constexpr int tile = TL * n1;
-  constexpr int BLK = S::BLOCK;
-  constexpr int ITEMS = (tile + BLK - 1) / BLK;
-  // all global loads of this thread first (memory-level parallelism), then
-  // the odd-extension scatter into shared memory
-  double vals[ITEMS];
+  // items = (line pair f, element j): two coalesced global loads, one 16-byte
+  // shared store per element and its odd mirror
+  constexpr int ITEMS_ALL = F * n1;
+  constexpr int ITEMS = (ITEMS_ALL + BLK - 1) / BLK;
+  double2 vals[ITEMS];
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int e = threadIdx.x + i * BLK;
-    int li, j;
+    int f, j;
     if (stride == 1) {
-      li = e / n1;
-      j = e - li * n1;
+      f = e / n1;
+      j = e - f * n1;
     } else {
-      j = e / TL;
-      li = e - j * TL;
+      j = e / F;
+      f = e - j * F;
     }
-    vals[i] = (e < tile && li < nt) ? __ldcs(in + lbase[li] + i64(j) * stride) : 0.0;
+    double a = 0.0, b = 0.0;
+    if (e < ITEMS_ALL) {
+      if (2 * f < nt) a = __ldcs(in + lbase[2 * f] + i64(j) * stride);
+      if (2 * f + 1 < nt) b = __ldcs(in + lbase[2 * f + 1] + i64(j) * stride);
+    }
+    vals[i] = make_double2(a, b);
   }
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int e = threadIdx.x + i * BLK;
-    int li, j;
+    if (e >= ITEMS_ALL) continue;
+    int f, j;
     if (stride == 1) {
-      li = e / n1;
-      j = e - li * n1;
+      f = e / n1;
+      j = e - f * n1;
     } else {
-      j = e / TL;
-      li = e - j * TL;
+      j = e / F;
+      f = e - j * F;
     }
-    if (e >= tile || li >= nt) continue;
-    const int f = li >> 1, comp = li & 1;
-    smd[2 * (f * BUF + dst_pad(j + 1)) + comp] = vals[i];
-    smd[2 * (f * BUF + dst_pad(L - 1 - j)) + comp] = -vals[i];
+    sm[f * BUF + dst_pad(j + 1)] = vals[i];
+    sm[f * BUF + dst_pad(L - 1 - j)] = make_double2(-vals[i].x, -vals[i].y);
   }
   __syncthreads();
-  dst_passes<LOG2N, 0>(sm + (threadIdx.x / TS) * BUF, threadIdx.x % TS, 1, tw);
+  dst_passes<LOG2N, 0, 1>(sm + (threadIdx.x / TS) * BUF, threadIdx.x % TS, tw);
   __syncthreads();
 
   const double hs = 0.5 * scale;
 #pragma unroll 4
-  for (int e = threadIdx.x; e < tile; e += blockDim.x) {
-    int li, j;
+  for (int e = threadIdx.x; e < ITEMS_ALL; e += BLK) {
+    int f, j;
     if (stride == 1) {
-      li = e / n1;
-      j = e - li * n1;
+      f = e / n1;
+      j = e - f * n1;
     } else {
-      j = e / TL;
-      li = e - j * TL;
+      j = e / F;
+      f = e - j * F;
     }
-    if (li >= nt) continue;
-    const int f = li >> 1, comp = li & 1;
     const double2 Z = sm[f * BUF + dst_pad(j + 1)];
-    const double v = (comp == 0 ? -Z.y : Z.x) * hs;
-    const i64 addr = lbase[li] + i64(j) * stride;
-    if (accumulate) out[addr] += alpha * v;
-    else out[addr] = v;
+    const double va = -Z.y * hs, vb = Z.x * hs;
+    if (2 * f < nt) {
+      const i64 addr = lbase[2 * f] + i64(j) * stride;
+      if (accumulate) out[addr] += alpha * va;
+      else __stcs(out + addr, va);
+    }
+    if (2 * f + 1 < nt) {
+      const i64 addr = lbase[2 * f + 1] + i64(j) * stride;
+      if (accumulate) out[addr] += alpha * vb;
+      else __stcs(out + addr, vb);
+    }
   }
 }
 
