@@ -1209,12 +1209,14 @@ __global__ void k_fold_u0(double* __restrict__ f, const double* __restrict__ u0,
 }
 
 // ================================================================ DST-I
-// Orthonormal DST-I of length n1 = N-1 (N = 2^LOG2N) along one axis.  Two
-// real lines a, b are packed into one complex sequence z = a + i b, oddly
-// extended to length L = 2N (z_0 = z_N = 0, z_{L-j} = -z_j); its DFT is
-// Z_k = -2i A_k + 2 B_k, so A_k = -Im Z_k / 2 and B_k = Re Z_k / 2.
-// The FFT is a Stockham autosort with register-resident radix-16 passes
-// (smem ping-pong between passes, padded against bank conflicts).
+// Orthonormal DST-I of length n1 = N-1 (N = 2^LOG2N) along one axis, with a
+// complex FFT of length N per PAIR of real lines (a + i b):
+//   y_j = sin(j pi/N)(x_j + x_{N-j}) + (x_j - x_{N-j})/2,   Y = FFT_N(y),
+//   X_{2k} = -Im Y_k,  X_{2k+1} = X_{2k-1} + Re Y_k,  X_1 = Re Y_0 / 2
+// (the real transforms of a and b are separated from Y by the usual
+// conjugate-symmetry split).  Half the FFT length of an odd extension.  The
+// FFT is a Stockham autosort with register-resident radix-16 passes; the
+// odd-index recurrence is a team-wide prefix sum.
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
@@ -1282,17 +1284,18 @@ template <int LOG2N>
 struct DSTShape {
   static constexpr int N = 1 << LOG2N;
   static constexpr int n1 = N - 1;
-  static constexpr int M = LOG2N + 1;
-  static constexpr int L = 1 << M;
+  static constexpr int M = LOG2N;  // FFT length L = N
+  static constexpr int L = N;
   static constexpr int V = L >= 16 ? 16 : L;
-  static constexpr int TS = L / V;
+  static constexpr int TS = L / V;  // threads per FFT (team)
   static constexpr int BLOCK = TS > 128 ? TS : 128;
-  static constexpr int F = BLOCK / TS;  // FFTs per block
+  static constexpr int F = BLOCK / TS;  // FFTs (= line pairs) per block
   static constexpr int TL = 2 * F;      // lines per block
   // padded FFT buffer; +4 double2 puts consecutive FFTs 64 B apart in the
   // bank space, so the line-pair scatter of a warp is conflict-free
   static constexpr int BUF = L + L / 16 + 4;
-  static constexpr size_t smem = size_t(F) * BUF * sizeof(double2);
+  static constexpr int KB = (L / 2 + TS - 1) / TS;  // recurrence values per thread
+  static constexpr size_t smem = size_t(F) * BUF * sizeof(double2) + size_t(BLOCK) * sizeof(double2);
 };
 
 template <int TS>
@@ -1316,7 +1319,7 @@ __device__ __forceinline__ void stockham_pass(double2* __restrict__ X, const int
     if (NS > 1) {
       const int step = (j % NS) * TSTEP;  // NS, TSTEP: powers of two, compile time
 #pragma unroll
-      for (int r = 1; r < R; ++r) v[i][r] = cmul(v[i][r], __ldg(tw + r * step));
+      for (int r = 1; r < R; ++r) v[i][r] = cmul(v[i][r], __ldg(tw + 2 * r * step));
     }
     RegFFT<R>::run(v[i]);
   }
@@ -1343,16 +1346,17 @@ __device__ __forceinline__ void dst_passes(double2* X, const int tt,
 }
 
 template <int LOG2N>
-__global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK, (LOG2N >= 3 ? 5 : 1)) k_dst_lines(
+__global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK, (LOG2N >= 4 ? 5 : 1)) k_dst_lines(
     const double* __restrict__ in, double* __restrict__ out, const i64 n_lines, const i64 stride,
     const double scale, const double alpha, const int accumulate,
     const double2* __restrict__ tw) {
   using S = DSTShape<LOG2N>;
-  constexpr int L = S::L, F = S::F, TL = S::TL, n1 = S::n1, N = S::N, BUF = S::BUF;
-  constexpr int TS = S::TS;
+  constexpr int F = S::F, TL = S::TL, n1 = S::n1, N = S::N, BUF = S::BUF;
+  constexpr int TS = S::TS, KB = S::KB;
   constexpr int BLK = S::BLOCK;
   extern __shared__ double2 sm[];
-  __shared__ i64 lbase[TL];  // global offset of element 0 of each tile line
+  double2* wsum = sm + F * BUF;  // per-thread scan totals
+  __shared__ i64 lbase[TL];      // global offset of element 0 of each tile line
 
   const i64 line0 = i64(blockIdx.x) * TL;
   const int nt = int(min(i64(TL), n_lines - line0));
@@ -1361,13 +1365,9 @@ __global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK, (LOG2N >= 3 ? 5 : 1)) 
     const i64 o = line / stride;
     lbase[li] = o * stride * n1 + (line - o * stride);
   }
-  for (int f = threadIdx.x; f < F; f += BLK) {
-    sm[f * BUF + dst_pad(0)] = make_double2(0.0, 0.0);
-    sm[f * BUF + dst_pad(N)] = make_double2(0.0, 0.0);
-  }
+  for (int f = threadIdx.x; f < F; f += BLK) sm[f * BUF + dst_pad(0)] = make_double2(0.0, 0.0);
   __syncthreads();
-  // items = (line pair f, element j): two coalesced global loads, one 16-byte
-  // shared store per element and its odd mirror
+  // ---- load: items = (line pair f, element j); z_{j+1} = (a_j, b_j)
   constexpr int ITEMS_ALL = F * n1;
   constexpr int ITEMS = (ITEMS_ALL + BLK - 1) / BLK;
   double2 vals[ITEMS];
@@ -1402,13 +1402,79 @@ __global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK, (LOG2N >= 3 ? 5 : 1)) 
       f = e - j * F;
     }
     sm[f * BUF + dst_pad(j + 1)] = vals[i];
-    sm[f * BUF + dst_pad(L - 1 - j)] = make_double2(-vals[i].x, -vals[i].y);
   }
   __syncthreads();
-  dst_passes<LOG2N, 0, 1>(sm + (threadIdx.x / TS) * BUF, threadIdx.x % TS, tw);
+  // ---- pre-processing: pairs (j, N-j), j = 1..N/2
+  for (int e = threadIdx.x; e < F * (N / 2); e += BLK) {
+    const int f = e / (N / 2), j = e - f * (N / 2) + 1;
+    double2* X = sm + f * BUF;
+    const double2 zj = X[dst_pad(j)], zm = X[dst_pad(N - j)];
+    const double sj = -__ldg(tw + j).y;  // sin(j pi / N)
+    const double2 sum = make_double2(zj.x + zm.x, zj.y + zm.y);
+    const double2 dif = make_double2(0.5 * (zj.x - zm.x), 0.5 * (zj.y - zm.y));
+    X[dst_pad(j)] = make_double2(sj * sum.x + dif.x, sj * sum.y + dif.y);
+    if (j != N / 2) X[dst_pad(N - j)] = make_double2(sj * sum.x - dif.x, sj * sum.y - dif.y);
+  }
+  __syncthreads();
+  // ---- FFT of length N per pair
+  const int team = threadIdx.x / TS, tt = threadIdx.x % TS;
+  dst_passes<LOG2N, 0, 1>(sm + team * BUF, tt, tw);
+  __syncthreads();
+  // ---- post-processing: split a/b, X_{2k} = I_k, X_{2k+1} = prefix sum of R
+  double2* X = sm + team * BUF;
+  double2 Rv[KB], Iv[KB];
+  double2 run = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int q = 0; q < KB; ++q) {
+    const int k = tt * KB + q;
+    double2 R = make_double2(0.0, 0.0), I = make_double2(0.0, 0.0);
+    if (k < N / 2) {
+      const double2 Y1 = X[dst_pad(k)], Y2 = X[dst_pad((N - k) & (N - 1))];
+      R = make_double2(0.5 * (Y1.x + Y2.x), 0.5 * (Y1.y + Y2.y));  // (Ra, Rb)
+      I = make_double2(0.5 * (Y2.y - Y1.y), 0.5 * (Y1.x - Y2.x));  // (Ia, Ib)
+      if (k == 0) R = make_double2(0.5 * R.x, 0.5 * R.y);
+    }
+    run = make_double2(run.x + R.x, run.y + R.y);
+    Rv[q] = run;  // inclusive prefix within the thread's block
+    Iv[q] = I;
+  }
+  // team-wide exclusive scan of the block totals
+  double2 off = make_double2(0.0, 0.0);
+  {
+    constexpr int W = TS < 32 ? TS : 32;
+    const int lane = threadIdx.x & 31;
+    double2 inc = run;
+#pragma unroll
+    for (int d = 1; d < W; d <<= 1) {
+      const double ux = __shfl_up_sync(0xffffffffu, inc.x, d, W);
+      const double uy = __shfl_up_sync(0xffffffffu, inc.y, d, W);
+      if ((lane % W) >= d) {
+        inc.x += ux;
+        inc.y += uy;
+      }
+    }
+    off = make_double2(inc.x - run.x, inc.y - run.y);
+    if (TS > 32) {  // combine the warps of a team
+      wsum[threadIdx.x] = inc;
+      __syncthreads();
+      const int w0 = (threadIdx.x / 32) * 32;  // first thread of this warp
+      for (int w = team * TS + 31; w < w0; w += 32) {
+        off.x += wsum[w].x;
+        off.y += wsum[w].y;
+      }
+    }
+  }
+  __syncthreads();  // every Y read is done; X is reused for the outputs
+#pragma unroll
+  for (int q = 0; q < KB; ++q) {
+    const int k = tt * KB + q;
+    if (k >= N / 2) continue;
+    if (k >= 1) X[dst_pad(2 * k)] = Iv[q];                               // X_{2k}
+    X[dst_pad(2 * k + 1)] = make_double2(off.x + Rv[q].x, off.y + Rv[q].y);  // X_{2k+1}
+  }
   __syncthreads();
 
-  const double hs = 0.5 * scale;
+  // ---- store: X_{j+1} of both lines of the pair
 #pragma unroll 4
   for (int e = threadIdx.x; e < ITEMS_ALL; e += BLK) {
     int f, j;
@@ -1420,7 +1486,7 @@ __global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK, (LOG2N >= 3 ? 5 : 1)) 
       f = e - j * F;
     }
     const double2 Z = sm[f * BUF + dst_pad(j + 1)];
-    const double va = -Z.y * hs, vb = Z.x * hs;
+    const double va = Z.x * scale, vb = Z.y * scale;
     if (2 * f < nt) {
       const i64 addr = lbase[2 * f] + i64(j) * stride;
       if (accumulate) out[addr] += alpha * va;
