@@ -153,6 +153,7 @@ struct stmg_ctx {
   cudaEvent_t ev_solve[2] = {nullptr, nullptr};
   // single-CTA coarse tail (levels >= tail_start), built on first solve
   void* tail_table = nullptr;
+  void* tail_host = nullptr;
   int tail_start = -1;
   size_t tail_smem = 0;
   int* d_flag = nullptr;
@@ -444,7 +445,7 @@ void ensure_spectral(stmg_ctx* c, int from_level) {
 
 // The suffix of levels whose vectors (f, u, u') fit in one SM's shared
 // memory runs inside the single-CTA tail kernel.
-constexpr i64 kTailSmemBytes = 184 * 1024;
+constexpr i64 kTailSmemBytes = 180 * 1024;
 
 // First level of the small suffix that runs in the tail kernel (0: none),
 // from the level vector sizes (doubles).
@@ -507,9 +508,11 @@ void ensure_tail(stmg_ctx* c) {
     t.U0 = L.U[0].base;
     t.U1 = L.U[1].base;
   }
-  CK(stmg::build_tail_table(spec.data(), int(spec.size()), &c->tail_table));
+  CK(stmg::build_tail_table(spec.data(), int(spec.size()), &c->tail_table, &c->tail_host));
   c->tail_start = start;
-  c->tail_smem = size_t(bytes);
+  i64 tab = 0;  // the sine tables are staged too
+  for (int l = start; l < nl; ++l) tab += 3 * c->levels[l].spec.n1() * i64(sizeof(double));
+  c->tail_smem = size_t(bytes + tab);
 }
 
 stmg::ModalArgs modal_args(const Level& L, const Level* C, double omega, bool grouped) {
@@ -564,7 +567,7 @@ void spectral_cycle(stmg_ctx* c, int level, bool zero_guess, const stmg_cycle_co
   }
   const bool fused = nu1 == 1 && nu2 == 1 && cfg.gamma == 1;
   if (fused && c->tail_table && level + 1 == c->tail_start) {
-    CK(stmg::launch_tail(L.spec.dim, L.spec.p_t + 1, c->tail_table,
+    CK(stmg::launch_tail(L.spec.dim, L.spec.p_t + 1, c->tail_table, c->tail_host,
                          int(c->levels.size()) - c->tail_start, cfg.omega_t, c->tail_smem,
                          c->stream));
     count(c);
@@ -1129,8 +1132,8 @@ void sharded_cycle(stmg_ctx* c, const stmg_cycle_config& cfg, bool copy_norm = t
   for (Shard& sh : ss.local) have_root |= sh.g == 0;
   if (have_root) {
     if (c->tail_table && lg == c->tail_start && nu1 == 1 && nu2 == 1) {  // tail = V(1,1)
-      CK(stmg::launch_tail(c->dim, c->p_t + 1, c->tail_table, int(c->levels.size()) - lg,
-                           cfg.omega_t, c->tail_smem, c->stream));
+      CK(stmg::launch_tail(c->dim, c->p_t + 1, c->tail_table, c->tail_host,
+                           int(c->levels.size()) - lg, cfg.omega_t, c->tail_smem, c->stream));
       count(c);
       for (int l = lg; l < int(c->levels.size()); ++l) c->cur[l] = 0;
     } else {
@@ -1474,6 +1477,7 @@ int stmg_destroy(stmg_ctx* c) {
     for (auto& kv : c->loops) cudaGraphExecDestroy(kv.second);
     cudaFreeHost(c->h_flag);
     if (c->tail_table) cudaFree(c->tail_table);
+    std::free(c->tail_host);
     cudaFreeHost(c->h_norm);
     cudaStreamDestroy(c->stream);
     delete c;

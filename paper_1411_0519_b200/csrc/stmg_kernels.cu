@@ -19,6 +19,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "stmg_launch.hpp"
@@ -147,15 +149,15 @@ __device__ __forceinline__ void matvec_t(const double (&A)[NL][NL], const double
   }
 }
 
-template <int DIM>
+template <int DIM, bool COH = false>
 __device__ __forceinline__ void mode_eig(const SP& s, i64 r, double& Mj, double& Kj) {
   double mv[DIM], kv[DIM];
 #pragma unroll
   for (int a = 0; a < DIM; ++a) {
     const i64 q = r % s.n1;
     r /= s.n1;
-    mv[a] = __ldg(s.mval + q);
-    kv[a] = __ldg(s.kval + q);
+    mv[a] = COH ? s.mval[q] : __ldg(s.mval + q);
+    kv[a] = COH ? s.kval[q] : __ldg(s.kval + q);
   }
   Mj = 1.0;
 #pragma unroll
@@ -203,7 +205,7 @@ struct Member {
   bool cok;      // group has a coarse mode
 };
 
-template <int DIM>
+template <int DIM, bool COH = false>
 __device__ __forceinline__ Member make_member(const SP& s, i64 t, i64 n1c, bool full) {
   Member m;
   const int b = int(t & ((1 << DIM) - 1));
@@ -228,9 +230,9 @@ __device__ __forceinline__ Member make_member(const SP& s, i64 t, i64 n1c, bool 
     mul *= s.n1;
     ci += ia * cm;
     cm *= n1c;
-    mv[a] = __ldg(s.mval + q);
-    kv[a] = __ldg(s.kval + q);
-    if (full) fac *= __ldg(s.rfac + q);
+    mv[a] = COH ? s.mval[q] : __ldg(s.mval + q);
+    kv[a] = COH ? s.kval[q] : __ldg(s.kval + q);
+    if (full) fac *= COH ? s.rfac[q] : __ldg(s.rfac + q);
   }
   double M = 1.0, K = 0.0;
 #pragma unroll
@@ -301,7 +303,7 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
                                           double* fc, const TM<NL>& t, const SP& s,
                                           const i64 n1c, const double omega, const bool has_prev,
                                           const bool has_prev2) {
-  const Member me = make_member<DIM>(s, tid, n1c, CO == 2);
+  const Member me = make_member<DIM, COH>(s, tid, n1c, CO == 2);
   const i64 nx = s.nx, slab = NL * nx;
   const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
   const double om1 = 1.0 - omega;
@@ -427,7 +429,7 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
                                           double* uout, const TM<NL>& t, const SP& s,
                                           const i64 n1c, const double omega, const bool has_prev,
                                           const bool has_prev2) {
-  const Member me = make_member<DIM>(s, tid, n1c, CO == 2);
+  const Member me = make_member<DIM, COH>(s, tid, n1c, CO == 2);
   const i64 nx = s.nx, slab = NL * nx;
   const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
   const double om1 = 1.0 - omega;
@@ -558,7 +560,7 @@ __device__ __forceinline__ void fwdsub_body(const i64 r, const double* f, double
                                             const TM<NL>& t, const SP& s, const i64 n_t) {
   if (r >= s.nx) return;
   double Mj, Kj;
-  mode_eig<DIM>(s, r, Mj, Kj);
+  mode_eig<DIM, COH>(s, r, Mj, Kj);
   const i64 nx = s.nx, slab = NL * nx;
   double prev[NL];
 #pragma unroll
@@ -635,9 +637,20 @@ struct TailLevel {
 
 constexpr int kTailMaxLevels = 24;
 
+// DG/transfer blocks of every tail level as a kernel parameter (constant
+// bank): indexed by the level, read with LDC instead of shared-memory loads
+// in the dependent per-step chains.
+template <int NL>
+struct TailParams {
+  TM<NL> t[kTailMaxLevels];
+};
+
+constexpr int kTailThreads = 512;  // 128 registers per thread: no spills
+
 template <int DIM, int NL>
-__global__ void __launch_bounds__(1024) k_tail(const TailLevel<NL>* __restrict__ lv,
-                                               const int nlev, const double omega) {
+__global__ void __launch_bounds__(kTailThreads) k_tail(const TailLevel<NL>* __restrict__ lv,
+                                               const int nlev, const double omega,
+                                               const __grid_constant__ TailParams<NL> P) {
   extern __shared__ double smem[];
   __shared__ TailLevel<NL> lvs[kTailMaxLevels];
   __shared__ i64 off[kTailMaxLevels + 1];
@@ -662,6 +675,20 @@ __global__ void __launch_bounds__(1024) k_tail(const TailLevel<NL>* __restrict__
     lvs[k].U0 = smem + off[k] + sz;
     lvs[k].U1 = smem + off[k] + 2 * sz;
   }
+  {  // sine tables (mval | kval | rfac, contiguous per level) -> shared memory
+    double* tab = smem + off[nlev];
+    for (int k = 0; k < nlev; ++k) {
+      const int n1 = int(lv[k].s.n1);
+      const double* g = lv[k].s.mval;  // the three tables are contiguous
+      for (int i = threadIdx.x; i < 3 * n1; i += T) tab[i] = g[i];
+      if (threadIdx.x == 0) {
+        lvs[k].s.mval = tab;
+        lvs[k].s.kval = tab + n1;
+        lvs[k].s.rfac = tab + 2 * n1;
+      }
+      tab += 3 * n1;
+    }
+  }
   const int sz0 = int(lv[0].n_t * NL * lv[0].s.nx);
   {  // stage the first level's rhs
     const double* g = lv[0].F;
@@ -682,18 +709,18 @@ __global__ void __launch_bounds__(1024) k_tail(const TailLevel<NL>* __restrict__
       if (n0 >= nt) continue;  // whole alias groups skip together
       const int nend = min(n0 + C, nt);
       if (A.mode == 2)
-        down_body<DIM, NL, true, 2, true>(lane, n0, nend, A.F, A.U1, A.U1, B.F, A.t, A.s, A.n1c,
-                                          omega, n0 > 0, n0 - 1 > 0);
+        down_body<DIM, NL, true, 2, true>(lane, n0, nend, A.F, A.U1, A.U1, B.F, P.t[k], A.s,
+                                          A.n1c, omega, n0 > 0, n0 - 1 > 0);
       else
-        down_body<DIM, NL, true, 1, true>(lane, n0, nend, A.F, A.U1, A.U1, B.F, A.t, A.s, A.s.n1,
-                                          omega, n0 > 0, n0 - 1 > 0);
+        down_body<DIM, NL, true, 1, true>(lane, n0, nend, A.F, A.U1, A.U1, B.F, P.t[k], A.s,
+                                          A.s.n1, omega, n0 > 0, n0 - 1 > 0);
     }
     __syncthreads();
   }
   {
     const TailLevel<NL>& A = lvs[nlev - 1];
     for (int r = threadIdx.x; r < int(A.s.nx); r += T)
-      fwdsub_body<DIM, NL, true>(r, A.F, A.U0, A.t, A.s, A.n_t);
+      fwdsub_body<DIM, NL, true>(r, A.F, A.U0, P.t[nlev - 1], A.s, A.n_t);
   }
   __syncthreads();
   for (int k = nlev - 2; k >= 0; --k) {
@@ -708,11 +735,11 @@ __global__ void __launch_bounds__(1024) k_tail(const TailLevel<NL>* __restrict__
       const int lane = it % lanes, n0 = (it / lanes) * C;
       const int nend = min(n0 + C, nt);
       if (A.mode == 2)
-        up_body<DIM, NL, 2, false, true>(lane, n0, nend, B.U0, A.U1, A.F, A.U0, A.t, A.s, A.n1c,
-                                         omega, n0 > 0, n0 - 1 > 0);
+        up_body<DIM, NL, 2, false, true>(lane, n0, nend, B.U0, A.U1, A.F, A.U0, P.t[k], A.s,
+                                         A.n1c, omega, n0 > 0, n0 - 1 > 0);
       else
-        up_body<DIM, NL, 1, false, true>(lane, n0, nend, B.U0, A.U1, A.F, A.U0, A.t, A.s, A.s.n1,
-                                         omega, n0 > 0, n0 - 1 > 0);
+        up_body<DIM, NL, 1, false, true>(lane, n0, nend, B.U0, A.U1, A.F, A.U0, P.t[k], A.s,
+                                         A.s.n1, omega, n0 > 0, n0 - 1 > 0);
     }
     __syncthreads();
   }
@@ -1784,7 +1811,7 @@ cudaError_t launch_nonzero(const double* v, int64_t n, int* flag, cudaStream_t s
 }
 
 template <int NL>
-cudaError_t build_tail_table_t(const TailSpec* lv, int nlev, void** out) {
+cudaError_t build_tail_table_t(const TailSpec* lv, int nlev, void** out, void** host_out) {
   std::vector<TailLevel<NL>> h(nlev);
   for (int k = 0; k < nlev; ++k) {
     h[k].t = make_tm<NL>(lv[k].view.tc);
@@ -1798,27 +1825,34 @@ cudaError_t build_tail_table_t(const TailSpec* lv, int nlev, void** out) {
   }
   cudaError_t e = cudaMalloc(out, sizeof(TailLevel<NL>) * nlev);
   if (e != cudaSuccess) return e;
+  void* hb = std::malloc(sizeof(TailLevel<NL>) * nlev);
+  std::memcpy(hb, h.data(), sizeof(TailLevel<NL>) * nlev);
+  *host_out = hb;
   return cudaMemcpy(*out, h.data(), sizeof(TailLevel<NL>) * nlev, cudaMemcpyHostToDevice);
 }
 
-cudaError_t build_tail_table(const TailSpec* levels, int nlev, void** dev_table) {
+cudaError_t build_tail_table(const TailSpec* levels, int nlev, void** dev_table,
+                             void** host_table) {
   switch (levels[0].view.tc.nl) {
-    case 1: return build_tail_table_t<1>(levels, nlev, dev_table);
-    case 2: return build_tail_table_t<2>(levels, nlev, dev_table);
-    case 3: return build_tail_table_t<3>(levels, nlev, dev_table);
-    case 4: return build_tail_table_t<4>(levels, nlev, dev_table);
+    case 1: return build_tail_table_t<1>(levels, nlev, dev_table, host_table);
+    case 2: return build_tail_table_t<2>(levels, nlev, dev_table, host_table);
+    case 3: return build_tail_table_t<3>(levels, nlev, dev_table, host_table);
+    case 4: return build_tail_table_t<4>(levels, nlev, dev_table, host_table);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_tail(int dim, int nl, const void* dev_table, int nlev, double omega,
-                        size_t smem_bytes, cudaStream_t st) {
+cudaError_t launch_tail(int dim, int nl, const void* dev_table, const void* host_table, int nlev,
+                        double omega, size_t smem_bytes, cudaStream_t st) {
   if (nlev > kTailMaxLevels) return cudaErrorInvalidValue;
   STMG_DISPATCH(dim, nl, {
+    TailParams<NL> P;
+    const TailLevel<NL>* h = static_cast<const TailLevel<NL>*>(host_table);
+    for (int k = 0; k < nlev; ++k) P.t[k] = h[k].t;
     cudaFuncSetAttribute(k_tail<DIM, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(smem_bytes));
-    k_tail<DIM, NL><<<1, 1024, smem_bytes, st>>>(static_cast<const TailLevel<NL>*>(dev_table),
-                                                  nlev, omega);
+    k_tail<DIM, NL><<<1, kTailThreads, smem_bytes, st>>>(
+        static_cast<const TailLevel<NL>*>(dev_table), nlev, omega, P);
   });
   return cudaGetLastError();
 }

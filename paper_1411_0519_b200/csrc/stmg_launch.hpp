@@ -118,9 +118,11 @@ struct TailSpec {
   double* U0 = nullptr;
   double* U1 = nullptr;
 };
-cudaError_t build_tail_table(const TailSpec* levels, int nlev, void** dev_table);
-cudaError_t launch_tail(int dim, int nl, const void* dev_table, int nlev, double omega,
-                        size_t smem_bytes, cudaStream_t st);
+// host_table: malloc'd host copy (free with std::free).
+cudaError_t build_tail_table(const TailSpec* levels, int nlev, void** dev_table,
+                             void** host_table);
+cudaError_t launch_tail(int dim, int nl, const void* dev_table, const void* host_table, int nlev,
+                        double omega, size_t smem_bytes, cudaStream_t st);
 // flag[0] = 1 if any v[i] != 0 (flag must be zeroed before).
 cudaError_t launch_nonzero(const double* v, int64_t n, int* flag, cudaStream_t st);
 
