@@ -73,6 +73,15 @@ SP make_sp(const SpaceConsts& s) {
 
 __host__ __device__ constexpr i64 ipow(i64 b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
 
+// Programmatic dependent launch: the V-cycle kernels are launched with
+// programmatic stream serialization, so the next kernel's CTAs are scheduled
+// while this one drains; every such kernel waits for its predecessor's
+// memory before touching global data.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
 // ------------------------------------------------------------ per-mode math
 // Exact per-mode block: A_j = M_j K_tau + K_j M_tau.  Its symmetric part is
 // positive definite (K_tau + K_tau^T = psi(tau)psi(tau)^T + psi(0)psi(0)^T),
@@ -586,11 +595,13 @@ __global__ void __launch_bounds__(256) k_down(const double* __restrict__ f,
                                               const SP s, const i64 n_t, const int C,
                                               const i64 n1c, const double omega,
                                               const bool first_global) {
+  pdl_wait();
   const i64 tid = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   const i64 n0 = i64(blockIdx.y) * C;
   const i64 nend = min(n0 + i64(C), n_t);
   down_body<DIM, NL, ZERO, CO, false>(tid, n0, nend, f, uin, uout, fc, t, s, n1c, omega,
                                       n0 > 0 || !first_global, n0 - 1 > 0 || !first_global);
+  pdl_trigger();
 }
 
 template <int DIM, int NL, int CO, bool RESID>
@@ -602,6 +613,7 @@ __global__ void __launch_bounds__(256) k_up(const double* __restrict__ ec,
                                             const SP s, const i64 n_t, const int C,
                                             const i64 n1c, const double omega,
                                             const bool first_global) {
+  pdl_wait();
   __shared__ double sh[32];
   const unsigned bx = blockIdx.x, by = blockIdx.y;
   const i64 tid = i64(bx) * blockDim.x + threadIdx.x;
@@ -610,6 +622,7 @@ __global__ void __launch_bounds__(256) k_up(const double* __restrict__ ec,
   const double sumsq = up_body<DIM, NL, CO, RESID, false>(
       tid, n0, nend, ec, uin, f, uout, t, s, n1c, omega, n0 > 0 || !first_global,
       n0 - 1 > 0 || !first_global);
+  pdl_trigger();
   if (RESID) {
     const double tot = block_sum(sumsq, sh);
     if (threadIdx.x == 0) partials[i64(by) * gridDim.x + bx] = tot;
@@ -651,6 +664,7 @@ template <int DIM, int NL>
 __global__ void __launch_bounds__(kTailThreads) k_tail(const TailLevel<NL>* __restrict__ lv,
                                                const int nlev, const double omega,
                                                const __grid_constant__ TailParams<NL> P) {
+  pdl_wait();
   extern __shared__ double smem[];
   __shared__ TailLevel<NL> lvs[kTailMaxLevels];
   __shared__ i64 off[kTailMaxLevels + 1];
@@ -756,6 +770,7 @@ __global__ void __launch_bounds__(128) k_smooth(const double* __restrict__ f,
                                                 double* __restrict__ uout, const TM<NL> t,
                                                 const SP s, const i64 n_t, const int C,
                                                 const double omega, const bool first_global) {
+  pdl_wait();
   const i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= s.nx) return;
   double Mj, Kj;
@@ -793,6 +808,7 @@ __global__ void __launch_bounds__(128) k_resnorm(const double* __restrict__ u,
                                                  double* __restrict__ partials, const TM<NL> t,
                                                  const SP s, const i64 n_t, const int C,
                                                  const bool first_global) {
+  pdl_wait();
   __shared__ double sh[32];
   const i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   double sumsq = 0.0;
@@ -828,6 +844,7 @@ template <int DIM, int NL>
 __global__ void __launch_bounds__(128) k_fwdsub(const double* __restrict__ f,
                                                 double* __restrict__ u, const TM<NL> t,
                                                 const SP s, const i64 n_t) {
+  pdl_wait();
   const i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   fwdsub_body<DIM, NL, false>(r, f, u, t, s, n_t);
 }
@@ -1546,6 +1563,7 @@ __global__ void __launch_bounds__(256) k_step_sumsq(const double* __restrict__ v
 __global__ void __launch_bounds__(256) k_norm_final(const double* __restrict__ partial,
                                                     const i64 n, double* __restrict__ out,
                                                     double* __restrict__ hist, const int hidx) {
+  pdl_wait();
   __shared__ double sh[256];
   double s = 0.0;
   for (i64 i = threadIdx.x; i < n; i += 256) s += partial[i];
@@ -1589,6 +1607,7 @@ __global__ void k_nonzero(const double* __restrict__ v, const i64 n, int* __rest
 __global__ void k_decide(cudaGraphConditionalHandle h, const double* __restrict__ norm,
                          const double* __restrict__ r0, double* __restrict__ hist,
                          int* __restrict__ iter, const double eps, const int max_iter) {
+  pdl_wait();
   const int k = *iter + 1;
   *iter = k;
   const double rk = *norm;
@@ -1604,6 +1623,28 @@ __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, con
 }
 
 inline unsigned grid1(i64 n, int bs) { return unsigned((n + bs - 1) / bs); }
+
+// Launch with programmatic stream serialization (see pdl_wait).
+template <typename... KArgs, typename... Args>
+cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+#define PDLK(...)                                   \
+  do {                                              \
+    const cudaError_t e_ = pdl_launch(__VA_ARGS__); \
+    if (e_ != cudaSuccess) return e_;               \
+  } while (0)
 // nodes along x (blocks of bs), time steps along y (grid-stride beyond 65535)
 inline dim3 grid2(i64 nodes, i64 steps, int bs) {
   return dim3(grid1(nodes, bs), unsigned(std::max<i64>(1, std::min<i64>(steps, 65535))));
@@ -1766,7 +1807,7 @@ cudaError_t launch_modal_solve(const LevelView& L, double* x, cudaStream_t st) {
 cudaError_t launch_modal_fwdsub(const LevelView& L, const double* f, double* u, cudaStream_t st) {
   const SP s = make_sp(L.sp);
   STMG_DISPATCH(L.sp.dim, L.tc.nl, {
-    k_fwdsub<DIM, NL><<<grid1(L.sp.nx, 128), 128, 0, st>>>(f, u, make_tm<NL>(L.tc), s, L.n_t);
+    PDLK(k_fwdsub<DIM, NL>, grid1(L.sp.nx, 128), 128, 0, st, f, u, make_tm<NL>(L.tc), s, L.n_t);
   });
   return cudaGetLastError();
 }
@@ -1780,7 +1821,7 @@ cudaError_t launch_step_sumsq(const LevelView& L, const double* v, double* parti
 
 cudaError_t launch_norm_final(const double* partial, int64_t n, double* out, double* hist,
                               int hidx, cudaStream_t st) {
-  k_norm_final<<<1, 256, 0, st>>>(partial, n, out, hist, hidx);
+  PDLK(k_norm_final, 1, 256, 0, st, partial, n, out, hist, hidx);
   return cudaGetLastError();
 }
 
@@ -1793,7 +1834,7 @@ cudaError_t launch_fill_uniform(double* v, int64_t n, uint64_t seed, uint64_t st
 
 cudaError_t launch_decide(cudaGraphConditionalHandle h, const double* norm, const double* r0,
                           double* hist, int* iter, double eps, int max_iter, cudaStream_t st) {
-  k_decide<<<1, 1, 0, st>>>(h, norm, r0, hist, iter, eps, max_iter);
+  PDLK(k_decide, 1, 1, 0, st, h, norm, r0, hist, iter, eps, max_iter);
   return cudaGetLastError();
 }
 
@@ -1851,7 +1892,7 @@ cudaError_t launch_tail(int dim, int nl, const void* dev_table, const void* host
     for (int k = 0; k < nlev; ++k) P.t[k] = h[k].t;
     cudaFuncSetAttribute(k_tail<DIM, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(smem_bytes));
-    k_tail<DIM, NL><<<1, kTailThreads, smem_bytes, st>>>(
+    PDLK(k_tail<DIM, NL>, 1, kTailThreads, smem_bytes, st, 
         static_cast<const TailLevel<NL>*>(dev_table), nlev, omega, P);
   });
   return cudaGetLastError();
@@ -1885,17 +1926,17 @@ cudaError_t launch_down(const LevelView& L, ModalArgs& a, bool zero_guess, const
     const TM<NL> t = make_tm<NL>(L.tc);
     if (a.mode == 2) {
       if (zero_guess)
-        k_down<DIM, NL, true, 2><<<grid, 128, 0, st>>>(f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
+        PDLK(k_down<DIM, NL, true, 2>, grid, 128, 0, st, f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
                                                       a.n1c, a.omega, L.first_global);
       else
-        k_down<DIM, NL, false, 2><<<grid, 128, 0, st>>>(f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
+        PDLK(k_down<DIM, NL, false, 2>, grid, 128, 0, st, f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
                                                        a.n1c, a.omega, L.first_global);
     } else {
       if (zero_guess)
-        k_down<DIM, NL, true, 1><<<grid, 128, 0, st>>>(f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
+        PDLK(k_down<DIM, NL, true, 1>, grid, 128, 0, st, f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
                                                       L.sp.n1, a.omega, L.first_global);
       else
-        k_down<DIM, NL, false, 1><<<grid, 128, 0, st>>>(f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
+        PDLK(k_down<DIM, NL, false, 1>, grid, 128, 0, st, f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
                                                        L.sp.n1, a.omega, L.first_global);
     }
   });
@@ -1913,17 +1954,17 @@ cudaError_t launch_up(const LevelView& L, ModalArgs& a, const double* ec, const 
     const i64 n1c = a.mode == 2 ? a.n1c : L.sp.n1;
     if (a.mode == 2) {
       if (partials)
-        k_up<DIM, NL, 2, true><<<grid, 128, 0, st>>>(ec, u_in, f, u_out, partials, t, s, L.n_t,
+        PDLK(k_up<DIM, NL, 2, true>, grid, 128, 0, st, ec, u_in, f, u_out, partials, t, s, L.n_t,
                                                     a.chunk, n1c, a.omega, L.first_global);
       else
-        k_up<DIM, NL, 2, false><<<grid, 128, 0, st>>>(ec, u_in, f, u_out, partials, t, s, L.n_t,
+        PDLK(k_up<DIM, NL, 2, false>, grid, 128, 0, st, ec, u_in, f, u_out, partials, t, s, L.n_t,
                                                      a.chunk, n1c, a.omega, L.first_global);
     } else {
       if (partials)
-        k_up<DIM, NL, 1, true><<<grid, 128, 0, st>>>(ec, u_in, f, u_out, partials, t, s, L.n_t,
+        PDLK(k_up<DIM, NL, 1, true>, grid, 128, 0, st, ec, u_in, f, u_out, partials, t, s, L.n_t,
                                                     a.chunk, n1c, a.omega, L.first_global);
       else
-        k_up<DIM, NL, 1, false><<<grid, 128, 0, st>>>(ec, u_in, f, u_out, partials, t, s, L.n_t,
+        PDLK(k_up<DIM, NL, 1, false>, grid, 128, 0, st, ec, u_in, f, u_out, partials, t, s, L.n_t,
                                                      a.chunk, n1c, a.omega, L.first_global);
     }
   });
@@ -1937,10 +1978,10 @@ cudaError_t launch_smooth(const LevelView& L, ModalArgs& a, bool zero_guess, con
   STMG_DISPATCH(L.sp.dim, L.tc.nl, {
     const TM<NL> t = make_tm<NL>(L.tc);
     if (zero_guess)
-      k_smooth<DIM, NL, true><<<grid, 128, 0, st>>>(f, u_in, u_out, t, s, L.n_t, a.chunk, a.omega,
+      PDLK(k_smooth<DIM, NL, true>, grid, 128, 0, st, f, u_in, u_out, t, s, L.n_t, a.chunk, a.omega,
                                                    L.first_global);
     else
-      k_smooth<DIM, NL, false><<<grid, 128, 0, st>>>(f, u_in, u_out, t, s, L.n_t, a.chunk, a.omega,
+      PDLK(k_smooth<DIM, NL, false>, grid, 128, 0, st, f, u_in, u_out, t, s, L.n_t, a.chunk, a.omega,
                                                     L.first_global);
   });
   return cudaGetLastError();
@@ -1952,7 +1993,7 @@ cudaError_t launch_resnorm(const LevelView& L, ModalArgs& a, const double* u, co
   const dim3 grid(grid1(L.sp.nx, 128), unsigned((L.n_t + a.chunk - 1) / a.chunk));
   a.n_partials = i64(grid.x) * grid.y;
   STMG_DISPATCH(L.sp.dim, L.tc.nl, {
-    k_resnorm<DIM, NL><<<grid, 128, 0, st>>>(u, f, partials, make_tm<NL>(L.tc), s, L.n_t, a.chunk,
+    PDLK(k_resnorm<DIM, NL>, grid, 128, 0, st, u, f, partials, make_tm<NL>(L.tc), s, L.n_t, a.chunk,
                                             L.first_global);
   });
   return cudaGetLastError();
