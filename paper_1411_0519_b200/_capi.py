@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstmg_b200.so")
+LIB_PATH = os.environ.get("STMG_LIB") or os.path.join(_HERE, "libstmg_b200.so")
 
 STMG_OK, STMG_EINVAL, STMG_ERUNTIME = 0, 1, 2
 PATH_SPECTRAL, PATH_PHYSICAL = 0, 1

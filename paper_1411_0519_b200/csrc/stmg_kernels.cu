@@ -284,6 +284,29 @@ __device__ __forceinline__ double group_sum(double v) {
   return v;
 }
 
+// cp.async (LDGSTS) helpers: 8-byte copies, zero fill when !valid.
+__device__ __forceinline__ void cp_async8(double* smem, const double* g, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(g),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Per-thread asynchronous staging ring of the fused level kernels: stage st
+// of thread t holds the loads of one step pair; element q of a stage lives at
+// ring[(st * Q + q) * blockDim.x + t] (thread-fastest: conflict-free).
+constexpr int kRing = 3;  // stages: two step pairs in flight while one is used
+#ifndef STMG_DOWN_ASYNC
+#define STMG_DOWN_ASYNC 1
+#endif
+#ifndef STMG_UP_ASYNC
+#define STMG_UP_ASYNC 1
+#endif
+
 // ==================================================== fused spectral kernels
 // Loads: the standalone kernels read through the read-only / streaming paths;
 // the single-CTA tail kernel reads data written earlier in the same launch
@@ -306,12 +329,12 @@ __device__ __forceinline__ void ld_st(const double* p, i64 nx, double (&v)[NL]) 
 // the residual r_n = f_n - A_j u'_n + M_j N u'_{n-1}, and the restriction
 // c_{n/2} += fac * R_{1|2} r_n summed over the alias group (transfer.cpp:75-85,
 // 138-149 in the sine basis).  has_prev: step n0-1 exists (warm-up).
-template <int DIM, int NL, bool ZERO, int CO, bool COH>
+template <int DIM, int NL, bool ZERO, int CO, bool COH, bool ASYNC = false>
 __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64 nend,
                                           const double* f, const double* uin, double* uout,
                                           double* fc, const TM<NL>& t, const SP& s,
                                           const i64 n1c, const double omega, const bool has_prev,
-                                          const bool has_prev2) {
+                                          const bool has_prev2, double* ring = nullptr) {
   const Member me = make_member<DIM, COH>(s, tid, n1c, CO == 2);
   const i64 nx = s.nx, slab = NL * nx;
   const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
@@ -350,21 +373,41 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
     }
   }
 
-  // software pipeline: the loads of step pair n+2 are in flight while pair
-  // n is computed (memory-level parallelism; the kernel is latency bound)
+  // ASYNC: the loads of the next kRing-1 step pairs sit in a per-thread
+  // cp.async ring in shared memory (no registers held); otherwise a register
+  // prefetch of the next pair (memory-level parallelism; latency bound).
+  constexpr int Q = (ZERO ? 2 : 4) * NL;  // doubles per pair
+  const int T = blockDim.x;
+  auto issue = [&](i64 n, int st) {  // step pair n, n+1 -> ring stage st
+    double* r = ring + i64(st) * Q * T + threadIdx.x;
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        cp_async8(r + (e * NL + l) * T, fp + (n + e) * slab + l * nx, me.ok);
+        if (!ZERO) cp_async8(r + ((2 + e) * NL + l) * T, up + (n + e) * slab + l * nx, me.ok);
+      }
+  };
   double f2[2][NL], u2[2][NL];
 #pragma unroll
   for (int e = 0; e < 2; ++e)
 #pragma unroll
     for (int l = 0; l < NL; ++l) f2[e][l] = u2[e][l] = 0.0;
-  if (me.ok && n0 < nend) {
+  if (ASYNC) {
+#pragma unroll
+    for (int q = 0; q < kRing - 1; ++q) {
+      if (n0 + 2 * q < nend) issue(n0 + 2 * q, q);
+      cp_async_commit();
+    }
+  } else if (me.ok && n0 < nend) {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       ld_st<COH, NL>(fp + (n0 + e) * slab, nx, f2[e]);
       if (!ZERO) ld_st<COH, NL>(up + (n0 + e) * slab, nx, u2[e]);
     }
   }
-  for (i64 n = n0; n < nend; n += 2) {
+  int pair = 0;
+  for (i64 n = n0; n < nend; n += 2, ++pair) {
     double acc[NL];
 #pragma unroll
     for (int l = 0; l < NL; ++l) acc[l] = 0.0;
@@ -373,7 +416,19 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
     for (int e = 0; e < 2; ++e)
 #pragma unroll
       for (int l = 0; l < NL; ++l) fn[e][l] = un2[e][l] = 0.0;
-    if (me.ok && n + 2 < nend) {
+    if (ASYNC) {
+      cp_async_wait<kRing - 2>();  // this pair's stage has landed
+      const double* r = ring + i64(pair % kRing) * Q * T + threadIdx.x;
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          f2[e][l] = r[(e * NL + l) * T];
+          if (!ZERO) u2[e][l] = r[((2 + e) * NL + l) * T];
+        }
+      if (n + 2 * (kRing - 1) < nend) issue(n + 2 * (kRing - 1), (pair + kRing - 1) % kRing);
+      cp_async_commit();
+    } else if (me.ok && n + 2 < nend) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         ld_st<COH, NL>(fp + (n + 2 + e) * slab, nx, fn[e]);
@@ -411,13 +466,15 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
         un[l] = w[l];
       }
     }
+    if (!ASYNC) {
 #pragma unroll
-    for (int e = 0; e < 2; ++e)
+      for (int e = 0; e < 2; ++e)
 #pragma unroll
-      for (int l = 0; l < NL; ++l) {
-        f2[e][l] = fn[e][l];
-        u2[e][l] = un2[e][l];
-      }
+        for (int l = 0; l < NL; ++l) {
+          f2[e][l] = fn[e][l];
+          u2[e][l] = un2[e][l];
+        }
+    }
     const i64 nc = n >> 1;
     if (CO == 2) {
 #pragma unroll
@@ -432,12 +489,12 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
 // up: u <- u + P e_c (mg.cpp:123-127), then one damped block-Jacobi sweep
 // (mg.cpp:129-131); with RESID also the residual of the result, returning its
 // sum of squares (stop test, mg.cpp:152-153).
-template <int DIM, int NL, int CO, bool RESID, bool COH>
+template <int DIM, int NL, int CO, bool RESID, bool COH, bool ASYNC = false>
 __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64 nend,
                                           const double* ec, const double* uin, const double* f,
                                           double* uout, const TM<NL>& t, const SP& s,
                                           const i64 n1c, const double omega, const bool has_prev,
-                                          const bool has_prev2) {
+                                          const bool has_prev2, double* ring = nullptr) {
   const Member me = make_member<DIM, COH>(s, tid, n1c, CO == 2);
   const i64 nx = s.nx, slab = NL * nx;
   const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
@@ -484,13 +541,34 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
     }
   }
 
-  // software pipeline (see down_body); off for NL > 2, where the extra
-  // registers cost more occupancy than the prefetch gains (C3: -20 %)
-  constexpr bool PF = NL <= 2;
+  // software pipeline (see down_body); the register prefetch is off for
+  // NL > 2, where the extra registers cost more occupancy than it gains
+  constexpr bool PF = !ASYNC && NL <= 2;
+  constexpr int Q = 5 * NL;  // u, f of two steps + e of the coarse step
+  const int T = blockDim.x;
+  auto issue = [&](i64 n, int st) {
+    double* r = ring + i64(st) * Q * T + threadIdx.x;
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        cp_async8(r + (e * NL + l) * T, up + (n + e) * slab + l * nx, true);
+        cp_async8(r + ((2 + e) * NL + l) * T, fp + (n + e) * slab + l * nx, true);
+      }
+#pragma unroll
+    for (int l = 0; l < NL; ++l)
+      cp_async8(r + (4 * NL + l) * T, has_c ? ep + (n >> 1) * cslab + l * nxc : fp, has_c);
+  };
   double u2[2][NL], f2[2][NL], en[NL];
 #pragma unroll
   for (int l = 0; l < NL; ++l) en[l] = 0.0;
-  if (n0 < nend) {
+  if (ASYNC) {
+#pragma unroll
+    for (int q = 0; q < kRing - 1; ++q) {
+      if (n0 + 2 * q < nend) issue(n0 + 2 * q, q);
+      cp_async_commit();
+    }
+  } else if (n0 < nend) {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       ld_st<COH, NL>(up + (n0 + e) * slab, nx, u2[e]);
@@ -498,10 +576,26 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
     }
     if (has_c) ld_ro<COH, NL>(ep + (n0 >> 1) * cslab, nxc, en);
   }
-  for (i64 n = n0; n < nend; n += 2) {
+  int pair = 0;
+  for (i64 n = n0; n < nend; n += 2, ++pair) {
 #pragma unroll
     for (int l = 0; l < NL; ++l) ev[l] = en[l];
     double un2[2][NL], fn[2][NL];
+    if (ASYNC) {
+      cp_async_wait<kRing - 2>();
+      const double* r = ring + i64(pair % kRing) * Q * T + threadIdx.x;
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          u2[e][l] = r[(e * NL + l) * T];
+          f2[e][l] = r[((2 + e) * NL + l) * T];
+        }
+#pragma unroll
+      for (int l = 0; l < NL; ++l) ev[l] = r[(4 * NL + l) * T];
+      if (n + 2 * (kRing - 1) < nend) issue(n + 2 * (kRing - 1), (pair + kRing - 1) % kRing);
+      cp_async_commit();
+    }
     if (PF && n + 2 < nend) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
@@ -510,7 +604,7 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
       }
       if (has_c) ld_ro<COH, NL>(ep + ((n + 2) >> 1) * cslab, nxc, en);
     }
-    if (!PF && n > n0) {  // plain: load this pair now
+    if (!PF && !ASYNC && n > n0) {  // plain: load this pair now
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         ld_st<COH, NL>(up + (n + e) * slab, nx, u2[e]);
@@ -599,8 +693,10 @@ __global__ void __launch_bounds__(256) k_down(const double* __restrict__ f,
   const i64 tid = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   const i64 n0 = i64(blockIdx.y) * C;
   const i64 nend = min(n0 + i64(C), n_t);
-  down_body<DIM, NL, ZERO, CO, false>(tid, n0, nend, f, uin, uout, fc, t, s, n1c, omega,
-                                      n0 > 0 || !first_global, n0 - 1 > 0 || !first_global);
+  extern __shared__ double ring[];
+  down_body<DIM, NL, ZERO, CO, false, bool(STMG_DOWN_ASYNC)>(tid, n0, nend, f, uin, uout, fc, t, s, n1c, omega,
+                                            n0 > 0 || !first_global, n0 - 1 > 0 || !first_global,
+                                            ring);
   pdl_trigger();
 }
 
@@ -619,9 +715,10 @@ __global__ void __launch_bounds__(256) k_up(const double* __restrict__ ec,
   const i64 tid = i64(bx) * blockDim.x + threadIdx.x;
   const i64 n0 = i64(by) * C;
   const i64 nend = min(n0 + i64(C), n_t);
-  const double sumsq = up_body<DIM, NL, CO, RESID, false>(
+  extern __shared__ double ring[];
+  const double sumsq = up_body<DIM, NL, CO, RESID, false, bool(STMG_UP_ASYNC)>(
       tid, n0, nend, ec, uin, f, uout, t, s, n1c, omega, n0 > 0 || !first_global,
-      n0 - 1 > 0 || !first_global);
+      n0 - 1 > 0 || !first_global, ring);
   pdl_trigger();
   if (RESID) {
     const double tot = block_sum(sumsq, sh);
@@ -932,16 +1029,6 @@ struct ResTile {
   static constexpr int THREADS = TX * TY * TZ;
 };
 
-__device__ __forceinline__ void cp_async8(double* smem, const double* g, bool valid) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(g),
-               "r"(valid ? 8 : 0));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
 
 // Staging plan of one thread: the (tile + halo) x NL elements it copies each
 // step, as slab-relative global offsets (-1: outside the Dirichlet domain ->
@@ -1623,6 +1710,9 @@ __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, con
 }
 
 inline unsigned grid1(i64 n, int bs) { return unsigned((n + bs - 1) / bs); }
+// cp.async ring of the fused level kernels (128 threads, q doubles per pair)
+inline size_t ring_bytes(int q) { return size_t(kRing) * q * 128 * sizeof(double); }
+
 
 // Launch with programmatic stream serialization (see pdl_wait).
 template <typename... KArgs, typename... Args>
@@ -1638,6 +1728,8 @@ cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 #define PDLK(...)                                   \
@@ -1926,17 +2018,17 @@ cudaError_t launch_down(const LevelView& L, ModalArgs& a, bool zero_guess, const
     const TM<NL> t = make_tm<NL>(L.tc);
     if (a.mode == 2) {
       if (zero_guess)
-        PDLK(k_down<DIM, NL, true, 2>, grid, 128, 0, st, f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
+        PDLK(k_down<DIM, NL, true, 2>, grid, 128, ring_bytes(2 * NL), st, f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
                                                       a.n1c, a.omega, L.first_global);
       else
-        PDLK(k_down<DIM, NL, false, 2>, grid, 128, 0, st, f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
+        PDLK(k_down<DIM, NL, false, 2>, grid, 128, ring_bytes(4 * NL), st, f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
                                                        a.n1c, a.omega, L.first_global);
     } else {
       if (zero_guess)
-        PDLK(k_down<DIM, NL, true, 1>, grid, 128, 0, st, f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
+        PDLK(k_down<DIM, NL, true, 1>, grid, 128, ring_bytes(2 * NL), st, f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
                                                       L.sp.n1, a.omega, L.first_global);
       else
-        PDLK(k_down<DIM, NL, false, 1>, grid, 128, 0, st, f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
+        PDLK(k_down<DIM, NL, false, 1>, grid, 128, ring_bytes(4 * NL), st, f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
                                                        L.sp.n1, a.omega, L.first_global);
     }
   });
@@ -1954,17 +2046,17 @@ cudaError_t launch_up(const LevelView& L, ModalArgs& a, const double* ec, const 
     const i64 n1c = a.mode == 2 ? a.n1c : L.sp.n1;
     if (a.mode == 2) {
       if (partials)
-        PDLK(k_up<DIM, NL, 2, true>, grid, 128, 0, st, ec, u_in, f, u_out, partials, t, s, L.n_t,
+        PDLK(k_up<DIM, NL, 2, true>, grid, 128, ring_bytes(5 * NL), st, ec, u_in, f, u_out, partials, t, s, L.n_t,
                                                     a.chunk, n1c, a.omega, L.first_global);
       else
-        PDLK(k_up<DIM, NL, 2, false>, grid, 128, 0, st, ec, u_in, f, u_out, partials, t, s, L.n_t,
+        PDLK(k_up<DIM, NL, 2, false>, grid, 128, ring_bytes(5 * NL), st, ec, u_in, f, u_out, partials, t, s, L.n_t,
                                                      a.chunk, n1c, a.omega, L.first_global);
     } else {
       if (partials)
-        PDLK(k_up<DIM, NL, 1, true>, grid, 128, 0, st, ec, u_in, f, u_out, partials, t, s, L.n_t,
+        PDLK(k_up<DIM, NL, 1, true>, grid, 128, ring_bytes(5 * NL), st, ec, u_in, f, u_out, partials, t, s, L.n_t,
                                                     a.chunk, n1c, a.omega, L.first_global);
       else
-        PDLK(k_up<DIM, NL, 1, false>, grid, 128, 0, st, ec, u_in, f, u_out, partials, t, s, L.n_t,
+        PDLK(k_up<DIM, NL, 1, false>, grid, 128, ring_bytes(5 * NL), st, ec, u_in, f, u_out, partials, t, s, L.n_t,
                                                      a.chunk, n1c, a.omega, L.first_global);
     }
   });
