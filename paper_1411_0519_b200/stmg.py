@@ -131,7 +131,7 @@ class Hierarchy:
         prm = A.HierarchyParams(p_t, dim, space_level, time_level, t_final, mu_star, policy,
                                 two_grid, device, shards)
         ctx = C.c_void_p()
-        if world > 1:
+        if world > 1 or nccl_id is not None:
             if nccl_id is None:
                 raise ValueError("world > 1 needs the NCCL id of rank 0")
             check(A.lib().stmg_create_distributed(C.byref(prm), rank, world, nccl_id,

@@ -258,3 +258,50 @@ def test_cpp_shim_solves_c1(S):
     o = O.Hierarchy(1, 1, 5, 6)
     _, rep_o = o.solve(O.make_inputs(o, 42))
     assert rep["iterations"] == rep_o["iterations"]
+
+
+@pytest.mark.parametrize("case", [
+    (1, 1, 3, 0, 1.0, 0),   # single time step: the hierarchy is one level (n_t = 1)
+    (1, 2, 0, 5, 1.0, 0),   # one spatial node, 32 steps (semi coarsening only)
+    (0, 1, 4, 4, 1.0, 1),   # p_t = 0, always_semi
+    (3, 1, 3, 3, 1.0, 2),   # p_t = 3, prefer_full
+    (1, 3, 2, 4, 0.25, 0),  # 3D
+])
+def test_solve_edge_cases_match_oracle(S, case):
+    p, dim, sl, tl, T, pol = case
+    g, o = pair(S, p, dim, sl, tl, T, pol)
+    f = O.fill_uniform(o.levels[0].size, 77, 0)
+    u0 = O.fill_uniform(o.levels[0].size, 78, 0)
+    u_o, rep_o = o.solve(f, u0, eps=1e-9)
+    du = g.upload(u0)
+    rep = g.solve(g.upload(f), du, S.CycleConfig(nu1=1, nu2=1), 1e-9)
+    assert rep.converged and rep.iterations == rep_o["iterations"]
+    assert rel(du.numpy(), u_o) < 1e-10
+
+
+def test_solve_zero_rhs_and_iteration_cap(S):
+    g = S.Hierarchy(1, 2, 3, 4)
+    f = g.vector(0)  # zero rhs and zero guess: r0 = 0 -> converged, no cycles (mg.cpp:146-149)
+    u = g.vector(0)
+    rep = g.solve(f, u, S.CycleConfig(nu1=1, nu2=1), 1e-8)
+    assert rep.converged and rep.iterations == 0 and rep.residual_history == [0.0]
+    g.fill_uniform(f, 5, 0)
+    rep = g.solve(f, u, S.CycleConfig(nu1=1, nu2=1), 1e-14, max_iter=3)
+    assert not rep.converged and rep.iterations == 3 and len(rep.residual_history) == 4
+    o = O.Hierarchy(1, 2, 3, 4)
+    _, rep_o = o.solve(O.fill_uniform(o.levels[0].size, 5, 0), eps=1e-14, max_iter=3)
+    assert not rep_o["converged"]
+    assert rel(np.array(rep.residual_history), np.array(rep_o["residual_history"])) < 1e-10
+
+
+def test_distributed_api_single_rank(S):
+    """stmg_create_distributed with world = 1 is the plain context (the
+    multi-rank path needs one GPU per rank)."""
+    uid = S.Hierarchy.unique_id()
+    g = S.Hierarchy(1, 2, 4, 5, rank=0, world=1, nccl_id=uid)
+    assert g.local_steps() == (0, 32)
+    o = O.Hierarchy(1, 2, 4, 5)
+    f = O.make_inputs(o, 42)
+    _, rep_o = o.solve(f)
+    rep = g.solve(g.upload(f), g.vector(0), S.CycleConfig(nu1=1, nu2=1), 1e-8)
+    assert rep.iterations == rep_o["iterations"]
