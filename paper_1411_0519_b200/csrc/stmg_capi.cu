@@ -160,9 +160,15 @@ struct stmg_ctx {
   int* h_flag = nullptr;  // pinned
   // device-side solve loop (conditional while node): cached per configuration
   std::map<std::string, cudaGraphExec_t> loops;
+  std::map<std::string, i64> loop_kernels;  // kernels per body iteration
+  // fused schedule: device ping-pong table {U0[0], U0[1]} and its selector
+  double** d_pp = nullptr;
+  int* d_par = nullptr;
+  std::map<std::string, cudaGraphExec_t> fused_bodies;  // per-cycle graphs (profiling)
   int* d_iter = nullptr;
   double* d_r0 = nullptr;
   bool use_device_loop = true;
+  bool use_fused = true;  // fused level-0 schedule for V(1,1) solves
 };
 
 namespace {
@@ -675,7 +681,7 @@ int nu_flips(const stmg_cycle_config& cfg) { return std::max(cfg.nu1, 1) + std::
 // iterate in the buffer it started from (true for V(1,1), any nu1 + nu2 even).
 template <class Body>
 cudaGraphExec_t device_loop(stmg_ctx* c, const std::string& key, double eps, int max_iter,
-                            Body&& body) {
+                            Body&& body, int* parity = nullptr) {
   auto it = c->loops.find(key);
   if (it != c->loops.end()) return it->second;
   cudaGraph_t g;
@@ -696,7 +702,7 @@ cudaGraphExec_t device_loop(stmg_ctx* c, const std::string& key, double eps, int
                                    cudaStreamCaptureModeThreadLocal));
   try {
     body();
-    CK(stmg::launch_decide(h, c->d_norm, c->d_r0, c->d_hist, c->d_iter, eps, max_iter,
+    CK(stmg::launch_decide(h, c->d_norm, c->d_r0, c->d_hist, c->d_iter, eps, max_iter, parity,
                            c->stream));
     count(c);
   } catch (...) {
@@ -713,6 +719,7 @@ cudaGraphExec_t device_loop(stmg_ctx* c, const std::string& key, double eps, int
   CK(cudaGraphInstantiate(&exec, g, 0));
   CK(cudaGraphDestroy(g));
   c->loops[key] = exec;
+  c->loop_kernels[key] = c->captured_kernels;
   return exec;
 }
 
@@ -742,6 +749,137 @@ void run_device_loop(stmg_ctx* c, cudaGraphExec_t exec, int max_iter, double* hi
   r.r_final = it > 0 ? h[it] : r.r0;
   r.converged = (it > 0 && h[it] <= eps * r.r0) ? 1 : 0;
   (void)max_iter;
+}
+
+// ---- fused V(1,1) schedule: one pass over level 0 per cycle ----------------
+// prefix: down(0) of cycle 1; then per cycle k: coarse levels of cycle k,
+// k_updown (post-smooth k + stop-test residual + pre-smooth/restrict k+1),
+// norm, stop test (+ swap of the level-0 buffers); suffix: up(0) of the last
+// cycle recomputed from its inputs (still intact) to produce the result.
+bool fused_eligible(const stmg_ctx* c, const stmg_cycle_config& cfg) {
+  return c->use_fused && cfg.path == STMG_PATH_SPECTRAL && cfg.nu1 == 1 && cfg.nu2 == 1 &&
+         cfg.gamma == 1 && c->levels.size() >= 2 && c->levels[0].spec.coarsen != 0;
+}
+
+// Coarse part (levels >= 1) of one V(1,1) cycle, zero initial guess.
+void coarse_cycle(stmg_ctx* c, const stmg_cycle_config& cfg) {
+  if (c->tail_table && c->tail_start == 1) {
+    CK(stmg::launch_tail(c->dim, c->p_t + 1, c->tail_table, c->tail_host,
+                         int(c->levels.size()) - 1, cfg.omega_t, c->tail_smem, c->stream));
+    count(c);
+    for (int l = 1; l < int(c->levels.size()); ++l) c->cur[l] = 0;
+  } else {
+    spectral_cycle(c, 1, true, cfg, false, nullptr);
+  }
+}
+
+// One fused cycle body (captured): coarse(k), k_updown, norm.
+void fused_body(stmg_ctx* c, const stmg_cycle_config& cfg, i64* np) {
+  Level& L = c->levels[0];
+  Level& C = c->levels[1];
+  coarse_cycle(c, cfg);
+  stmg::ModalArgs a = modal_args(L, &C, cfg.omega_t, true);
+  prof_begin(c, 0);
+  CK(stmg::launch_updown(L.view, a, C.U[c->cur[1]].base, c->d_pp, c->d_par, L.F.base, C.F.base,
+                         c->partials.base, c->stream));
+  prof_end(c, 0, 8.0 * double(3 * L.view.size() + 2 * C.view.size()));
+  count(c);
+  *np = a.n_partials;
+  CK(stmg::launch_norm_final(c->partials.base, *np, c->d_norm, nullptr, 0, c->stream));
+  count(c);
+}
+
+// Runs the cycles of a solve whose finest iterate is in U0[0] (r0 known and
+// > 0); leaves the result in U0[c->cur[0]].  Fills r and history.
+void run_fused(stmg_ctx* c, const stmg_cycle_config& cfg, double eps, int max_iter,
+               double* history, int history_cap, int* nh, stmg_solve_report& r,
+               bool u_zero) {
+  Level& L = c->levels[0];
+  Level& C = c->levels[1];
+  ensure_hist(c, max_iter + 1);
+  // prefix: pre-smooth + restriction of cycle 1 into U0[1], F1
+  {
+    stmg::ModalArgs a = modal_args(L, &C, cfg.omega_t, true);
+    CK(stmg::launch_down(L.view, a, u_zero, L.F.base, L.U[0].base, L.U[1].base, C.F.base,
+                         c->stream));
+    count(c);
+  }
+  double* tbl[2] = {L.U[0].base, L.U[1].base};
+  const int par1 = 1;
+  CK(cudaMemcpyAsync(c->d_pp, tbl, sizeof(tbl), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->d_par, &par1, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->d_r0, c->d_norm, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->d_hist, c->d_norm, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemsetAsync(c->d_iter, 0, sizeof(int), c->stream));
+  int iters = 0;
+  if (c->use_device_loop && !c->profile) {
+    cudaGraphExec_t ex = device_loop(
+        c, loop_key("fused", cfg, 0, eps, max_iter), eps, max_iter,
+        [&] {
+          i64 np = 0;
+          fused_body(c, cfg, &np);
+        },
+        c->d_par);
+    CK(cudaGraphLaunch(ex, c->stream));
+    CK(cudaMemcpyAsync(&iters, c->d_iter, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->launches += iters * c->loop_kernels[loop_key("fused", cfg, 0, eps, max_iter)];
+  } else {  // host-driven cycles (profiling: event records around k_updown)
+    const std::string key = loop_key("fusedbody", cfg, 0, eps, max_iter);
+    auto it = c->fused_bodies.find(key);
+    if (it == c->fused_bodies.end()) {
+      cudaGraph_t g;
+      c->capturing = true;
+      c->captured_kernels = 0;
+      CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        i64 np = 0;
+        fused_body(c, cfg, &np);
+        CK(stmg::launch_decide(0, c->d_norm, c->d_r0, c->d_hist, c->d_iter, eps, max_iter,
+                               c->d_par, c->stream));
+        count(c);
+        CK(cudaMemcpyAsync(c->h_norm, c->d_norm, sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+      } catch (...) {
+        cudaStreamEndCapture(c->stream, &g);
+        c->capturing = false;
+        throw;
+      }
+      CK(cudaStreamEndCapture(c->stream, &g));
+      c->capturing = false;
+      cudaGraphExec_t ex;
+      CK(cudaGraphInstantiate(&ex, g, 0));
+      CK(cudaGraphDestroy(g));
+      it = c->fused_bodies.emplace(key, ex).first;
+    }
+    for (int k = 0; k < max_iter; ++k) {
+      CK(cudaGraphLaunch(it->second, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      prof_collect_graph(c);
+      ++iters;
+      if (*c->h_norm <= eps * r.r0) break;
+    }
+  }
+  // history and report
+  std::vector<double> h(size_t(iters) + 1);
+  CK(cudaMemcpy(h.data(), c->d_hist, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  for (int k = 1; k <= iters; ++k) {
+    if (history && *nh < history_cap) history[*nh] = h[k];
+    ++*nh;
+  }
+  r.iterations = iters;
+  r.r_final = iters > 0 ? h[iters] : r.r0;
+  r.converged = (iters > 0 && h[iters] <= eps * r.r0) ? 1 : 0;
+  // suffix: the last cycle's post-smooth from its (intact) inputs; after an
+  // even number of cycles the last input A is U0[1], after an odd number U0[0]
+  const int a_last = (iters % 2 == 1) ? 1 : 0;
+  {
+    stmg::ModalArgs a = modal_args(L, &C, cfg.omega_t, true);
+    CK(stmg::launch_up(L.view, a, C.U[c->cur[1]].base, L.U[a_last].base, L.F.base,
+                       L.U[1 - a_last].base, nullptr, c->stream));
+    count(c);
+  }
+  c->cur[0] = 1 - a_last;
 }
 
 void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config& cfg, double eps,
@@ -792,10 +930,17 @@ void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config
     r.r0 = r.r_final = r0;
     push(r0);
     if (r0 == 0.0) r.converged = 1;
+    const bool fused = fused_eligible(c, cfg) && !r.converged && max_iter > 0;
+    if (fused) run_fused(c, cfg, eps, max_iter, history, history_cap, &nh, r, !*c->h_flag);
     // the device-side loop needs the finest iterate back in its buffer after
     // a cycle; the per-cycle graph (kept for profiling) reports where it ends
-    const stmg_ctx::GraphEntry& probe = cycle_graph(c, cfg);
-    const bool loop_ok = c->use_device_loop && !c->profile && probe.cur0_after == c->cur[0];
+    bool loop_ok = false;
+    i64 probe_kernels = 0;
+    if (!fused) {
+      const stmg_ctx::GraphEntry& probe = cycle_graph(c, cfg);
+      loop_ok = c->use_device_loop && !c->profile && probe.cur0_after == c->cur[0];
+      probe_kernels = probe.kernels;
+    }
     if (loop_ok && !r.converged && max_iter > 0) {
       ensure_hist(c, max_iter + 1);
       CK(cudaMemcpyAsync(c->d_r0, c->d_norm, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
@@ -812,9 +957,9 @@ void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config
                                        });
       c->cur[0] = cur0;
       run_device_loop(c, ex, max_iter, history, history_cap, &nh, r, eps);
-      c->launches += r.iterations * (probe.kernels + 1);
+      c->launches += r.iterations * (probe_kernels + 1);
     }
-    for (int k = 0; k < max_iter && !r.converged && !loop_ok; ++k) {
+    for (int k = 0; k < max_iter && !r.converged && !loop_ok && !fused; ++k) {
       stmg_ctx::GraphEntry& g = cycle_graph(c, cfg);
       CK(cudaGraphLaunch(g.exec, c->stream));
       c->launches += g.kernels;
@@ -1419,8 +1564,11 @@ int stmg_create(const stmg_hierarchy_params* p, stmg_ctx** out) {
     CK(cudaMallocHost(&c->h_norm, sizeof(double)));
     CK(cudaMalloc(&c->d_flag, sizeof(int)));
     CK(cudaMalloc(&c->d_iter, sizeof(int)));
+    CK(cudaMalloc(&c->d_pp, 2 * sizeof(double*)));
+    CK(cudaMalloc(&c->d_par, sizeof(int)));
     CK(cudaMalloc(&c->d_r0, sizeof(double)));
     if (const char* e = std::getenv("STMG_DEVICE_LOOP")) c->use_device_loop = std::atoi(e) != 0;
+    if (const char* e = std::getenv("STMG_FUSED")) c->use_fused = std::atoi(e) != 0;
     CK(cudaMallocHost(&c->h_flag, sizeof(int)));
     CK(cudaEventCreate(&c->ev_solve[0]));
     CK(cudaEventCreate(&c->ev_solve[1]));
@@ -1473,6 +1621,9 @@ int stmg_destroy(stmg_ctx* c) {
     cudaFree(c->d_hist);
     cudaFree(c->d_flag);
     cudaFree(c->d_iter);
+    cudaFree(c->d_pp);
+    cudaFree(c->d_par);
+    for (auto& kv : c->fused_bodies) cudaGraphExecDestroy(kv.second);
     cudaFree(c->d_r0);
     for (auto& kv : c->loops) cudaGraphExecDestroy(kv.second);
     cudaFreeHost(c->h_flag);

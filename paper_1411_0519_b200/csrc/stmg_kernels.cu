@@ -656,6 +656,203 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
   return sumsq;
 }
 
+// updown: the post-smooth of cycle k (prolongation + correction + damped
+// Jacobi, mg.cpp:123-131) fused with the pre-smooth, residual and restriction
+// of cycle k+1 (mg.cpp:106-117) in ONE pass over a level, plus the residual
+// sum of squares of the post-smoothed iterate (the stop test of cycle k,
+// mg.cpp:152-153).  Per step n (chains kept in registers):
+//   v = u + P e                         corrected iterate of cycle k
+//   w = (1-w) v + w A^-1 (f + M N v_{n-1})     post-smoothed (cycle k result)
+//   r = f - A w + M N w_{n-1}           stop-test residual
+//   x = (1-w) w + w A^-1 (f + M N w_{n-1})     pre-smoothed (cycle k+1)
+//   c_{n/2} += fac R (f - A x + M N x_{n-1})   restricted residual (cycle k+1)
+// A three-step warm-up rebuilds v, w, x of step n0-1.  Non-sharded only.
+template <int DIM, int NL, int CO>
+__device__ __forceinline__ double updown_body(const i64 tid, const i64 n0, const i64 nend,
+                                              const double* ec, const double* uin,
+                                              const double* f, double* uout, double* fc,
+                                              const TM<NL>& t, const SP& s, const i64 n1c,
+                                              const double omega, double* ring) {
+  const Member me = make_member<DIM>(s, tid, n1c, CO == 2);
+  const i64 nx = s.nx, slab = NL * nx;
+  const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
+  const double om1 = 1.0 - omega;
+  const double Mj = me.Mj, Kj = me.Kj;
+  const double fac = (CO == 2) ? me.fac : 1.0;
+  const bool has_c = (CO == 2) ? me.cok : me.ok;
+  const double* ep = ec + ((CO == 2) ? me.cidx : me.idx);
+  const double* fp = f + me.idx;
+  const double* up = uin + me.idx;
+  double* op = uout + me.idx;
+  double sumsq = 0.0;
+
+  // corrected iterate v of step m (m >= 0)
+  auto vstep = [&](i64 m, double (&v)[NL]) {
+    double u[NL], e[NL], c[NL];
+    load_nl<NL>(up + m * slab, nx, u);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) e[l] = 0.0;
+    if (has_c) load_nl<NL>(ep + (m >> 1) * cslab, nxc, e);
+    if (m & 1) matvec_t<NL>(t.R2, e, c);
+    else matvec_t<NL>(t.R1, e, c);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) v[l] = u[l] + fac * c[l];
+  };
+  // damped Jacobi sweep of one step: out = (1-w) cur + w A^-1 (fv + M N prev)
+  auto sweep = [&](const double (&cur)[NL], const double (&prev)[NL], const double (&fv)[NL],
+                   double (&out)[NL]) {
+    double nv[NL], rhs[NL], x[NL];
+    matvec<NL>(t.N, prev, nv);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) rhs[l] = fv[l] + Mj * nv[l];
+    solve_mode<NL>(t, Mj, Kj, rhs, x);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) out[l] = om1 * cur[l] + omega * x[l];
+  };
+
+  double vp[NL], wp[NL], xp[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) vp[l] = wp[l] = xp[l] = 0.0;
+  if (me.ok && n0 > 0) {  // warm-up: steps n0-3 .. n0-1
+    double v3[NL], v2[NL], w2[NL], f2v[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) v3[l] = w2[l] = 0.0;
+    if (n0 - 3 >= 0) vstep(n0 - 3, v3);
+    vstep(n0 - 2, v2);
+    load_nl<NL>(fp + (n0 - 2) * slab, nx, f2v);
+    sweep(v2, v3, f2v, w2);
+    double v1[NL], w1[NL], x1[NL], f1v[NL];
+    vstep(n0 - 1, v1);
+    load_nl<NL>(fp + (n0 - 1) * slab, nx, f1v);
+    sweep(v1, v2, f1v, w1);
+    sweep(w1, w2, f1v, x1);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      vp[l] = v1[l];
+      wp[l] = w1[l];
+      xp[l] = x1[l];
+    }
+  }
+
+  constexpr int Q = 5 * NL;  // u, f of two steps + e of the coarse step
+  const int T = blockDim.x;
+  auto issue = [&](i64 n, int st) {
+    double* r = ring + i64(st) * Q * T + threadIdx.x;
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        cp_async8(r + (e * NL + l) * T, up + (n + e) * slab + l * nx, me.ok);
+        cp_async8(r + ((2 + e) * NL + l) * T, fp + (n + e) * slab + l * nx, me.ok);
+      }
+#pragma unroll
+    for (int l = 0; l < NL; ++l)
+      cp_async8(r + (4 * NL + l) * T, has_c ? ep + (n >> 1) * cslab + l * nxc : fp, has_c);
+  };
+#pragma unroll
+  for (int q = 0; q < kRing - 1; ++q) {
+    if (n0 + 2 * q < nend) issue(n0 + 2 * q, q);
+    cp_async_commit();
+  }
+  int pair = 0;
+  for (i64 n = n0; n < nend; n += 2, ++pair) {
+    double u2[2][NL], f2[2][NL], ev[NL];
+    cp_async_wait<kRing - 2>();
+    {
+      const double* r = ring + i64(pair % kRing) * Q * T + threadIdx.x;
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          u2[e][l] = r[(e * NL + l) * T];
+          f2[e][l] = r[((2 + e) * NL + l) * T];
+        }
+#pragma unroll
+      for (int l = 0; l < NL; ++l) ev[l] = r[(4 * NL + l) * T];
+    }
+    if (n + 2 * (kRing - 1) < nend) issue(n + 2 * (kRing - 1), (pair + kRing - 1) % kRing);
+    cp_async_commit();
+    double acc[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) acc[l] = 0.0;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const i64 m = n + e;
+      double c[NL], v[NL], w[NL], x[NL], aw[NL], np[NL], rt[NL], res[NL];
+      if (e == 0) matvec_t<NL>(t.R1, ev, c);
+      else matvec_t<NL>(t.R2, ev, c);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) v[l] = u2[e][l] + fac * c[l];
+      sweep(v, vp, f2[e], w);
+      // stop-test residual of the post-smoothed iterate
+      apply_mode<NL>(t, Mj, Kj, w, aw);
+      matvec<NL>(t.N, wp, np);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        const double r = f2[e][l] - aw[l] + Mj * np[l];
+        sumsq += me.ok ? r * r : 0.0;
+      }
+      // next cycle's pre-smoothing, residual and restriction
+      sweep(w, wp, f2[e], x);
+      if (me.ok) store_nl<NL>(op + m * slab, nx, x);
+      apply_mode<NL>(t, Mj, Kj, x, aw);
+      matvec<NL>(t.N, xp, np);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) res[l] = f2[e][l] - aw[l] + Mj * np[l];
+      if (e == 0) matvec<NL>(t.R1, res, rt);
+      else matvec<NL>(t.R2, res, rt);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        acc[l] += (CO == 2) ? me.fac * rt[l] : rt[l];
+        vp[l] = v[l];
+        wp[l] = w[l];
+        xp[l] = x[l];
+      }
+    }
+    const i64 nc = n >> 1;
+    if (CO == 2) {
+#pragma unroll
+      for (int l = 0; l < NL; ++l) acc[l] = group_sum<DIM>(me.ok ? acc[l] : 0.0);
+      if (me.cok && (tid & ((1 << DIM) - 1)) == 0) store_nl<NL>(fc + nc * cslab + me.cidx, nxc, acc);
+    } else if (me.ok) {
+      store_nl<NL>(fc + nc * cslab + me.idx, nxc, acc);
+    }
+  }
+  return sumsq;
+}
+
+// Ping-pong level-0 buffers selected on the device (the solve graph is
+// replayed unchanged while the buffers alternate): A = tbl[*par] holds the
+// pre-smoothed iterate of cycle k, B = tbl[1 - *par] receives cycle k+1's.
+struct PingPong {
+  double* const* tbl;
+  const int* par;
+};
+
+template <int DIM, int NL, int CO>
+__global__ void __launch_bounds__(128) k_updown(const double* __restrict__ ec, const PingPong pp,
+                                                const double* __restrict__ f,
+                                                double* __restrict__ fc,
+                                                double* __restrict__ partials, const TM<NL> t,
+                                                const SP s, const i64 n_t, const int C,
+                                                const i64 n1c, const double omega) {
+  pdl_wait();
+  __shared__ double sh[32];
+  extern __shared__ double ring[];
+  const int p = *pp.par;
+  const double* uin = pp.tbl[p];
+  double* uout = pp.tbl[1 - p];
+  const unsigned bx = blockIdx.x, by = blockIdx.y;
+  const i64 tid = i64(bx) * blockDim.x + threadIdx.x;
+  const i64 n0 = i64(by) * C;
+  const i64 nend = min(n0 + i64(C), n_t);
+  const double sumsq =
+      updown_body<DIM, NL, CO>(tid, n0, nend, ec, uin, f, uout, fc, t, s, n1c, omega, ring);
+  pdl_trigger();
+  const double tot = block_sum(sumsq, sh);
+  if (threadIdx.x == 0) partials[i64(by) * gridDim.x + bx] = tot;
+}
+
 // Per-mode forward substitution u_n = A_j^-1 (f_n + M_j N u_{n-1})
 // (st_system.cpp:118-130 in the sine basis).
 template <int DIM, int NL, bool COH>
@@ -1693,14 +1890,16 @@ __global__ void k_nonzero(const double* __restrict__ v, const i64 n, int* __rest
 // and set the while-loop condition of the solve graph.
 __global__ void k_decide(cudaGraphConditionalHandle h, const double* __restrict__ norm,
                          const double* __restrict__ r0, double* __restrict__ hist,
-                         int* __restrict__ iter, const double eps, const int max_iter) {
+                         int* __restrict__ iter, const double eps, const int max_iter,
+                         int* __restrict__ parity) {
   pdl_wait();
   const int k = *iter + 1;
   *iter = k;
   const double rk = *norm;
   hist[k] = rk;
   const bool more = !(rk <= eps * (*r0)) && k < max_iter;
-  cudaGraphSetConditional(h, more ? 1u : 0u);
+  if (parity) *parity = 1 - *parity;  // fused schedule: swap the level-0 buffers
+  if (h) cudaGraphSetConditional(h, more ? 1u : 0u);
 }
 
 __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, const double a,
@@ -1925,8 +2124,29 @@ cudaError_t launch_fill_uniform(double* v, int64_t n, uint64_t seed, uint64_t st
 }
 
 cudaError_t launch_decide(cudaGraphConditionalHandle h, const double* norm, const double* r0,
-                          double* hist, int* iter, double eps, int max_iter, cudaStream_t st) {
-  PDLK(k_decide, 1, 1, 0, st, h, norm, r0, hist, iter, eps, max_iter);
+                          double* hist, int* iter, double eps, int max_iter, int* parity,
+                          cudaStream_t st) {
+  PDLK(k_decide, 1, 1, 0, st, h, norm, r0, hist, iter, eps, max_iter, parity);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_updown(const LevelView& L, ModalArgs& a, const double* ec,
+                          double* const* tbl, const int* par, const double* f, double* fc,
+                          double* partials, cudaStream_t st) {
+  const SP s = make_sp(L.sp);
+  const i64 lanes = ipow(s.G, L.sp.dim) << L.sp.dim;
+  const dim3 grid(grid1(lanes, 128), unsigned((L.n_t + a.chunk - 1) / a.chunk));
+  a.n_partials = i64(grid.x) * grid.y;
+  const PingPong pp{tbl, par};
+  STMG_DISPATCH(L.sp.dim, L.tc.nl, {
+    const TM<NL> t = make_tm<NL>(L.tc);
+    if (a.mode == 2)
+      PDLK(k_updown<DIM, NL, 2>, grid, 128, ring_bytes(5 * NL), st, ec, pp, f, fc, partials, t,
+           s, L.n_t, a.chunk, a.n1c, a.omega);
+    else
+      PDLK(k_updown<DIM, NL, 1>, grid, 128, ring_bytes(5 * NL), st, ec, pp, f, fc, partials, t,
+           s, L.n_t, a.chunk, L.sp.n1, a.omega);
+  });
   return cudaGetLastError();
 }
 

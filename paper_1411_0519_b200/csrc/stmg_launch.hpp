@@ -76,7 +76,8 @@ cudaError_t launch_axpy(double* y, const double* x, double a, int64_t n,
 // Device-side stop test: hist[++iter] = norm; loop while norm > eps*r0 and
 // iter < max_iter (sets the conditional handle of the solve graph).
 cudaError_t launch_decide(cudaGraphConditionalHandle h, const double* norm, const double* r0,
-                          double* hist, int* iter, double eps, int max_iter, cudaStream_t st);
+                          double* hist, int* iter, double eps, int max_iter, int* parity,
+                          cudaStream_t st);
 
 // ---- fused spectral V-cycle kernels (sine coefficients) -------------------
 struct ModalArgs {
@@ -99,6 +100,11 @@ cudaError_t launch_up(const LevelView& L, ModalArgs& a, const double* ec,
 cudaError_t launch_smooth(const LevelView& L, ModalArgs& a, bool zero_guess,
                           const double* f, const double* u_in, double* u_out,
                           cudaStream_t st);
+// Fused level-0 kernel: post-smooth of cycle k + pre-smooth/residual/restriction of
+// cycle k+1 (+ stop-test partials).  Buffers: A = tbl[*par] (in), B = tbl[1 - *par] (out).
+cudaError_t launch_updown(const LevelView& L, ModalArgs& a, const double* ec,
+                          double* const* tbl, const int* par, const double* f, double* fc,
+                          double* partials, cudaStream_t st);
 // Residual sum-of-squares partials of f - L u.
 cudaError_t launch_resnorm(const LevelView& L, ModalArgs& a, const double* u,
                            const double* f, double* partials, cudaStream_t st);
