@@ -332,25 +332,24 @@ def run_ours(args, cfgname):
     A.lib().stmg_host_free(h._ctx, hu)
 
     peak, peak_kind = peaks()
-    ms0, n0l, b0 = prof[0]
-    ms1, n1l, b1 = prof[1]
-    dom = 0 if ms0 >= ms1 else 1
+    fused = prof[1][1] == 0  # fused schedule: slot 0 = k_updown, no standalone k_up
+    names = ({0: "k_updown (level 0: post-smooth of cycle k + stop-test residual + pre-smooth "
+                 "and restriction of cycle k+1, one pass)"} if fused else
+             {0: "k_down (level 0: pre-smooth + residual + restrict)",
+              1: "k_up (level 0: prolong + correct + post-smooth + residual norm)"})
+    cands = [k for k in names if prof[k][1]]
+    dom = max(cands, key=lambda k: prof[k][0])
     ms, nl, b = prof[dom]
-    avg_s = (ms / nl) * 1e-3 if nl else float("nan")
-    achieved = b / avg_s / 1e9 if nl else None
-    names = {0: "k_down (level 0: pre-smooth + residual + restrict)",
-             1: "k_up (level 0: prolong + correct + post-smooth + residual norm)"}
+    avg_s = (ms / nl) * 1e-3
+    achieved = b / avg_s / 1e9
+    tag = {0: "k_updown" if fused else "k_down", 1: "k_up"}[dom]
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak if achieved else None,
-            "traffic": traffic_from_profiles("k_down" if dom == 0 else "k_up"),
+            "frac": achieved / peak, "traffic": traffic_from_profiles(tag),
             "kernel": names[dom], "peak_kind": peak_kind,
             "algorithmic_bytes_per_launch": b, "avg_launch_ms": avg_s * 1e3,
-            "step_share": (ms0 + ms1) / (1e3 * sum(prof_dev)) if prof_dev else None,
+            "step_share": sum(prof[k][0] for k in names) / (1e3 * sum(prof_dev)) if prof_dev else None,
             "measured": "CUDA events on the library stream around every launch, in a replay of "
                         "the K timed steps right after the timed region",
-            "other_kernel": {"name": names[1 - dom],
-                             "achieved_gbs": (prof[1 - dom][2] / (prof[1 - dom][0] / prof[1 - dom][1] * 1e-3) / 1e9)
-                             if prof[1 - dom][1] else None},
             "transform_ms_per_solve": prof[2][0] / max(len(prof_dev), 1)}
 
     line = {

@@ -32,7 +32,9 @@ def run(name, reps=5):
         rep = h.solve(f, u, cc, 1e-8)
     out = {"config": name, "dofs": n0, "iterations": rep.iterations,
            "solve_ms": rep.device_time_seconds * 1e3}
-    names = {0: "k_down_l0", 1: "k_up_l0", 2: "transform"}
+    fused = h.profile_read(1)[1] == 0
+    names = ({0: "k_updown_l0", 2: "transform"} if fused else
+             {0: "k_down_l0", 1: "k_up_l0", 2: "transform"})
     for k, nm in names.items():
         ms, n, b = h.profile_read(k)
         if n:
