@@ -1050,7 +1050,8 @@ struct Shard {
   std::vector<ShardLevel> lv;  // sharded levels 0..lg-1
   std::vector<int> cur;
   DevBuf Fg;  // local part of F_lg (written by down(lg-1))
-  DevBuf Eg;  // local part of the coarse correction at lg (+1 halo slab)
+  DevBuf Eg;  // local part of the coarse correction at lg (+2 halo slabs)
+  DevBuf tbl;  // {U0[0], U0[1]} base pointers (fused schedule's ping-pong table)
 };
 
 struct ShardSet {
@@ -1060,6 +1061,7 @@ struct ShardSet {
   ncclComm_t comm = nullptr;
   std::vector<Shard> local;  // virtual: all S shards; nccl: this rank's
   DevBuf partials;           // S * P partial sums (global chunk order)
+  DevBuf par01;              // device ints {0, 1}: fixed ping-pong parities
   i64 P = 0;                 // partials per shard (level-0 residual)
   i64 m = 0;                 // coarse steps per shard at lg
   bool built = false;
@@ -1096,7 +1098,8 @@ void build_shards(stmg_ctx* c) {
       s.view = c->levels[l].view;
       s.view.n_t = c->levels[l].spec.n_t / ss.S;
       s.view.first_global = sh.g == 0;
-      const i64 n = s.view.size(), halo = 2 * s.view.slab();
+      // level 0: 3 halo slabs (the fused k_updown's warm-up reads steps -3..-1)
+      const i64 n = s.view.size(), halo = (l == 0 ? 3 : 2) * s.view.slab();
       s.F.alloc(n, halo);
       s.U[0].alloc(n, halo);
       s.U[1].alloc(n, halo);
@@ -1104,6 +1107,14 @@ void build_shards(stmg_ctx* c) {
     const i64 cslab = c->levels[lg].view.slab();
     sh.Fg.alloc(ss.m * cslab, 2 * cslab);
     sh.Eg.alloc(ss.m * cslab, 2 * cslab);
+    sh.tbl.alloc(2, 0);
+    double* t2[2] = {sh.lv[0].U[0].base, sh.lv[0].U[1].base};
+    CK(cudaMemcpy(sh.tbl.base, t2, sizeof(t2), cudaMemcpyHostToDevice));
+  }
+  {
+    ss.par01.alloc(1, 0);
+    const int p01[2] = {0, 1};
+    CK(cudaMemcpy(ss.par01.base, p01, sizeof(p01), cudaMemcpyHostToDevice));
   }
   // root holds the gathered levels (full size)
   bool have_root = false;
@@ -1177,16 +1188,18 @@ void gather_rhs(stmg_ctx* c) {
   nccl_check(N.GroupEnd(), "group end");
 }
 
-// root's coarse correction at lg -> every shard's Eg (+ the step before).
+// root's coarse correction at lg -> every shard's Eg (+ the two steps before:
+// k_up reads one, the fused k_updown's warm-up two).
 void scatter_corr(stmg_ctx* c) {
   ShardSet& ss = *c->shards;
   const i64 cslab = c->levels[ss.lg].view.slab();
+  auto nh = [&](int g) { return std::min<i64>(2, i64(g) * ss.m); };
   auto src_of = [&](int g) {
     const double* E = c->levels[ss.lg].U[c->cur[ss.lg]].base;
-    return E + (g * ss.m - (g > 0 ? 1 : 0)) * cslab;
+    return E + (g * ss.m - nh(g)) * cslab;
   };
-  auto count_of = [&](int g) { return size_t((ss.m + (g > 0 ? 1 : 0)) * cslab); };
-  auto dst_of = [&](Shard& sh) { return sh.Eg.base - (sh.g > 0 ? cslab : 0); };
+  auto count_of = [&](int g) { return size_t((ss.m + nh(g)) * cslab); };
+  auto dst_of = [&](Shard& sh) { return sh.Eg.base - nh(sh.g) * cslab; };
   if (!ss.nccl) {
     for (Shard& sh : ss.local)
       CK(cudaMemcpyAsync(dst_of(sh), src_of(sh.g), count_of(sh.g) * sizeof(double),
@@ -1234,12 +1247,14 @@ stmg::ModalArgs shard_args(stmg_ctx* c, int l, const ShardLevel& s, double omega
 }
 
 // One V-cycle (gamma = 1) over the sharded levels + the root's tail, plus the
-// residual norm into d_norm (and h_norm).
-void sharded_cycle(stmg_ctx* c, const stmg_cycle_config& cfg, bool copy_norm = true) {
+// residual norm into d_norm (and h_norm).  from = 1: only the coarse part
+// (levels >= 1, zero guess) of the fused schedule -- no norm.
+void sharded_cycle(stmg_ctx* c, const stmg_cycle_config& cfg, bool copy_norm = true,
+                   int from = 0) {
   ShardSet& ss = *c->shards;
   const int lg = ss.lg;
   const int nu1 = cfg.nu1, nu2 = cfg.nu2;
-  for (int l = 0; l < lg; ++l) {
+  for (int l = from; l < lg; ++l) {
     const stmg::LevelView& v = ss.local[0].lv[l].view;
     const i64 n_loc = v.n_t, slab = v.slab();
     bool zero = l > 0;
@@ -1286,7 +1301,7 @@ void sharded_cycle(stmg_ctx* c, const stmg_cycle_config& cfg, bool copy_norm = t
     }
   }
   scatter_corr(c);
-  for (int l = lg - 1; l >= 0; --l) {
+  for (int l = lg - 1; l >= from; --l) {
     const stmg::LevelView& v = ss.local[0].lv[l].view;
     const i64 n_loc = v.n_t, slab = v.slab();
     if (l + 1 < lg) {
@@ -1334,12 +1349,143 @@ void sharded_cycle(stmg_ctx* c, const stmg_cycle_config& cfg, bool copy_norm = t
       }
     }
   }
+  if (from > 0) return;
   const i64 np = shard_np(c, nu2 == 1);
   allgather_partials(c, np);
   CK(stmg::launch_norm_final(ss.partials.base, ss.S * np, c->d_norm, nullptr, 0, c->stream));
   count(c);
   if (copy_norm)
     CK(cudaMemcpyAsync(c->h_norm, c->d_norm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+}
+
+// ---- fused V(1,1) schedule on time slabs (see run_fused) -------------------
+// Same passes as the single-device schedule; per cycle the level-0 exchange is
+// 3 slabs of the pre-smoothed iterate A (k_updown's warm-up rebuilds steps
+// -3..-1) and 2 coarse-correction slabs; the rhs halo (2 slabs) is sent once
+// per solve.  Buffer parity alternates per cycle, so the host drives the
+// cycles with two captured graphs (A = U0[1], A = U0[0]).
+bool sharded_fused_ok(stmg_ctx* c, const stmg_cycle_config& cfg) {
+  const ShardSet& ss = *c->shards;
+  return fused_eligible(c, cfg) && ss.local[0].lv[0].view.n_t >= 4;
+}
+
+const double* shard_ec(stmg_ctx* c, Shard& sh) {
+  return c->shards->lg > 1 ? sh.lv[1].U[sh.cur[1]].base : sh.Eg.base;
+}
+
+double* shard_fc(stmg_ctx* c, Shard& sh) {
+  return c->shards->lg > 1 ? sh.lv[1].F.base : sh.Fg.base;
+}
+
+// One cycle body: coarse part, halos, k_updown per shard, norm, stop test.
+void sharded_fused_body(stmg_ctx* c, const stmg_cycle_config& cfg, int pa, double eps,
+                        int max_iter) {
+  ShardSet& ss = *c->shards;
+  sharded_cycle(c, cfg, false, 1);
+  if (ss.lg > 1) {
+    const stmg::LevelView& v1 = ss.local[0].lv[1].view;
+    halo(c, v1.n_t, v1.slab(), 2, [&](Shard& sh) { return sh.lv[1].U[sh.cur[1]].base; });
+  }
+  const stmg::LevelView& v0 = ss.local[0].lv[0].view;
+  halo(c, v0.n_t, v0.slab(), 3, [&](Shard& sh) { return sh.lv[0].U[pa].base; });
+  const i64 np = shard_np(c, true);  // k_updown's partials = k_up's (grouped)
+  for (Shard& sh : ss.local) {
+    ShardLevel& L = sh.lv[0];
+    stmg::ModalArgs a = shard_args(c, 0, L, cfg.omega_t, true);
+    const bool p = sh.g == 0;
+    if (p) prof_begin(c, 0);
+    CK(stmg::launch_updown(L.view, a, shard_ec(c, sh),
+                           reinterpret_cast<double* const*>(sh.tbl.base),
+                           reinterpret_cast<const int*>(ss.par01.base) + pa, L.F.base,
+                           shard_fc(c, sh), ss.partials.base + sh.g * np, c->stream,
+                           int64_t(sh.g) * v0.n_t));
+    if (p) {
+      const Level& C = c->levels[1];
+      prof_end(c, 0, 8.0 * double(3 * L.view.size() + 2 * C.view.size() / ss.S));
+    }
+    count(c);
+    require(np == a.n_partials, "partial count mismatch");
+  }
+  allgather_partials(c, np);
+  CK(stmg::launch_norm_final(ss.partials.base, ss.S * np, c->d_norm, nullptr, 0, c->stream));
+  count(c);
+  CK(stmg::launch_decide(0, c->d_norm, c->d_r0, c->d_hist, c->d_iter, eps, max_iter, nullptr,
+                         c->stream));
+  count(c);
+  CK(cudaMemcpyAsync(c->h_norm, c->d_norm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+}
+
+void run_sharded_fused(stmg_ctx* c, const stmg_cycle_config& cfg, double eps, int max_iter,
+                       double* history, int history_cap, int* nh, stmg_solve_report& r,
+                       bool u_zero) {
+  ShardSet& ss = *c->shards;
+  const stmg::LevelView& v0 = ss.local[0].lv[0].view;
+  ensure_hist(c, max_iter + 1);
+  halo(c, v0.n_t, v0.slab(), 2, [&](Shard& sh) { return sh.lv[0].F.base; });
+  // prefix: pre-smooth + restriction of cycle 1 into U0[1]
+  if (!u_zero) halo(c, v0.n_t, v0.slab(), 2, [&](Shard& sh) { return sh.lv[0].U[0].base; });
+  for (Shard& sh : ss.local) {
+    ShardLevel& L = sh.lv[0];
+    stmg::ModalArgs a = shard_args(c, 0, L, cfg.omega_t, true);
+    CK(stmg::launch_down(L.view, a, u_zero, L.F.base, L.U[0].base, L.U[1].base, shard_fc(c, sh),
+                         c->stream));
+    count(c);
+  }
+  CK(cudaMemcpyAsync(c->d_r0, c->d_norm, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->d_hist, c->d_norm, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemsetAsync(c->d_iter, 0, sizeof(int), c->stream));
+  int iters = 0;
+  for (int k = 0; k < max_iter; ++k) {
+    const int pa = (k % 2 == 0) ? 1 : 0;  // A of cycle k
+    const std::string key = loop_key(pa ? "shfused1" : "shfused0", cfg, 0, eps, max_iter);
+    auto it = c->fused_bodies.find(key);
+    if (it == c->fused_bodies.end()) {
+      cudaGraph_t g;
+      c->capturing = true;
+      c->captured_kernels = 0;
+      CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        sharded_fused_body(c, cfg, pa, eps, max_iter);
+      } catch (...) {
+        cudaStreamEndCapture(c->stream, &g);
+        c->capturing = false;
+        throw;
+      }
+      CK(cudaStreamEndCapture(c->stream, &g));
+      c->capturing = false;
+      cudaGraphExec_t ex;
+      CK(cudaGraphInstantiate(&ex, g, 0));
+      CK(cudaGraphDestroy(g));
+      c->loop_kernels[key] = c->captured_kernels;
+      it = c->fused_bodies.emplace(key, ex).first;
+    }
+    CK(cudaGraphLaunch(it->second, c->stream));
+    c->launches += c->loop_kernels[key];
+    CK(cudaStreamSynchronize(c->stream));
+    prof_collect_graph(c);
+    ++iters;
+    if (*c->h_norm <= eps * r.r0) break;
+  }
+  std::vector<double> h(size_t(iters) + 1);
+  CK(cudaMemcpy(h.data(), c->d_hist, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  for (int k = 1; k <= iters; ++k) {
+    if (history && *nh < history_cap) history[*nh] = h[k];
+    ++*nh;
+  }
+  r.iterations = iters;
+  r.r_final = iters > 0 ? h[iters] : r.r0;
+  r.converged = (iters > 0 && h[iters] <= eps * r.r0) ? 1 : 0;
+  // suffix: the last cycle's post-smooth from its intact inputs (A and the
+  // correction, whose halos the last body already exchanged)
+  const int a_last = (iters % 2 == 1) ? 1 : 0;
+  for (Shard& sh : ss.local) {
+    ShardLevel& L = sh.lv[0];
+    stmg::ModalArgs a = shard_args(c, 0, L, cfg.omega_t, true);
+    CK(stmg::launch_up(L.view, a, shard_ec(c, sh), L.U[a_last].base, L.F.base,
+                       L.U[1 - a_last].base, nullptr, c->stream));
+    count(c);
+    sh.cur[0] = 1 - a_last;
+  }
 }
 
 // Sharded solve: f, u are this process's time slabs (virtual shards: the whole
@@ -1420,9 +1566,12 @@ void solve_sharded(stmg_ctx* c, const double* f, double* u, const stmg_cycle_con
   r.r0 = r.r_final = r0;
   push(r0);
   if (r0 == 0.0) r.converged = 1;
+  const bool fused = sharded_fused_ok(c, cfg) && !r.converged && max_iter > 0;
+  if (fused) run_sharded_fused(c, cfg, eps, max_iter, history, history_cap, &nh, r, !u_nonzero);
   // virtual shards: all cycles in one graph (device-side stop test); the
   // finest parity is preserved when nu1 + nu2 is even
-  const bool loop_ok = !ss.nccl && c->use_device_loop && !c->profile && (nu_flips(cfg) % 2 == 0);
+  const bool loop_ok = !fused && !ss.nccl && c->use_device_loop && !c->profile &&
+                       (nu_flips(cfg) % 2 == 0);
   if (loop_ok && !r.converged && max_iter > 0) {
     ensure_hist(c, max_iter + 1);
     CK(cudaMemcpyAsync(c->d_r0, c->d_norm, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
@@ -1434,7 +1583,7 @@ void solve_sharded(stmg_ctx* c, const double* f, double* u, const stmg_cycle_con
     for (size_t i = 0; i < ss.local.size(); ++i) ss.local[i].cur[0] = cur0[i];
     run_device_loop(c, ex, max_iter, history, history_cap, &nh, r, eps);
   }
-  for (int k = 0; k < max_iter && !r.converged && !loop_ok; ++k) {
+  for (int k = 0; k < max_iter && !r.converged && !loop_ok && !fused; ++k) {
     // the cycle's buffer parity pattern is the same every iteration (coarse
     // levels restart at buffer 0) except the finest level's, so at most two
     // graphs; key on shard 0's finest parity
@@ -1593,8 +1742,10 @@ int stmg_destroy(stmg_ctx* c) {
           for (DevBuf* b : {&L.F, &L.U[0], &L.U[1]}) b->release();
         sh.Fg.release();
         sh.Eg.release();
+        sh.tbl.release();
       }
       c->shards->partials.release();
+      c->shards->par01.release();
       if (c->shards->comm) nccl().CommDestroy(c->shards->comm);
       c->shards.reset();
     }

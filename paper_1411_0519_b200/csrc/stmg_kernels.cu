@@ -307,6 +307,7 @@ constexpr int kRing = 3;  // stages: two step pairs in flight while one is used
 #define STMG_UP_ASYNC 1
 #endif
 
+
 // ==================================================== fused spectral kernels
 // Loads: the standalone kernels read through the read-only / streaming paths;
 // the single-CTA tail kernel reads data written earlier in the same launch
@@ -672,7 +673,7 @@ __device__ __forceinline__ double updown_body(const i64 tid, const i64 n0, const
                                               const double* ec, const double* uin,
                                               const double* f, double* uout, double* fc,
                                               const TM<NL>& t, const SP& s, const i64 n1c,
-                                              const double omega, double* ring) {
+                                              const double omega, double* ring, const i64 s0) {
   const Member me = make_member<DIM>(s, tid, n1c, CO == 2);
   const i64 nx = s.nx, slab = NL * nx;
   const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
@@ -713,11 +714,12 @@ __device__ __forceinline__ double updown_body(const i64 tid, const i64 n0, const
   double vp[NL], wp[NL], xp[NL];
 #pragma unroll
   for (int l = 0; l < NL; ++l) vp[l] = wp[l] = xp[l] = 0.0;
-  if (me.ok && n0 > 0) {  // warm-up: steps n0-3 .. n0-1
+  // s0: global index of local step 0 (sharded: steps -1..-3 are halo slabs)
+  if (me.ok && s0 + n0 > 0) {  // warm-up: steps n0-3 .. n0-1
     double v3[NL], v2[NL], w2[NL], f2v[NL];
 #pragma unroll
     for (int l = 0; l < NL; ++l) v3[l] = w2[l] = 0.0;
-    if (n0 - 3 >= 0) vstep(n0 - 3, v3);
+    if (s0 + n0 - 3 >= 0) vstep(n0 - 3, v3);
     vstep(n0 - 2, v2);
     load_nl<NL>(fp + (n0 - 2) * slab, nx, f2v);
     sweep(v2, v3, f2v, w2);
@@ -835,7 +837,8 @@ __global__ void __launch_bounds__(128) k_updown(const double* __restrict__ ec, c
                                                 double* __restrict__ fc,
                                                 double* __restrict__ partials, const TM<NL> t,
                                                 const SP s, const i64 n_t, const int C,
-                                                const i64 n1c, const double omega) {
+                                                const i64 n1c, const double omega,
+                                                const i64 s0) {
   pdl_wait();
   __shared__ double sh[32];
   extern __shared__ double ring[];
@@ -847,7 +850,7 @@ __global__ void __launch_bounds__(128) k_updown(const double* __restrict__ ec, c
   const i64 n0 = i64(by) * C;
   const i64 nend = min(n0 + i64(C), n_t);
   const double sumsq =
-      updown_body<DIM, NL, CO>(tid, n0, nend, ec, uin, f, uout, fc, t, s, n1c, omega, ring);
+      updown_body<DIM, NL, CO>(tid, n0, nend, ec, uin, f, uout, fc, t, s, n1c, omega, ring, s0);
   pdl_trigger();
   const double tot = block_sum(sumsq, sh);
   if (threadIdx.x == 0) partials[i64(by) * gridDim.x + bx] = tot;
@@ -2132,7 +2135,7 @@ cudaError_t launch_decide(cudaGraphConditionalHandle h, const double* norm, cons
 
 cudaError_t launch_updown(const LevelView& L, ModalArgs& a, const double* ec,
                           double* const* tbl, const int* par, const double* f, double* fc,
-                          double* partials, cudaStream_t st) {
+                          double* partials, cudaStream_t st, int64_t s0) {
   const SP s = make_sp(L.sp);
   const i64 lanes = ipow(s.G, L.sp.dim) << L.sp.dim;
   const dim3 grid(grid1(lanes, 128), unsigned((L.n_t + a.chunk - 1) / a.chunk));
@@ -2142,10 +2145,10 @@ cudaError_t launch_updown(const LevelView& L, ModalArgs& a, const double* ec,
     const TM<NL> t = make_tm<NL>(L.tc);
     if (a.mode == 2)
       PDLK(k_updown<DIM, NL, 2>, grid, 128, ring_bytes(5 * NL), st, ec, pp, f, fc, partials, t,
-           s, L.n_t, a.chunk, a.n1c, a.omega);
+           s, L.n_t, a.chunk, a.n1c, a.omega, i64(s0));
     else
       PDLK(k_updown<DIM, NL, 1>, grid, 128, ring_bytes(5 * NL), st, ec, pp, f, fc, partials, t,
-           s, L.n_t, a.chunk, L.sp.n1, a.omega);
+           s, L.n_t, a.chunk, L.sp.n1, a.omega, i64(s0));
   });
   return cudaGetLastError();
 }

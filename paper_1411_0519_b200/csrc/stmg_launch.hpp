@@ -102,9 +102,10 @@ cudaError_t launch_smooth(const LevelView& L, ModalArgs& a, bool zero_guess,
                           cudaStream_t st);
 // Fused level-0 kernel: post-smooth of cycle k + pre-smooth/residual/restriction of
 // cycle k+1 (+ stop-test partials).  Buffers: A = tbl[*par] (in), B = tbl[1 - *par] (out).
+// s0: global index of local step 0 (time-slab shards read steps -3..-1 from halos).
 cudaError_t launch_updown(const LevelView& L, ModalArgs& a, const double* ec,
                           double* const* tbl, const int* par, const double* f, double* fc,
-                          double* partials, cudaStream_t st);
+                          double* partials, cudaStream_t st, int64_t s0 = 0);
 // Residual sum-of-squares partials of f - L u.
 cudaError_t launch_resnorm(const LevelView& L, ModalArgs& a, const double* u,
                            const double* f, double* partials, cudaStream_t st);

@@ -6,7 +6,8 @@ rank g+1, per-step norm partials all-gathered and summed in global order --
 checked against the undecomposed operator (dense oracle).
 GPU: virtual shards on one device run the exact multi-GPU code path (halo /
 gather / scatter / partial all-gather with D2D copies instead of NCCL); their
-iterates and residual histories must be BITWISE equal to the 1-shard solve.
+iterates and residual histories must be BITWISE equal to the 1-shard solve,
+for the per-level and the fused level-0 schedule alike.
 """
 import os
 import socket
@@ -121,23 +122,23 @@ def test_virtual_shards_bitwise(cfg, S):
     o = O.Hierarchy(p, dim, sl, tl, t_final=T)
     f = O.make_inputs(o, 42, random_u0=(dim == 2))
     cc = stmg.CycleConfig(nu1=1, nu2=1)
-    # the sharded driver runs the per-level schedule; compare it with the
-    # same schedule on one shard (the fused level-0 schedule of the single
-    # context may round differently in the last bit; it is checked against
-    # the oracle in test_gpu_parity.py)
-    os.environ["STMG_FUSED"] = "0"
-    try:
-        g1 = stmg.Hierarchy(p, dim, sl, tl, t_final=T)
-    finally:
-        os.environ.pop("STMG_FUSED", None)
-    u1 = g1.vector(0)
-    r1 = g1.solve(g1.upload(f), u1, cc, 1e-8)
-    gs = stmg.Hierarchy(p, dim, sl, tl, t_final=T, shards=S)
-    us = gs.vector(0)
-    rs = gs.solve(gs.upload(f), us, cc, 1e-8)
-    assert rs.iterations == r1.iterations
-    assert rs.residual_history == r1.residual_history
-    assert np.array_equal(us.numpy(), u1.numpy())
+    # both schedules -- per-level (STMG_FUSED=0) and fused level-0 (default)
+    # -- on S shards against the same schedule on one shard
+    for fused in ("0", "1"):
+        os.environ["STMG_FUSED"] = fused
+        try:
+            g1 = stmg.Hierarchy(p, dim, sl, tl, t_final=T)
+            gs = stmg.Hierarchy(p, dim, sl, tl, t_final=T, shards=S)
+        finally:
+            os.environ.pop("STMG_FUSED", None)
+        u1 = g1.vector(0)
+        r1 = g1.solve(g1.upload(f), u1, cc, 1e-8)
+        us = gs.vector(0)
+        rs = gs.solve(gs.upload(f), us, cc, 1e-8)
+        assert rs.iterations == r1.iterations, fused
+        assert rs.residual_history == r1.residual_history, fused
+        assert np.array_equal(us.numpy(), u1.numpy()), fused
+        del g1, gs
 
 
 @pytest.mark.gpu
@@ -162,3 +163,29 @@ def test_virtual_shards_general_cycle_and_initial_guess():
     u_o, rep_o = o.solve(f, u0, nu1=2, nu2=2, eps=1e-9)
     assert rep_o["iterations"] == r2.iterations
     assert np.abs(u2.numpy() - u_o).max() <= 1e-10 * np.abs(u_o).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("S", [2, 4, 8])
+def test_virtual_shards_fused_nonzero_guess_vs_oracle(S):
+    """Fused sharded schedule from a nonzero initial guess (prefix k_down with
+    a 2-slab halo), checked bitwise against one shard and against the oracle."""
+    from oracle import oracle as O
+    from paper_1411_0519_b200 import build, stmg
+    build.build()
+    p, dim, sl, tl = 2, 1, 6, 7
+    o = O.Hierarchy(p, dim, sl, tl)
+    f = O.fill_uniform(o.levels[0].size, 11, 0)
+    u0 = O.fill_uniform(o.levels[0].size, 12, 0)
+    cc = stmg.CycleConfig(nu1=1, nu2=1)
+    g1 = stmg.Hierarchy(p, dim, sl, tl)
+    u1 = g1.upload(u0)
+    r1 = g1.solve(g1.upload(f), u1, cc, 1e-9)
+    gs = stmg.Hierarchy(p, dim, sl, tl, shards=S)
+    us = gs.upload(u0)
+    rs = gs.solve(gs.upload(f), us, cc, 1e-9)
+    assert rs.iterations == r1.iterations and rs.residual_history == r1.residual_history
+    assert np.array_equal(us.numpy(), u1.numpy())
+    u_o, rep_o = o.solve(f, u0, nu1=1, nu2=1, eps=1e-9)
+    assert rep_o["iterations"] == rs.iterations
+    assert np.abs(us.numpy() - u_o).max() <= 1e-10 * np.abs(u_o).max()
