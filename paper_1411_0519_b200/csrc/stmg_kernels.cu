@@ -85,37 +85,52 @@ __device__ __forceinline__ void pdl_trigger() {
 // ------------------------------------------------------------ per-mode math
 // Exact per-mode block: A_j = M_j K_tau + K_j M_tau.  Its symmetric part is
 // positive definite (K_tau + K_tau^T = psi(tau)psi(tau)^T + psi(0)psi(0)^T),
-// so elimination without pivoting is stable.
+// so elimination without pivoting is stable.  A_j is constant along a mode's
+// time line, so its factors are computed once per thread (the divisions and
+// the assembly leave the time loop) and solve() runs the substitutions.
 template <int NL>
-__device__ __forceinline__ void solve_mode(const TM<NL>& t, double Mj, double Kj,
-                                           const double (&b)[NL], double (&x)[NL]) {
-  double A[NL][NL];
-#pragma unroll
-  for (int i = 0; i < NL; ++i)
-#pragma unroll
-    for (int j = 0; j < NL; ++j) A[i][j] = Mj * t.K[i][j] + Kj * t.M[i][j];
+struct ModeLU {
   double inv[NL];
+  double L[NL][NL];  // multipliers (r > c)
+  double U[NL][NL];  // eliminated rows (k > c)
+  __device__ __forceinline__ ModeLU(const TM<NL>& t, double Mj, double Kj) {
+    double A[NL][NL];
 #pragma unroll
-  for (int i = 0; i < NL; ++i) x[i] = b[i];
+    for (int i = 0; i < NL; ++i)
 #pragma unroll
-  for (int c = 0; c < NL; ++c) {
-    inv[c] = 1.0 / A[c][c];
+      for (int j = 0; j < NL; ++j) A[i][j] = Mj * t.K[i][j] + Kj * t.M[i][j];
 #pragma unroll
-    for (int r = c + 1; r < NL; ++r) {
-      const double f = A[r][c] * inv[c];
+    for (int c = 0; c < NL; ++c) {
+      inv[c] = 1.0 / A[c][c];
 #pragma unroll
-      for (int k = c + 1; k < NL; ++k) A[r][k] -= f * A[c][k];
-      x[r] -= f * x[c];
+      for (int r = c + 1; r < NL; ++r) {
+        const double f = A[r][c] * inv[c];
+        L[r][c] = f;
+#pragma unroll
+        for (int k = c + 1; k < NL; ++k) A[r][k] -= f * A[c][k];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NL; ++c)
+#pragma unroll
+      for (int k = c + 1; k < NL; ++k) U[c][k] = A[c][k];
+  }
+  __device__ __forceinline__ void solve(const double (&b)[NL], double (&x)[NL]) const {
+#pragma unroll
+    for (int i = 0; i < NL; ++i) x[i] = b[i];
+#pragma unroll
+    for (int c = 0; c < NL; ++c)
+#pragma unroll
+      for (int r = c + 1; r < NL; ++r) x[r] -= L[r][c] * x[c];
+#pragma unroll
+    for (int c = NL - 1; c >= 0; --c) {
+      double s = x[c];
+#pragma unroll
+      for (int k = c + 1; k < NL; ++k) s -= U[c][k] * x[k];
+      x[c] = s * inv[c];
     }
   }
-#pragma unroll
-  for (int c = NL - 1; c >= 0; --c) {
-    double s = x[c];
-#pragma unroll
-    for (int k = c + 1; k < NL; ++k) s -= A[c][k] * x[k];
-    x[c] = s * inv[c];
-  }
-}
+};
 
 // y = A_j x
 template <int NL>
@@ -341,6 +356,7 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
   const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
   const double om1 = 1.0 - omega;
   const double Mj = me.Mj, Kj = me.Kj;
+  const ModeLU<NL> lu(t, Mj, Kj);
   const double* fp = f + me.idx;
   const double* up = uin + me.idx;
   double* op = uout + me.idx;
@@ -353,7 +369,7 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
     double fv[NL], x[NL];
     ld_ro<COH, NL>(fp + (n0 - 1) * slab, nx, fv);
     if (ZERO) {
-      solve_mode<NL>(t, Mj, Kj, fv, x);
+      lu.solve(fv, x);
 #pragma unroll
       for (int l = 0; l < NL; ++l) un[l] = omega * x[l];
     } else {
@@ -365,7 +381,7 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
       matvec<NL>(t.N, u2, nv);
 #pragma unroll
       for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
-      solve_mode<NL>(t, Mj, Kj, fv, x);
+      lu.solve(fv, x);
 #pragma unroll
       for (int l = 0; l < NL; ++l) {
         un[l] = om1 * u1[l] + omega * x[l];
@@ -449,7 +465,7 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
 #pragma unroll
         for (int l = 0; l < NL; ++l) rhs[l] = f2[e][l];
       }
-      solve_mode<NL>(t, Mj, Kj, rhs, x);
+      lu.solve(rhs, x);
 #pragma unroll
       for (int l = 0; l < NL; ++l) w[l] = ZERO ? omega * x[l] : om1 * u2[e][l] + omega * x[l];
       if (me.ok) store_nl<NL>(op + m * slab, nx, w);
@@ -501,6 +517,7 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
   const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
   const double om1 = 1.0 - omega;
   const double Mj = me.Mj, Kj = me.Kj;
+  const ModeLU<NL> lu(t, Mj, Kj);
   const double fac = (CO == 2) ? me.fac : 1.0;
   const bool has_c = (CO == 2) ? me.cok : me.ok;
   const double* ep = ec + ((CO == 2) ? me.cidx : me.idx);
@@ -536,7 +553,7 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
       matvec<NL>(t.N, v2, nv);
 #pragma unroll
       for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
-      solve_mode<NL>(t, Mj, Kj, fv, x);
+      lu.solve(fv, x);
 #pragma unroll
       for (int l = 0; l < NL; ++l) wp[l] = om1 * vo[l] + omega * x[l];
     }
@@ -624,7 +641,7 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
       matvec<NL>(t.N, vo, nv);
 #pragma unroll
       for (int l = 0; l < NL; ++l) rhs[l] = f2[e][l] + Mj * nv[l];
-      solve_mode<NL>(t, Mj, Kj, rhs, x);
+      lu.solve(rhs, x);
 #pragma unroll
       for (int l = 0; l < NL; ++l) w[l] = om1 * v[l] + omega * x[l];
       store_nl<NL>(op + m * slab, nx, w);
@@ -679,6 +696,7 @@ __device__ __forceinline__ double updown_body(const i64 tid, const i64 n0, const
   const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
   const double om1 = 1.0 - omega;
   const double Mj = me.Mj, Kj = me.Kj;
+  const ModeLU<NL> lu(t, Mj, Kj);
   const double fac = (CO == 2) ? me.fac : 1.0;
   const bool has_c = (CO == 2) ? me.cok : me.ok;
   const double* ep = ec + ((CO == 2) ? me.cidx : me.idx);
@@ -706,7 +724,7 @@ __device__ __forceinline__ double updown_body(const i64 tid, const i64 n0, const
     matvec<NL>(t.N, prev, nv);
 #pragma unroll
     for (int l = 0; l < NL; ++l) rhs[l] = fv[l] + Mj * nv[l];
-    solve_mode<NL>(t, Mj, Kj, rhs, x);
+    lu.solve(rhs, x);
 #pragma unroll
     for (int l = 0; l < NL; ++l) out[l] = om1 * cur[l] + omega * x[l];
   };
@@ -864,6 +882,7 @@ __device__ __forceinline__ void fwdsub_body(const i64 r, const double* f, double
   if (r >= s.nx) return;
   double Mj, Kj;
   mode_eig<DIM, COH>(s, r, Mj, Kj);
+  const ModeLU<NL> lu(t, Mj, Kj);
   const i64 nx = s.nx, slab = NL * nx;
   double prev[NL];
 #pragma unroll
@@ -874,7 +893,7 @@ __device__ __forceinline__ void fwdsub_body(const i64 r, const double* f, double
     matvec<NL>(t.N, prev, nv);
 #pragma unroll
     for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
-    solve_mode<NL>(t, Mj, Kj, fv, x);
+    lu.solve(fv, x);
     store_nl<NL>(u + m * slab + r, nx, x);
 #pragma unroll
     for (int l = 0; l < NL; ++l) prev[l] = x[l];
@@ -1072,6 +1091,7 @@ __global__ void __launch_bounds__(128) k_smooth(const double* __restrict__ f,
   if (r >= s.nx) return;
   double Mj, Kj;
   mode_eig<DIM>(s, r, Mj, Kj);
+  const ModeLU<NL> lu(t, Mj, Kj);
   const i64 nx = s.nx, slab = NL * nx;
   const i64 n0 = i64(blockIdx.y) * C;
   const i64 nend = min(n0 + i64(C), n_t);
@@ -1088,7 +1108,7 @@ __global__ void __launch_bounds__(128) k_smooth(const double* __restrict__ f,
 #pragma unroll
       for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
     }
-    solve_mode<NL>(t, Mj, Kj, fv, x);
+    lu.solve(fv, x);
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
       w[l] = ZERO ? omega * x[l] : (1.0 - omega) * uv[l] + omega * x[l];
@@ -1154,11 +1174,12 @@ __global__ void __launch_bounds__(256) k_modal_solve(double* __restrict__ x, con
   if (r >= s.nx) return;
   double Mj, Kj;
   mode_eig<DIM>(s, r, Mj, Kj);
+  const ModeLU<NL> lu(t, Mj, Kj);
   for (i64 n = blockIdx.y; n < n_t; n += gridDim.y) {
     double b[NL], y[NL];
     double* p = x + n * NL * s.nx + r;
     load_nl<NL>(p, s.nx, b);
-    solve_mode<NL>(t, Mj, Kj, b, y);
+    lu.solve(b, y);
     store_nl<NL>(p, s.nx, y);
   }
 }

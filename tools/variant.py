@@ -1,0 +1,22 @@
+"""Build an A/B variant of the library with extra nvcc defines:
+
+  python tools/variant.py NAME -DSTMG_COARSE_MINB=1 ...
+-> paper_1411_0519_b200/_variant_NAME.so (load it with STMG_LIB=<path>).
+"""
+import os
+import subprocess
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1411_0519_b200 import build as B  # noqa: E402
+
+name, defs = sys.argv[1], sys.argv[2:]
+B.build()
+obj = os.path.join(B.OBJ, f"stmg_kernels_{name}.o")
+subprocess.run([B.nvcc()] + B.NVFLAGS + defs + ["-c", os.path.join(B.CSRC, "stmg_kernels.cu"),
+                                               "-o", obj], check=True)
+others = [os.path.join(B.OBJ, o) for o in ("stmg_capi.o", "stmg_setup.o")]
+out = os.path.join(B.PKG, f"_variant_{name}.so")
+subprocess.run([B.nvcc()] + B.ARCH + ["-shared", "-o", out, obj] + others + ["-cudart", "static"],
+               check=True)
+print(out)
