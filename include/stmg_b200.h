@@ -183,9 +183,12 @@ int stmg_local_steps(const stmg_ctx* ctx, int64_t* first_step,
                      int64_t* n_steps);
 
 /* ---- live per-kernel timing (CUDA events inside the cycle) --------------- */
-/* Kernel ids: 0 = fused pre-smooth+residual+restrict on the finest level,
+/* Kernel ids: 0 = fused pre-smooth+residual+restrict on the finest level
+ *                 (fused V(1,1) schedule: the k_updown pass),
  *             1 = fused prolong+correct+post-smooth+residual-norm (finest),
- *             2 = basis transform pass, 3 = physical residual. */
+ *             2 = basis transform pass, 3 = physical residual,
+ *             4 = coarse part of a fused V(1,1) cycle (levels >= 1, all
+ *                 kernels between two finest-level passes; bytes = 0). */
 int stmg_profile_enable(stmg_ctx* ctx, int on);
 int stmg_profile_read(stmg_ctx* ctx, int kernel_id, double* total_ms,
                       int64_t* launches, double* bytes_per_launch);

@@ -146,7 +146,7 @@ struct stmg_ctx {
   std::vector<int> cur;  // current U buffer per level
   // profiling
   bool profile = false;
-  ProfSlot prof[4];
+  ProfSlot prof[5];
   i64 launches = 0;
   bool capturing = false;
   i64 captured_kernels = 0;
@@ -777,7 +777,9 @@ void coarse_cycle(stmg_ctx* c, const stmg_cycle_config& cfg) {
 void fused_body(stmg_ctx* c, const stmg_cycle_config& cfg, i64* np) {
   Level& L = c->levels[0];
   Level& C = c->levels[1];
+  prof_begin(c, 4);
   coarse_cycle(c, cfg);
+  prof_end(c, 4, 0.0);
   stmg::ModalArgs a = modal_args(L, &C, cfg.omega_t, true);
   prof_begin(c, 0);
   CK(stmg::launch_updown(L.view, a, C.U[c->cur[1]].base, c->d_pp, c->d_par, L.F.base, C.F.base,
@@ -2113,7 +2115,7 @@ int stmg_profile_read(stmg_ctx* c, int id, double* total_ms, int64_t* launches,
                       double* bytes_per_launch) {
   return guard([&] {
     require(c != nullptr, "null context");
-    require(id >= 0 && id < 4, "kernel id out of range");
+    require(id >= 0 && id < 5, "kernel id out of range");
     CK(cudaStreamSynchronize(c->stream));
     prof_collect(c);
     if (total_ms) *total_ms = c->prof[id].total_ms;

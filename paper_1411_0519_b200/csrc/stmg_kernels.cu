@@ -345,7 +345,10 @@ __device__ __forceinline__ void ld_st(const double* p, i64 nx, double (&v)[NL]) 
 // the residual r_n = f_n - A_j u'_n + M_j N u'_{n-1}, and the restriction
 // c_{n/2} += fac * R_{1|2} r_n summed over the alias group (transfer.cpp:75-85,
 // 138-149 in the sine basis).  has_prev: step n0-1 exists (warm-up).
-template <int DIM, int NL, bool ZERO, int CO, bool COH, bool ASYNC = false>
+// WAIT: the body issues the PDL wait itself, after the per-mode setup (sine
+// tables, block factors), which only reads constants and so overlaps the
+// previous kernel's tail; every read of data a previous kernel wrote follows.
+template <int DIM, int NL, bool ZERO, int CO, bool COH, bool ASYNC = false, bool WAIT = false>
 __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64 nend,
                                           const double* f, const double* uin, double* uout,
                                           double* fc, const TM<NL>& t, const SP& s,
@@ -357,6 +360,7 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
   const double om1 = 1.0 - omega;
   const double Mj = me.Mj, Kj = me.Kj;
   const ModeLU<NL> lu(t, Mj, Kj);
+  if (WAIT) pdl_wait();
   const double* fp = f + me.idx;
   const double* up = uin + me.idx;
   double* op = uout + me.idx;
@@ -365,31 +369,7 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
 #pragma unroll
   for (int l = 0; l < NL; ++l) uo[l] = un[l] = 0.0;
 
-  if (me.ok && has_prev) {  // warm-up: smoothed step n0-1
-    double fv[NL], x[NL];
-    ld_ro<COH, NL>(fp + (n0 - 1) * slab, nx, fv);
-    if (ZERO) {
-      lu.solve(fv, x);
-#pragma unroll
-      for (int l = 0; l < NL; ++l) un[l] = omega * x[l];
-    } else {
-      double u1[NL], u2[NL], nv[NL];
-      ld_ro<COH, NL>(up + (n0 - 1) * slab, nx, u1);
-#pragma unroll
-      for (int l = 0; l < NL; ++l) u2[l] = 0.0;
-      if (has_prev2) ld_ro<COH, NL>(up + (n0 - 2) * slab, nx, u2);
-      matvec<NL>(t.N, u2, nv);
-#pragma unroll
-      for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
-      lu.solve(fv, x);
-#pragma unroll
-      for (int l = 0; l < NL; ++l) {
-        un[l] = om1 * u1[l] + omega * x[l];
-        uo[l] = u1[l];
-      }
-    }
-  }
-
+  // (issued before the warm-up, whose loads and solve overlap their latency)
   // ASYNC: the loads of the next kRing-1 step pairs sit in a per-thread
   // cp.async ring in shared memory (no registers held); otherwise a register
   // prefetch of the next pair (memory-level parallelism; latency bound).
@@ -423,6 +403,31 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
       if (!ZERO) ld_st<COH, NL>(up + (n0 + e) * slab, nx, u2[e]);
     }
   }
+  if (me.ok && has_prev) {  // warm-up: smoothed step n0-1
+    double fv[NL], x[NL];
+    ld_ro<COH, NL>(fp + (n0 - 1) * slab, nx, fv);
+    if (ZERO) {
+      lu.solve(fv, x);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) un[l] = omega * x[l];
+    } else {
+      double u1[NL], u2[NL], nv[NL];
+      ld_ro<COH, NL>(up + (n0 - 1) * slab, nx, u1);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) u2[l] = 0.0;
+      if (has_prev2) ld_ro<COH, NL>(up + (n0 - 2) * slab, nx, u2);
+      matvec<NL>(t.N, u2, nv);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
+      lu.solve(fv, x);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        un[l] = om1 * u1[l] + omega * x[l];
+        uo[l] = u1[l];
+      }
+    }
+  }
+
   int pair = 0;
   for (i64 n = n0; n < nend; n += 2, ++pair) {
     double acc[NL];
@@ -506,7 +511,7 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
 // up: u <- u + P e_c (mg.cpp:123-127), then one damped block-Jacobi sweep
 // (mg.cpp:129-131); with RESID also the residual of the result, returning its
 // sum of squares (stop test, mg.cpp:152-153).
-template <int DIM, int NL, int CO, bool RESID, bool COH, bool ASYNC = false>
+template <int DIM, int NL, int CO, bool RESID, bool COH, bool ASYNC = false, bool WAIT = false>
 __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64 nend,
                                           const double* ec, const double* uin, const double* f,
                                           double* uout, const TM<NL>& t, const SP& s,
@@ -518,6 +523,7 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
   const double om1 = 1.0 - omega;
   const double Mj = me.Mj, Kj = me.Kj;
   const ModeLU<NL> lu(t, Mj, Kj);
+  if (WAIT) pdl_wait();
   const double fac = (CO == 2) ? me.fac : 1.0;
   const bool has_c = (CO == 2) ? me.cok : me.ok;
   const double* ep = ec + ((CO == 2) ? me.cidx : me.idx);
@@ -531,35 +537,8 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
 #pragma unroll
   for (int l = 0; l < NL; ++l) vo[l] = wp[l] = ev[l] = 0.0;
 
-  if (has_prev) {
-    if (has_c) ld_ro<COH, NL>(ep + ((n0 >> 1) - 1) * cslab, nxc, ev);  // coarse step of n0-2, n0-1
-    double u1[NL], c1[NL];
-    ld_ro<COH, NL>(up + (n0 - 1) * slab, nx, u1);
-    matvec_t<NL>(t.R2, ev, c1);
-#pragma unroll
-    for (int l = 0; l < NL; ++l) vo[l] = u1[l] + fac * c1[l];
-    if (RESID) {
-      double v2[NL], fv[NL], nv[NL], x[NL];
-#pragma unroll
-      for (int l = 0; l < NL; ++l) v2[l] = 0.0;
-      if (has_prev2) {
-        double u2[NL], c2[NL];
-        ld_ro<COH, NL>(up + (n0 - 2) * slab, nx, u2);
-        matvec_t<NL>(t.R1, ev, c2);
-#pragma unroll
-        for (int l = 0; l < NL; ++l) v2[l] = u2[l] + fac * c2[l];
-      }
-      ld_ro<COH, NL>(fp + (n0 - 1) * slab, nx, fv);
-      matvec<NL>(t.N, v2, nv);
-#pragma unroll
-      for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
-      lu.solve(fv, x);
-#pragma unroll
-      for (int l = 0; l < NL; ++l) wp[l] = om1 * vo[l] + omega * x[l];
-    }
-  }
-
-  // software pipeline (see down_body); the register prefetch is off for
+  // software pipeline (see down_body; issued before the warm-up); the
+  // register prefetch is off for
   // NL > 2, where the extra registers cost more occupancy than it gains
   constexpr bool PF = !ASYNC && NL <= 2;
   constexpr int Q = 5 * NL;  // u, f of two steps + e of the coarse step
@@ -594,6 +573,34 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
     }
     if (has_c) ld_ro<COH, NL>(ep + (n0 >> 1) * cslab, nxc, en);
   }
+  if (has_prev) {
+    if (has_c) ld_ro<COH, NL>(ep + ((n0 >> 1) - 1) * cslab, nxc, ev);  // coarse step of n0-2, n0-1
+    double u1[NL], c1[NL];
+    ld_ro<COH, NL>(up + (n0 - 1) * slab, nx, u1);
+    matvec_t<NL>(t.R2, ev, c1);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) vo[l] = u1[l] + fac * c1[l];
+    if (RESID) {
+      double v2[NL], fv[NL], nv[NL], x[NL];
+#pragma unroll
+      for (int l = 0; l < NL; ++l) v2[l] = 0.0;
+      if (has_prev2) {
+        double uu2[NL], c2[NL];
+        ld_ro<COH, NL>(up + (n0 - 2) * slab, nx, uu2);
+        matvec_t<NL>(t.R1, ev, c2);
+#pragma unroll
+        for (int l = 0; l < NL; ++l) v2[l] = uu2[l] + fac * c2[l];
+      }
+      ld_ro<COH, NL>(fp + (n0 - 1) * slab, nx, fv);
+      matvec<NL>(t.N, v2, nv);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
+      lu.solve(fv, x);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) wp[l] = om1 * vo[l] + omega * x[l];
+    }
+  }
+
   int pair = 0;
   for (i64 n = n0; n < nend; n += 2, ++pair) {
 #pragma unroll
@@ -674,6 +681,14 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
   return sumsq;
 }
 
+// Ping-pong level-0 buffers selected on the device (the solve graph is
+// replayed unchanged while the buffers alternate): A = tbl[*par] holds the
+// pre-smoothed iterate of cycle k, B = tbl[1 - *par] receives cycle k+1's.
+struct PingPong {
+  double* const* tbl;
+  const int* par;
+};
+
 // updown: the post-smooth of cycle k (prolongation + correction + damped
 // Jacobi, mg.cpp:123-131) fused with the pre-smooth, residual and restriction
 // of cycle k+1 (mg.cpp:106-117) in ONE pass over a level, plus the residual
@@ -687,8 +702,8 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
 // A three-step warm-up rebuilds v, w, x of step n0-1.  Non-sharded only.
 template <int DIM, int NL, int CO>
 __device__ __forceinline__ double updown_body(const i64 tid, const i64 n0, const i64 nend,
-                                              const double* ec, const double* uin,
-                                              const double* f, double* uout, double* fc,
+                                              const double* ec, const PingPong pp,
+                                              const double* f, double* fc,
                                               const TM<NL>& t, const SP& s, const i64 n1c,
                                               const double omega, double* ring, const i64 s0) {
   const Member me = make_member<DIM>(s, tid, n1c, CO == 2);
@@ -701,8 +716,10 @@ __device__ __forceinline__ double updown_body(const i64 tid, const i64 n0, const
   const bool has_c = (CO == 2) ? me.cok : me.ok;
   const double* ep = ec + ((CO == 2) ? me.cidx : me.idx);
   const double* fp = f + me.idx;
-  const double* up = uin + me.idx;
-  double* op = uout + me.idx;
+  pdl_wait();  // after the constant-only setup above (see down_body)
+  const int par = *pp.par;
+  const double* up = pp.tbl[par] + me.idx;
+  double* op = pp.tbl[1 - par] + me.idx;
   double sumsq = 0.0;
 
   // corrected iterate v of step m (m >= 0)
@@ -732,6 +749,27 @@ __device__ __forceinline__ double updown_body(const i64 tid, const i64 n0, const
   double vp[NL], wp[NL], xp[NL];
 #pragma unroll
   for (int l = 0; l < NL; ++l) vp[l] = wp[l] = xp[l] = 0.0;
+  // ring prologue first: the warm-up below overlaps its latency
+  constexpr int Q = 5 * NL;  // u, f of two steps + e of the coarse step
+  const int T = blockDim.x;
+  auto issue = [&](i64 n, int st) {
+    double* r = ring + i64(st) * Q * T + threadIdx.x;
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        cp_async8(r + (e * NL + l) * T, up + (n + e) * slab + l * nx, me.ok);
+        cp_async8(r + ((2 + e) * NL + l) * T, fp + (n + e) * slab + l * nx, me.ok);
+      }
+#pragma unroll
+    for (int l = 0; l < NL; ++l)
+      cp_async8(r + (4 * NL + l) * T, has_c ? ep + (n >> 1) * cslab + l * nxc : fp, has_c);
+  };
+#pragma unroll
+  for (int q = 0; q < kRing - 1; ++q) {
+    if (n0 + 2 * q < nend) issue(n0 + 2 * q, q);
+    cp_async_commit();
+  }
   // s0: global index of local step 0 (sharded: steps -1..-3 are halo slabs)
   if (me.ok && s0 + n0 > 0) {  // warm-up: steps n0-3 .. n0-1
     double v3[NL], v2[NL], w2[NL], f2v[NL];
@@ -754,26 +792,6 @@ __device__ __forceinline__ double updown_body(const i64 tid, const i64 n0, const
     }
   }
 
-  constexpr int Q = 5 * NL;  // u, f of two steps + e of the coarse step
-  const int T = blockDim.x;
-  auto issue = [&](i64 n, int st) {
-    double* r = ring + i64(st) * Q * T + threadIdx.x;
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-#pragma unroll
-      for (int l = 0; l < NL; ++l) {
-        cp_async8(r + (e * NL + l) * T, up + (n + e) * slab + l * nx, me.ok);
-        cp_async8(r + ((2 + e) * NL + l) * T, fp + (n + e) * slab + l * nx, me.ok);
-      }
-#pragma unroll
-    for (int l = 0; l < NL; ++l)
-      cp_async8(r + (4 * NL + l) * T, has_c ? ep + (n >> 1) * cslab + l * nxc : fp, has_c);
-  };
-#pragma unroll
-  for (int q = 0; q < kRing - 1; ++q) {
-    if (n0 + 2 * q < nend) issue(n0 + 2 * q, q);
-    cp_async_commit();
-  }
   int pair = 0;
   for (i64 n = n0; n < nend; n += 2, ++pair) {
     double u2[2][NL], f2[2][NL], ev[NL];
@@ -841,14 +859,6 @@ __device__ __forceinline__ double updown_body(const i64 tid, const i64 n0, const
   return sumsq;
 }
 
-// Ping-pong level-0 buffers selected on the device (the solve graph is
-// replayed unchanged while the buffers alternate): A = tbl[*par] holds the
-// pre-smoothed iterate of cycle k, B = tbl[1 - *par] receives cycle k+1's.
-struct PingPong {
-  double* const* tbl;
-  const int* par;
-};
-
 template <int DIM, int NL, int CO>
 __global__ void __launch_bounds__(128) k_updown(const double* __restrict__ ec, const PingPong pp,
                                                 const double* __restrict__ f,
@@ -857,18 +867,14 @@ __global__ void __launch_bounds__(128) k_updown(const double* __restrict__ ec, c
                                                 const SP s, const i64 n_t, const int C,
                                                 const i64 n1c, const double omega,
                                                 const i64 s0) {
-  pdl_wait();
   __shared__ double sh[32];
   extern __shared__ double ring[];
-  const int p = *pp.par;
-  const double* uin = pp.tbl[p];
-  double* uout = pp.tbl[1 - p];
   const unsigned bx = blockIdx.x, by = blockIdx.y;
   const i64 tid = i64(bx) * blockDim.x + threadIdx.x;
   const i64 n0 = i64(by) * C;
   const i64 nend = min(n0 + i64(C), n_t);
   const double sumsq =
-      updown_body<DIM, NL, CO>(tid, n0, nend, ec, uin, f, uout, fc, t, s, n1c, omega, ring, s0);
+      updown_body<DIM, NL, CO>(tid, n0, nend, ec, pp, f, fc, t, s, n1c, omega, ring, s0);
   pdl_trigger();
   const double tot = block_sum(sumsq, sh);
   if (threadIdx.x == 0) partials[i64(by) * gridDim.x + bx] = tot;
@@ -908,12 +914,11 @@ __global__ void __launch_bounds__(256) k_down(const double* __restrict__ f,
                                               const SP s, const i64 n_t, const int C,
                                               const i64 n1c, const double omega,
                                               const bool first_global) {
-  pdl_wait();
   const i64 tid = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   const i64 n0 = i64(blockIdx.y) * C;
   const i64 nend = min(n0 + i64(C), n_t);
   extern __shared__ double ring[];
-  down_body<DIM, NL, ZERO, CO, false, bool(STMG_DOWN_ASYNC)>(tid, n0, nend, f, uin, uout, fc, t, s, n1c, omega,
+  down_body<DIM, NL, ZERO, CO, false, bool(STMG_DOWN_ASYNC), true>(tid, n0, nend, f, uin, uout, fc, t, s, n1c, omega,
                                             n0 > 0 || !first_global, n0 - 1 > 0 || !first_global,
                                             ring);
   pdl_trigger();
@@ -928,14 +933,13 @@ __global__ void __launch_bounds__(256) k_up(const double* __restrict__ ec,
                                             const SP s, const i64 n_t, const int C,
                                             const i64 n1c, const double omega,
                                             const bool first_global) {
-  pdl_wait();
   __shared__ double sh[32];
   const unsigned bx = blockIdx.x, by = blockIdx.y;
   const i64 tid = i64(bx) * blockDim.x + threadIdx.x;
   const i64 n0 = i64(by) * C;
   const i64 nend = min(n0 + i64(C), n_t);
   extern __shared__ double ring[];
-  const double sumsq = up_body<DIM, NL, CO, RESID, false, bool(STMG_UP_ASYNC)>(
+  const double sumsq = up_body<DIM, NL, CO, RESID, false, bool(STMG_UP_ASYNC), true>(
       tid, n0, nend, ec, uin, f, uout, t, s, n1c, omega, n0 > 0 || !first_global,
       n0 - 1 > 0 || !first_global, ring);
   pdl_trigger();
@@ -980,7 +984,6 @@ template <int DIM, int NL>
 __global__ void __launch_bounds__(kTailThreads) k_tail(const TailLevel<NL>* __restrict__ lv,
                                                const int nlev, const double omega,
                                                const __grid_constant__ TailParams<NL> P) {
-  pdl_wait();
   extern __shared__ double smem[];
   __shared__ TailLevel<NL> lvs[kTailMaxLevels];
   __shared__ i64 off[kTailMaxLevels + 1];
@@ -1020,6 +1023,7 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(const TailLevel<NL>* __re
     }
   }
   const int sz0 = int(lv[0].n_t * NL * lv[0].s.nx);
+  pdl_wait();  // the tables above are constants; the rhs is the previous kernel's output
   {  // stage the first level's rhs
     const double* g = lv[0].F;
     for (int i = threadIdx.x; i < sz0; i += T) smem[i] = g[i];
@@ -1670,8 +1674,21 @@ __device__ __forceinline__ void stockham_pass(double2* __restrict__ X, const int
     for (int r = 0; r < R; ++r) v[i][r] = X[dst_pad(j + r * NJ)];
     if (NS > 1) {
       const int step = (j % NS) * TSTEP;  // NS, TSTEP: powers of two, compile time
+      // w^r from the table entries w, w^2, w^4, w^8 (<= 3 products each):
+      // 4 cached loads per butterfly instead of R - 1 (the L1 pipe, not
+      // the FP64 pipe, is this kernel's limiter)
+      double2 w[R];
+      w[1] = __ldg(tw + 2 * step);
+      if (R > 2) w[2] = __ldg(tw + 4 * step);
+      if (R > 4) w[4] = __ldg(tw + 8 * step);
+      if (R > 8) w[8] = __ldg(tw + 16 * step);
 #pragma unroll
-      for (int r = 1; r < R; ++r) v[i][r] = cmul(v[i][r], __ldg(tw + 2 * r * step));
+      for (int r = 3; r < R; ++r) {
+        const int hi = (r >= 8) ? 8 : (r >= 4) ? 4 : 2;
+        if (r != hi) w[r] = cmul(w[hi], w[r - hi]);
+      }
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[i][r] = cmul(v[i][r], w[r]);
     }
     RegFFT<R>::run(v[i]);
   }
@@ -2240,12 +2257,15 @@ int64_t partial_count(const LevelView& L, int chunk, bool grouped) {
   return i64(grid1(units, 128)) * ((L.n_t + chunk - 1) / chunk);
 }
 
+#ifndef STMG_CHUNK_TARGET
+#define STMG_CHUNK_TARGET (148 * 512)
+#endif
 int pick_chunk(const LevelView& L, bool grouped) {
   const i64 G = (L.sp.n1 + 1) / 2;
   const i64 units = grouped ? (ipow(G, L.sp.dim) << L.sp.dim) : L.sp.nx;
   // aim for ~1K resident threads per SM; chunks are even and divide the
   // (power-of-two) n_t; longer chunks amortise the one-step warm-up
-  const i64 target = 148 * 1024;
+  const i64 target = STMG_CHUNK_TARGET;
   i64 c = 2;
   while (c < 64 && c * 2 <= L.n_t && units * (L.n_t / (c * 2)) >= target) c *= 2;
   if (c > L.n_t) c = L.n_t;

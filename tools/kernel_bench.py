@@ -1,7 +1,8 @@
 """Per-kernel HBM throughput on the BASELINE configs (run on the GPU box).
 
-For each config: the fused level-0 V-cycle kernels (k_down / k_up, timed
-live with CUDA events inside the cycle graph), one full sine-basis transform
+For each config: the fused level-0 V-cycle kernel (k_updown; k_down / k_up
+for the per-level schedule) and the coarse part of each cycle (levels >= 1),
+timed live with CUDA events inside the cycle graph, one full sine-basis transform
 (dim DST-I passes), the physical Q1 residual kernel (stmg_residual) and the
 physical block-Jacobi sweep (stmg_smooth, nu = 1).  Achieved GB/s use
 ALGORITHMIC bytes.  Prints one JSON line per config.
@@ -33,12 +34,14 @@ def run(name, reps=5):
     out = {"config": name, "dofs": n0, "iterations": rep.iterations,
            "solve_ms": rep.device_time_seconds * 1e3}
     fused = h.profile_read(1)[1] == 0
-    names = ({0: "k_updown_l0", 2: "transform"} if fused else
+    names = ({0: "k_updown_l0", 2: "transform", 4: "coarse_part"} if fused else
              {0: "k_down_l0", 1: "k_up_l0", 2: "transform"})
     for k, nm in names.items():
         ms, n, b = h.profile_read(k)
         if n:
-            out[nm] = {"avg_ms": ms / n, "alg_GBps": b / (ms / n * 1e-3) / 1e9, "launches": n}
+            out[nm] = {"avg_ms": ms / n, "launches": n}
+            if b:
+                out[nm]["alg_GBps"] = b / (ms / n * 1e-3) / 1e9
     # physical residual (24 B/dof: read u, f; write r)
     r = h.vector(0)
     h.profile_reset()
