@@ -2103,9 +2103,12 @@ int stmg_local_steps(const stmg_ctx* c, int64_t* first_step, int64_t* n_steps) {
 int stmg_profile_enable(stmg_ctx* c, int on) {
   return guard([&] {
     require(c != nullptr, "null context");
-    if (bool(on) != c->profile) {
+    if (bool(on) != c->profile) {  // re-capture with / without event nodes
+      CK(cudaStreamSynchronize(c->stream));
       for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
-      c->graphs.clear();  // re-capture with / without event nodes
+      c->graphs.clear();
+      for (auto& kv : c->fused_bodies) cudaGraphExecDestroy(kv.second);
+      c->fused_bodies.clear();
     }
     c->profile = on != 0;
   });
