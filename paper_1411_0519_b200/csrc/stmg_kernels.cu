@@ -1247,6 +1247,9 @@ struct ResTile {
   static constexpr int TX = DIM == 1 ? 256 : 32;
   static constexpr int TY = DIM == 1 ? 1 : (DIM == 2 ? 8 : 4);
   static constexpr int TZ = DIM == 3 ? 2 : 1;
+  // cp.async ring depth: 3 in 1D/2D; 2 in 3D, where the larger halo makes a
+  // third stage cost more occupancy than the extra step in flight gains
+  static constexpr int STAGES = DIM == 3 ? 2 : 3;
   static constexpr int HX = TX + 2;
   static constexpr int HY = DIM >= 2 ? TY + 2 : 1;
   static constexpr int HZ = DIM == 3 ? TZ + 2 : 1;
@@ -1372,41 +1375,56 @@ __global__ void __launch_bounds__(ResTile<DIM>::THREADS) k_apply(
     b[k] = ab[kMaxNL + k];
   }
 
-  // warm-up: M-stencil trace of step n0-1
-  double mw_prev = 0.0;
-  const bool has_prev = n0 > 0 || !first_global;
+  // cp.async ring: stage m holds slab m of u (tile + halo) and, for the
+  // residual, this tile's f of step m; STAGES - 1 steps are in flight while
+  // one is computed (the kernel is latency bound with a single slab ahead)
+  constexpr int NS = T::STAGES;
+  constexpr int FS = RES ? NL * T::THREADS : 0;
+  constexpr int SS = BS + FS;  // doubles per stage
+  auto stage = [&](int m) { return dsm + ((m + NS) % NS) * SS; };
   StagePlan<DIM, NL> plan;
   make_plan<DIM, NL>(plan, n1, nx, x0, y0, z0);
-  if (has_prev) stage_slab<DIM, NL>(dsm, u, n0 - 1, nx, plan);
+  auto issue = [&](i64 n) {  // slab n -> stage (n - n0 + 1) mod NS
+    double* st = stage(int(n - n0 + 1));
+    stage_slab<DIM, NL>(st, u, n, nx, plan);
+    if (RES) {
+#pragma unroll
+      for (int k = 0; k < NL; ++k)
+        cp_async8(st + BS + k * T::THREADS + threadIdx.x,
+                  inside ? f + n * slab + k * nx + r : f, inside);
+    }
+  };
+  double mw_prev = 0.0;  // M-stencil trace of step n-1 (rank-one jump)
+  const bool has_prev = n0 > 0 || !first_global;
+  if (has_prev) issue(n0 - 1);
   cp_async_commit();
-  stage_slab<DIM, NL>(dsm + BS, u, n0, nx, plan);
-  cp_async_commit();
-  cp_async_wait<1>();
+#pragma unroll
+  for (int q = 0; q < NS - 1; ++q) {
+    if (n0 + q < nend) issue(n0 + q);
+    cp_async_commit();
+  }
+  cp_async_wait<NS - 1>();
   __syncthreads();
   if (has_prev && inside) {
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
       double Mv, Kv;
-      stencil_smem<DIM>(dsm + l * T::HALO, tx, ty, tz, h, Mv, Kv);
+      stencil_smem<DIM>(stage(0) + l * T::HALO, tx, ty, tz, h, Mv, Kv);
       mw_prev += b[l] * Mv;
     }
   }
   for (i64 n = n0; n < nend; ++n) {
-    const int cur = int((n - n0 + 1) & 1);
-    cp_async_wait<0>();
-    __syncthreads();  // slab n visible; slab n-1's buffer free
-    if (n + 1 < nend) stage_slab<DIM, NL>(dsm + (cur ^ 1) * BS, u, n + 1, nx, plan);
+    const int j = int(n - n0 + 1);
+    cp_async_wait<NS - 2>();  // groups up to step n landed
+    __syncthreads();          // slab n visible; stage of n - 1 free
+    if (n + NS - 1 < nend) issue(n + NS - 1);
     cp_async_commit();
     if (inside) {
-      double fv[NL];
-      if (RES) {
-#pragma unroll
-        for (int k = 0; k < NL; ++k) fv[k] = __ldcs(f + n * slab + k * nx + r);
-      }
+      const double* st = stage(j);
       double MU[NL], KU[NL], mw = 0.0;
 #pragma unroll
       for (int l = 0; l < NL; ++l) {
-        stencil_smem<DIM>(dsm + cur * BS + l * T::HALO, tx, ty, tz, h, MU[l], KU[l]);
+        stencil_smem<DIM>(st + l * T::HALO, tx, ty, tz, h, MU[l], KU[l]);
         mw += b[l] * MU[l];
       }
 #pragma unroll
@@ -1416,7 +1434,7 @@ __global__ void __launch_bounds__(ResTile<DIM>::THREADS) k_apply(
         for (int l = 0; l < NL; ++l) acc += MU[l] * t.K[k][l] + KU[l] * t.M[k][l];
         acc -= a[k] * mw_prev;
         const i64 o = n * slab + k * nx + r;
-        __stcs(y + o, RES ? fv[k] - acc : acc);
+        __stcs(y + o, RES ? st[BS + k * T::THREADS + threadIdx.x] - acc : acc);
       }
       mw_prev = mw;
     }
@@ -2017,19 +2035,22 @@ cudaError_t launch_apply(const LevelView& L, const double* u, const double* f, d
     const i64 n1 = L.sp.n1;
     const i64 tiles = ((n1 + T::TX - 1) / T::TX) * (DIM >= 2 ? (n1 + T::TY - 1) / T::TY : 1) *
                       (DIM == 3 ? (n1 + T::TZ - 1) / T::TZ : 1);
-    // chunk: enough CTAs for ~8 per SM, at least 4 steps to amortise the warm-up
+    // chunk: enough CTAs for ~4 per SM, at least 4 steps to amortise the warm-up
     i64 C = 64;
-    while (C > 4 && tiles * ((L.n_t + C - 1) / C) < 148 * 8) C /= 2;
+    while (C > 4 && tiles * ((L.n_t + C - 1) / C) < 148 * 4) C /= 2;
     C = std::min<i64>(C, L.n_t);
     const dim3 g(unsigned(tiles), unsigned((L.n_t + C - 1) / C));
     const TM<NL> t = make_tm<NL>(L.tc);
-    const size_t smem = 2 * size_t(NL) * T::HALO * sizeof(double);
+    const size_t smem = size_t(T::STAGES) *
+                        (size_t(NL) * T::HALO + (residual ? size_t(NL) * T::THREADS : 0)) *
+                        sizeof(double);
     static bool attr = false;
     if (!attr) {
+      const int most = int(T::STAGES * 2 * size_t(NL) * T::HALO * sizeof(double));  // >= smem
       cudaFuncSetAttribute(k_apply<DIM, NL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(smem));
+                           most);
       cudaFuncSetAttribute(k_apply<DIM, NL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(smem));
+                           most);
       attr = true;
     }
     if (residual)
