@@ -196,6 +196,66 @@ int stmg_profile_reset(stmg_ctx* ctx);
 /* Kernel launches issued by the library since creation (all kinds). */
 int stmg_launch_count(const stmg_ctx* ctx, int64_t* out);
 
+/* ---- local Fourier analysis (lfa.hpp:15-150; host only, no GPU) ----------
+ * Nondimensionalised like the reference: h = 1, tau = mu; mode is
+ * STMG_COARSEN_SEMI or STMG_COARSEN_FULL; cfg supplies nu1, nu2, omega_t. */
+/* beta(theta_x) = 6 (1 - cos)/(2 + cos) (lfa.hpp:15-17). */
+int stmg_lfa_beta(double theta_x, double* out);
+/* alpha = R(-mu beta(theta_x)) (lfa.hpp:19-20). */
+int stmg_lfa_alpha(int p_t, double mu, double theta_x, double* out);
+/* Spectral radius of the damped block-Jacobi symbol, by eigenvalues and by
+ * the closed form (SymbolBuilder::smoother_symbol / smoother_rho_closed_form,
+ * lfa.hpp:75-85). */
+int stmg_lfa_smoother_rho(int p_t, double mu, double omega_t, double theta_x,
+                          double theta_t, double* rho, double* rho_closed_form);
+/* (p_t+1)^2 smoother symbol, row-major real / imaginary parts (lfa.hpp:75-77). */
+int stmg_lfa_smoother_symbol(int p_t, double mu, double omega_t, double theta_x,
+                             double theta_t, double* re, double* im);
+/* (4(p_t+1))^2 two-grid symbol on the four harmonics (lfa.hpp:93-99);
+ * STMG_EINVAL for theta_x = 0 (the reference's std::domain_error). */
+int stmg_lfa_twogrid_symbol(int p_t, double mu, const stmg_cycle_config* cfg, int mode,
+                            double theta_x, double theta_t, double* re, double* im);
+/* Spectral radius of an n x n complex matrix (lfa.hpp:50); im may be NULL. */
+int stmg_lfa_spectral_radius(int n, const double* re, const double* im, double* out);
+/* smoothing_factor (lfa.hpp:125-132): sup over the closed high-frequency
+ * region, grid n_theta_x x n_theta_t (each at least 64). */
+int stmg_lfa_smoothing_factor(int p_t, double mu, double omega_t, int mode,
+                              int n_theta_x, int n_theta_t, double* out);
+/* twogrid_factor (lfa.hpp:137-141): max over the sampled low quarter. */
+int stmg_lfa_twogrid_factor(int p_t, double mu, const stmg_cycle_config* cfg, int mode,
+                            int n_theta_x, int n_theta_t, double* out);
+/* twogrid_factor_inexact (lfa.hpp:142-145): block solves replaced by one
+ * spatial two-grid iteration (damped Jacobi omega_x, nu1_x / nu2_x sweeps). */
+int stmg_lfa_twogrid_factor_inexact(int p_t, double mu, const stmg_cycle_config* cfg,
+                                    double omega_x, int nu1_x, int nu2_x, int mode,
+                                    int n_theta_x, int n_theta_t, double* out);
+
+/* ---- two-grid factor measurement on the GPU (bench.hpp:12-39) ------------ */
+typedef struct {
+  int p_t;
+  int dim;
+  int space_level;
+  int time_level;
+  double mu;      /* tau = mu h^2 */
+  int mode;       /* STMG_COARSEN_SEMI / STMG_COARSEN_FULL */
+  int device;
+} stmg_rho_problem;
+
+typedef struct {
+  double measured_rho;   /* largest ||r_k+1|| / ||r_k|| above the 1e-13 guard */
+  double predicted_rho;  /* stmg_lfa_twogrid_factor of the same problem */
+  int n_iterations_used;
+  uint64_t seed_used;
+} stmg_rho_measurement;
+
+/* measure_convergence_factor (bench.cpp:77-145): f = 0, seeded random initial
+ * guess (this library's uniform generator, stream 1), two-grid cycles with
+ * exact block solves until ||r|| <= 1e-13 ||r_0|| or 250 cycles. */
+int stmg_measure_convergence_factor(const stmg_rho_problem* problem,
+                                    const stmg_cycle_config* cfg, uint64_t seed,
+                                    int n_theta_x, int n_theta_t,
+                                    stmg_rho_measurement* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -44,6 +44,16 @@ class LevelInfo(C.Structure):
                 ("coarsen_to_next", C.c_int), ("tau", D), ("h", D), ("mu", D)]
 
 
+class RhoProblem(C.Structure):
+    _fields_ = [("p_t", C.c_int), ("dim", C.c_int), ("space_level", C.c_int),
+                ("time_level", C.c_int), ("mu", D), ("mode", C.c_int), ("device", C.c_int)]
+
+
+class RhoMeasurement(C.Structure):
+    _fields_ = [("measured_rho", D), ("predicted_rho", D), ("n_iterations_used", C.c_int),
+                ("seed_used", C.c_uint64)]
+
+
 # (name, restype, argtypes) for every symbol declared in include/stmg_b200.h
 SIGNATURES = [
     ("stmg_last_error", C.c_char_p, []),
@@ -88,6 +98,21 @@ SIGNATURES = [
     ("stmg_profile_read", C.c_int, [VP, C.c_int, PD, C.POINTER(C.c_int64), PD]),
     ("stmg_profile_reset", C.c_int, [VP]),
     ("stmg_launch_count", C.c_int, [VP, C.POINTER(C.c_int64)]),
+    ("stmg_lfa_beta", C.c_int, [D, PD]),
+    ("stmg_lfa_alpha", C.c_int, [C.c_int, D, D, PD]),
+    ("stmg_lfa_smoother_rho", C.c_int, [C.c_int, D, D, D, D, PD, PD]),
+    ("stmg_lfa_smoother_symbol", C.c_int, [C.c_int, D, D, D, D, PD, PD]),
+    ("stmg_lfa_twogrid_symbol", C.c_int, [C.c_int, D, C.POINTER(CycleConfig), C.c_int, D, D,
+                                          PD, PD]),
+    ("stmg_lfa_spectral_radius", C.c_int, [C.c_int, PD, PD, PD]),
+    ("stmg_lfa_smoothing_factor", C.c_int, [C.c_int, D, D, C.c_int, C.c_int, C.c_int, PD]),
+    ("stmg_lfa_twogrid_factor", C.c_int, [C.c_int, D, C.POINTER(CycleConfig), C.c_int, C.c_int,
+                                          C.c_int, PD]),
+    ("stmg_lfa_twogrid_factor_inexact", C.c_int, [C.c_int, D, C.POINTER(CycleConfig), D, C.c_int,
+                                                  C.c_int, C.c_int, C.c_int, C.c_int, PD]),
+    ("stmg_measure_convergence_factor", C.c_int, [C.POINTER(RhoProblem), C.POINTER(CycleConfig),
+                                                  C.c_uint64, C.c_int, C.c_int,
+                                                  C.POINTER(RhoMeasurement)]),
 ]
 
 _lib = None

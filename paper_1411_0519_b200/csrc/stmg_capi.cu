@@ -29,6 +29,7 @@
 
 #include "../../include/stmg_b200.h"
 #include "stmg_launch.hpp"
+#include "stmg_lfa.hpp"
 #include "stmg_setup.hpp"
 
 namespace {
@@ -55,6 +56,9 @@ int guard(F&& fn) {
   } catch (const std::invalid_argument& e) {
     g_err = e.what();
     return STMG_EINVAL;
+  } catch (const std::domain_error& e) {  // lfa: theta_x = 0 (lfa.cpp:207-211)
+    g_err = e.what();
+    return STMG_EINVAL;
   } catch (const std::exception& e) {
     g_err = e.what();
     return STMG_ERUNTIME;
@@ -64,6 +68,14 @@ int guard(F&& fn) {
 void require(bool ok, const char* msg) {
   if (!ok) throw std::invalid_argument(msg);
 }
+
+// Calls of this library's own C ABI from inside another entry point.
+#define CK_ABI(call)                                                   \
+  do {                                                                 \
+    const int st_ = (call);                                            \
+    if (st_ == STMG_EINVAL) throw std::invalid_argument(g_err);        \
+    if (st_ != STMG_OK) throw std::runtime_error(g_err);               \
+  } while (0)
 
 // Device buffer with `halo` leading slabs (multi-GPU halo exchange lands there).
 struct DevBuf {
@@ -2145,6 +2157,180 @@ int stmg_launch_count(const stmg_ctx* c, int64_t* out) {
     require(c && out, "null argument");
     *out = c->launches;
   });
+}
+
+// ---------------------------------------------------------------- LFA (host)
+namespace {
+void check_lfa(int p_t, double mu) {
+  require(p_t >= 0 && p_t <= stmg::kMaxTimeDegree, "p_t out of range");
+  require(mu > 0.0, "mu must be positive");
+}
+void check_mode(int mode) {
+  require(mode == STMG_COARSEN_SEMI || mode == STMG_COARSEN_FULL,
+          "LFA needs semi or full coarsening");
+}
+}  // namespace
+
+int stmg_lfa_beta(double theta_x, double* out) {
+  return guard([&] {
+    require(out != nullptr, "null argument");
+    *out = stmg::lfa::beta(theta_x);
+  });
+}
+
+int stmg_lfa_alpha(int p_t, double mu, double theta_x, double* out) {
+  return guard([&] {
+    require(out != nullptr, "null argument");
+    require(p_t >= 0 && p_t <= stmg::kMaxTimeDegree, "p_t out of range");
+    *out = stmg::lfa::alpha(p_t, mu, theta_x);
+  });
+}
+
+int stmg_lfa_smoother_rho(int p_t, double mu, double omega_t, double theta_x, double theta_t,
+                          double* rho, double* rho_closed_form) {
+  return guard([&] {
+    check_lfa(p_t, mu);
+    const stmg::lfa::Symbols s(p_t, mu);
+    if (rho) *rho = s.smoother_rho(omega_t, theta_x, theta_t);
+    if (rho_closed_form) *rho_closed_form = s.smoother_rho_closed_form(omega_t, theta_x, theta_t);
+  });
+}
+
+int stmg_lfa_smoother_symbol(int p_t, double mu, double omega_t, double theta_x, double theta_t,
+                             double* re, double* im) {
+  return guard([&] {
+    check_lfa(p_t, mu);
+    require(re && im, "null argument");
+    const stmg::lfa::Symbols s(p_t, mu);
+    s.smoother_symbol(omega_t, theta_x, theta_t, re, im);
+  });
+}
+
+int stmg_lfa_twogrid_symbol(int p_t, double mu, const stmg_cycle_config* cfg, int mode,
+                            double theta_x, double theta_t, double* re, double* im) {
+  return guard([&] {
+    check_lfa(p_t, mu);
+    check_mode(mode);
+    require(cfg && re && im, "null argument");
+    require(cfg->nu1 >= 0 && cfg->nu2 >= 0, "nu must be >= 0");
+    const stmg::lfa::Symbols s(p_t, mu);
+    s.twogrid_symbol(cfg->omega_t, cfg->nu1, cfg->nu2, mode, theta_x, theta_t, re, im);
+  });
+}
+
+int stmg_lfa_spectral_radius(int n, const double* re, const double* im, double* out) {
+  return guard([&] {
+    require(n >= 1 && re && out, "bad argument");
+    *out = stmg::lfa::spectral_radius(n, re, im);
+  });
+}
+
+int stmg_lfa_smoothing_factor(int p_t, double mu, double omega_t, int mode, int n_theta_x,
+                              int n_theta_t, double* out) {
+  return guard([&] {
+    check_lfa(p_t, mu);
+    check_mode(mode);
+    require(out != nullptr, "null argument");
+    *out = stmg::lfa::smoothing_factor(p_t, mu, omega_t, mode, n_theta_x, n_theta_t);
+  });
+}
+
+int stmg_lfa_twogrid_factor(int p_t, double mu, const stmg_cycle_config* cfg, int mode,
+                            int n_theta_x, int n_theta_t, double* out) {
+  return guard([&] {
+    check_lfa(p_t, mu);
+    check_mode(mode);
+    require(cfg && out, "null argument");
+    require(cfg->nu1 >= 0 && cfg->nu2 >= 0, "nu must be >= 0");
+    *out = stmg::lfa::twogrid_factor(p_t, mu, cfg->omega_t, cfg->nu1, cfg->nu2, mode, n_theta_x,
+                                     n_theta_t);
+  });
+}
+
+int stmg_lfa_twogrid_factor_inexact(int p_t, double mu, const stmg_cycle_config* cfg,
+                                    double omega_x, int nu1_x, int nu2_x, int mode, int n_theta_x,
+                                    int n_theta_t, double* out) {
+  return guard([&] {
+    check_lfa(p_t, mu);
+    check_mode(mode);
+    require(cfg && out, "null argument");
+    require(cfg->nu1 >= 0 && cfg->nu2 >= 0 && nu1_x >= 0 && nu2_x >= 0, "nu must be >= 0");
+    *out = stmg::lfa::twogrid_factor_inexact(p_t, mu, cfg->omega_t, cfg->nu1, cfg->nu2, omega_x,
+                                             nu1_x, nu2_x, mode, n_theta_x, n_theta_t);
+  });
+}
+
+// ------------------------------------------- two-grid factor measurement (GPU)
+int stmg_measure_convergence_factor(const stmg_rho_problem* pr, const stmg_cycle_config* cfg,
+                                    uint64_t seed, int n_theta_x, int n_theta_t,
+                                    stmg_rho_measurement* out) {
+  stmg_ctx* c = nullptr;
+  double* u = nullptr;
+  double* f = nullptr;
+  double* r = nullptr;
+  const int st = guard([&] {
+    require(pr && cfg && out, "null argument");
+    check_cfg(cfg);
+    check_mode(pr->mode);
+    require(pr->mu > 0.0, "mu must be positive");
+    require(pr->time_level >= 1 && pr->time_level <= 30, "time_level out of range");
+    require(pr->space_level >= 0 && pr->space_level <= 20, "space_level out of range");
+    // tau = mu h^2 with h = 1 / (n1 + 1) (bench.cpp:81-83)
+    const double h = 1.0 / double(int64_t(1) << (pr->space_level + 1));
+    const int64_t n_t = int64_t(1) << pr->time_level;
+    stmg_hierarchy_params hp{};
+    hp.p_t = pr->p_t;
+    hp.dim = pr->dim;
+    hp.space_level = pr->space_level;
+    hp.time_level = pr->time_level;
+    hp.t_final = pr->mu * h * h * double(n_t);
+    hp.mu_star = 0.0;
+    hp.policy = STMG_POLICY_MU_DRIVEN;
+    hp.two_grid = pr->mode;
+    hp.device = pr->device;
+    hp.shards = 1;
+    if (stmg_create(&hp, &c) != STMG_OK) throw std::runtime_error(g_err);
+    int64_t n = 0;
+    CK_ABI(stmg_level_size(c, 0, &n));
+    CK_ABI(stmg_device_alloc(c, size_t(n) * 8, reinterpret_cast<void**>(&u)));
+    CK_ABI(stmg_device_alloc(c, size_t(n) * 8, reinterpret_cast<void**>(&f)));
+    CK_ABI(stmg_device_alloc(c, size_t(n) * 8, reinterpret_cast<void**>(&r)));
+    CK_ABI(stmg_memset_zero(c, f, size_t(n) * 8));
+    stmg_rho_measurement m{};
+    m.seed_used = seed;
+    double r0 = 0.0;
+    for (bool first = true;; first = false) {  // a zero initial residual reseeds (bench.cpp:107-121)
+      if (!first) ++m.seed_used;
+      CK_ABI(stmg_fill_uniform(c, u, n, m.seed_used, 1, 0));
+      CK_ABI(stmg_residual(c, 0, u, f, r));
+      CK_ABI(stmg_norm(c, 0, r, &r0));
+      if (r0 > 0.0) break;
+      require(m.seed_used - seed < 16, "initial guess keeps solving the system");
+    }
+    const double floor = 1e-13 * r0;
+    double prev = r0, rho = 0.0;
+    for (int k = 0; k < 250; ++k) {
+      CK_ABI(stmg_mg_cycle(c, 0, u, f, cfg));
+      double rk = 0.0;
+      CK_ABI(stmg_residual(c, 0, u, f, r));
+      CK_ABI(stmg_norm(c, 0, r, &rk));
+      ++m.n_iterations_used;
+      if (prev > floor) rho = std::max(rho, rk / prev);
+      prev = rk;
+      if (rk <= floor) break;
+    }
+    m.measured_rho = rho;
+    m.predicted_rho = stmg::lfa::twogrid_factor(pr->p_t, pr->mu, cfg->omega_t, cfg->nu1, cfg->nu2,
+                                                pr->mode, n_theta_x, n_theta_t);
+    *out = m;
+  });
+  if (c) {
+    if (u) stmg_device_free(c, u);
+    if (f) stmg_device_free(c, f);
+    if (r) stmg_device_free(c, r);
+    stmg_destroy(c);
+  }
+  return st;
 }
 
 }  // extern "C"

@@ -22,7 +22,7 @@ B.build()
 obj = os.path.join(B.OBJ, f"stmg_kernels_{name}.o")
 subprocess.run([B.nvcc()] + B.NVFLAGS + ["-I" + B.CSRC] + defs + ["-c", src, "-o", obj],
                check=True)
-others = [os.path.join(B.OBJ, o) for o in ("stmg_capi.o", "stmg_setup.o")]
+others = [os.path.join(B.OBJ, os.path.splitext(s)[0] + ".o") for s in B.SOURCES if s != "stmg_kernels.cu"]
 out = os.path.join(B.PKG, f"_variant_{name}.so")
 subprocess.run([B.nvcc()] + B.ARCH + ["-shared", "-o", out, obj] + others + ["-cudart", "static"],
                check=True)
