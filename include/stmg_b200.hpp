@@ -75,6 +75,58 @@ inline double critical_mu(int p_t) {
   if (v != v) throw std::invalid_argument(stmg_last_error());
   return v;
 }
+// lfa.hpp:15-47 (host-side analysis; no GPU needed)
+inline double beta(double theta_x) {
+  double v = 0.0;
+  check(stmg_lfa_beta(theta_x, &v));
+  return v;
+}
+inline double alpha(int p_t, double mu, double theta_x) {
+  double v = 0.0;
+  check(stmg_lfa_alpha(p_t, mu, theta_x, &v));
+  return v;
+}
+struct FrequencyGrid {
+  int n_theta_x = 256;
+  int n_theta_t = 256;
+};
+struct TwoGridConfig {
+  double omega_t = 0.5;
+  int nu1 = 1;
+  int nu2 = 1;
+};
+struct SpatialSmootherConfig {
+  double omega_x = 2.0 / 3.0;
+  int nu1_x = 2;
+  int nu2_x = 2;
+};
+inline stmg_cycle_config to_c(const TwoGridConfig& c) {
+  return stmg_cycle_config{c.nu1, c.nu2, 1, c.omega_t, STMG_PATH_SPECTRAL};
+}
+// lfa.hpp:125-150
+inline double smoothing_factor(int p_t, double mu, double omega_t, Coarsening mode,
+                               const FrequencyGrid& grid = {}) {
+  double v = 0.0;
+  check(stmg_lfa_smoothing_factor(p_t, mu, omega_t, int(mode), grid.n_theta_x, grid.n_theta_t,
+                                  &v));
+  return v;
+}
+inline double twogrid_factor(int p_t, double mu, const TwoGridConfig& cfg, Coarsening mode,
+                             const FrequencyGrid& grid = {}) {
+  const stmg_cycle_config c = to_c(cfg);
+  double v = 0.0;
+  check(stmg_lfa_twogrid_factor(p_t, mu, &c, int(mode), grid.n_theta_x, grid.n_theta_t, &v));
+  return v;
+}
+inline double twogrid_factor_inexact(int p_t, double mu, const TwoGridConfig& cfg,
+                                     const SpatialSmootherConfig& sp, Coarsening mode,
+                                     const FrequencyGrid& grid = {}) {
+  const stmg_cycle_config c = to_c(cfg);
+  double v = 0.0;
+  check(stmg_lfa_twogrid_factor_inexact(p_t, mu, &c, sp.omega_x, sp.nu1_x, sp.nu2_x, int(mode),
+                                        grid.n_theta_x, grid.n_theta_t, &v));
+  return v;
+}
 }  // namespace lfa
 
 // mg.hpp:49-58
