@@ -66,14 +66,35 @@ typedef struct {
                        halo/gather/scatter logic as the multi-GPU path) */
 } stmg_hierarchy_params;
 
-/* CycleConfig + SmootherConfig (mg.hpp:66-71, smoother.hpp:15-24). */
+/* Block solver behind the smoother (smoother.hpp:13, BlockSolverKind). */
+#define STMG_BLOCK_EXACT 0  /* exact inverse of every time-step block */
+#define STMG_BLOCK_VCYCLE 1 /* one spatial V-cycle per block (spatial_vcycle) */
+
+/* CycleConfig + SmootherConfig (mg.hpp:66-71, smoother.hpp:15-24).  The
+ * spatial fields are read only when block_solver == STMG_BLOCK_VCYCLE;
+ * stmg_cycle_config_init fills the reference defaults. */
 typedef struct {
   int nu1;          /* pre-smoothing sweeps */
   int nu2;          /* post-smoothing sweeps */
   int gamma;        /* 1 = V-cycle */
   double omega_t;   /* block-Jacobi damping */
   int path;         /* STMG_PATH_* */
+  int block_solver; /* STMG_BLOCK_* (0 = exact when zero-initialised) */
+  double omega_x;   /* spatial damped-Jacobi weight (2/3) */
+  int nu1_x;        /* spatial pre-smoothing sweeps (2) */
+  int nu2_x;        /* spatial post-smoothing sweeps (2) */
+  int gamma_x;      /* spatial cycle index (1 = V) */
 } stmg_cycle_config;
+
+/* SmootherConfig (smoother.hpp:15-24) for the single-operator entry points. */
+typedef struct {
+  double omega_t;   /* damping of the block Jacobi iteration (0.5) */
+  int nu;           /* smoothing steps per call (1) */
+  int block_solver; /* STMG_BLOCK_* */
+  double omega_x;   /* (2/3) */
+  int nu1_x, nu2_x; /* (2, 2) */
+  int gamma_x;      /* (1) */
+} stmg_smoother_config;
 
 /* SolveReport (mg.hpp:83-89). */
 typedef struct {
@@ -128,6 +149,12 @@ int stmg_fill_uniform(stmg_ctx* ctx, double* dst_dev, int64_t n, uint64_t seed,
 /* f(0,k,:) += psi_k(0) * M_h u0 on the finest level (u0: n_x nodal values). */
 int stmg_fold_u0(stmg_ctx* ctx, double* f_dev, const double* u0_dev);
 
+/* Reference defaults: CycleConfig (mg.hpp:66-71: nu1 = nu2 = 2, gamma = 1)
+ * with SmootherConfig (smoother.hpp:15-24: omega_t = 1/2, exact blocks,
+ * omega_x = 2/3, nu1_x = nu2_x = 2, gamma_x = 1), spectral path. */
+int stmg_cycle_config_init(stmg_cycle_config* cfg);
+int stmg_smoother_config_init(stmg_smoother_config* cfg);
+
 /* ---- operators: reference entry points (device pointers) ---------------- */
 /* apply (st_system.cpp:44-49): y = L u. */
 int stmg_apply(stmg_ctx* ctx, int level, const double* u, double* y);
@@ -142,6 +169,16 @@ int stmg_block_solve(stmg_ctx* ctx, int level, const double* b, double* x);
  * u <- u + omega_t A^-1 (f - L u). */
 int stmg_smooth(stmg_ctx* ctx, int level, double* u, const double* f,
                 double omega_t, int nu);
+/* block_jacobi_step with a full SmootherConfig (smoother.cpp:96-106): nu
+ * sweeps of u <- u + omega_t D~^-1 (f - L u), D~^-1 = the exact block inverse
+ * or one spatial V-cycle per time step (block_solver). */
+int stmg_block_jacobi_step(stmg_ctx* ctx, int level, double* u, const double* f,
+                           const stmg_smoother_config* cfg);
+/* SpatialVCycleSolver::cycle (smoother.cpp:71-78) on every time step of the
+ * level: x_n = cycle(b_n, x0_n); x0 NULL = zero initial guess (the smoother's
+ * D~ approximation).  Uses omega_x, nu1_x, nu2_x, gamma_x of cfg. */
+int stmg_spatial_vcycle(stmg_ctx* ctx, int level, const double* b, const double* x0,
+                        double* x, const stmg_smoother_config* cfg);
 /* restrict_semi / restrict_full (transfer.cpp:75-85, 138-149).  mode 0 uses
  * the level's coarsen_to_next. */
 int stmg_restrict(stmg_ctx* ctx, int level, int mode, const double* fine,

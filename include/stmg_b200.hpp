@@ -101,7 +101,8 @@ struct SpatialSmootherConfig {
   int nu2_x = 2;
 };
 inline stmg_cycle_config to_c(const TwoGridConfig& c) {
-  return stmg_cycle_config{c.nu1, c.nu2, 1, c.omega_t, STMG_PATH_SPECTRAL};
+  return stmg_cycle_config{c.nu1, c.nu2, 1, c.omega_t, STMG_PATH_SPECTRAL, STMG_BLOCK_EXACT,
+                           2.0 / 3.0, 2, 2, 1};
 }
 // lfa.hpp:125-150
 inline double smoothing_factor(int p_t, double mu, double omega_t, Coarsening mode,
@@ -148,7 +149,16 @@ struct SmootherConfig {
   double omega_t = 0.5;
   int nu = 1;
   BlockSolverKind block_solver = BlockSolverKind::exact;
+  // spatial multigrid used when block_solver == spatial_vcycle
+  double omega_x = 2.0 / 3.0;
+  int nu1_x = 2;
+  int nu2_x = 2;
+  int gamma_x = 1;
 };
+inline stmg_smoother_config to_c(const SmootherConfig& c) {
+  return stmg_smoother_config{c.omega_t, c.nu, int(c.block_solver), c.omega_x,
+                              c.nu1_x,   c.nu2_x, c.gamma_x};
+}
 
 // mg.hpp:66-71
 struct CycleConfig {
@@ -208,8 +218,8 @@ class STHierarchy {
 };
 
 inline stmg_hierarchy_params to_c(const HierarchyParams& p, int two_grid) {
-  if (p.block_solver != BlockSolverKind::exact)
-    throw std::invalid_argument("only exact block solves are available on the B200 path");
+  // block_solver needs no setup on the B200 path (no factorisations; the
+  // spatial cycle's constants are built on first use): the cycle config selects it.
   stmg_hierarchy_params c{};
   c.p_t = p.p_t;
   c.dim = p.dim;
@@ -286,18 +296,35 @@ inline double norm(const STOperator& op, const BlockVector& v) {
   check(stmg_norm(op.ctx, op.level, v.data(), &out));
   return out;
 }
+// smoother.hpp:29-58: SpatialVCycleSolver.  On the B200 path it is bound to a
+// level's operator (its DG block and finest grid) and cycles every time step
+// of a level vector at once; x0 == nullptr is the smoother's zero guess.
+class SpatialVCycleSolver {
+ public:
+  explicit SpatialVCycleSolver(const STOperator& op) : op_(op) {}
+  BlockVector cycle(const BlockVector& b, const BlockVector* x0, const SmootherConfig& cfg) const {
+    BlockVector x = BlockVector::for_level(op_);
+    const stmg_smoother_config c = to_c(cfg);
+    check(stmg_spatial_vcycle(op_.ctx, op_.level, b.data(), x0 ? x0->data() : nullptr, x.data(),
+                              &c));
+    return x;
+  }
+
+ private:
+  STOperator op_;
+};
+
 // st_system.hpp:70-72
 inline BlockVector forward_substitution_solve(const STOperator& op, const BlockVector& f) {
   BlockVector u = make_vector(op);
   check(stmg_forward_substitution(op.ctx, op.level, f.data(), u.data()));
   return u;
 }
-// smoother.hpp:68-70 (exact block solves)
+// smoother.hpp:68-70 (exact block solves or one spatial V-cycle per block)
 inline void block_jacobi_step(const STOperator& op, BlockVector& u, const BlockVector& f,
                               const SmootherConfig& cfg) {
-  if (cfg.block_solver != BlockSolverKind::exact)
-    throw std::invalid_argument("only exact block solves are available on the B200 path");
-  check(stmg_smooth(op.ctx, op.level, u.data(), f.data(), cfg.omega_t, cfg.nu));
+  const stmg_smoother_config c = to_c(cfg);
+  check(stmg_block_jacobi_step(op.ctx, op.level, u.data(), f.data(), &c));
 }
 
 namespace detail {
@@ -334,9 +361,9 @@ inline BlockVector prolong_full(const STOperator& op, const BlockVector& coarse)
 }
 
 inline stmg_cycle_config to_c(const CycleConfig& c) {
-  if (c.smoother.block_solver != BlockSolverKind::exact)
-    throw std::invalid_argument("only exact block solves are available on the B200 path");
-  return stmg_cycle_config{c.nu1, c.nu2, c.gamma, c.smoother.omega_t, c.path};
+  const SmootherConfig& s = c.smoother;
+  return stmg_cycle_config{c.nu1,    c.nu2,   c.gamma,   s.omega_t, c.path, int(s.block_solver),
+                           s.omega_x, s.nu1_x, s.nu2_x, s.gamma_x};
 }
 
 // mg.hpp:75-76

@@ -131,11 +131,47 @@ def time_restriction(R1, R2, n_t, nx):
     return T
 
 
+def spatial_vcycle(p, tau, dim, level, b, x0=None, omega_x=2.0 / 3.0, nu1_x=2, nu2_x=2,
+                   gamma_x=1):
+    """Dense restatement of SpatialVCycleSolver::cycle (smoother.cpp:8-78) on one
+    slab b (DG-major, length (p+1) * n1^dim): damped point-block Jacobi with
+    D = K diag(M_h) + M diag(K_h), full weighting / its transpose per DG
+    component, numpy.linalg.solve on the 1-node grid."""
+    K, M, _ = dg_block(p, tau)
+    nl = p + 1
+
+    def rec(s, x, rhs):
+        Mh, Kh = space_mats(dim, s)
+        A = dense_block(K, M, Mh, Kh)
+        if s == 0:
+            return np.linalg.solve(A, rhs)
+        D = np.kron(K * Mh[0, 0] + M * Kh[0, 0], np.eye(Mh.shape[0]))
+        for _ in range(nu1_x):
+            x = x + omega_x * np.linalg.solve(D, rhs - A @ x)
+        r = rhs - A @ x
+        Rf = np.kron(np.eye(nl), space_restriction(dim, s))
+        rc = Rf @ r
+        ec = np.zeros_like(rc)
+        for _ in range(gamma_x):
+            ec = rec(s - 1, ec, rc)
+        x = x + Rf.T @ ec
+        for _ in range(nu2_x):
+            x = x + omega_x * np.linalg.solve(D, rhs - A @ x)
+        return x
+
+    x = np.zeros_like(b) if x0 is None else np.array(x0, dtype=np.float64)
+    return rec(level, x, b)
+
+
 class DenseHierarchy:
     """Dense restatement of build_hierarchy + mg_cycle (mg.cpp:10-132)."""
 
-    def __init__(self, p_t, dim, space_level, time_level, t_final=1.0, mu_star=0.3, policy=0):
+    def __init__(self, p_t, dim, space_level, time_level, t_final=1.0, mu_star=0.3, policy=0,
+                 block_solver="exact", spatial=None):
         self.levels = []
+        self.p_t, self.dim = p_t, dim
+        self.block_solver = block_solver  # "exact" | "vcycle" (smoother.cpp:82-92)
+        self.spatial = dict(spatial or {})
         n_t = 2 ** time_level
         tau = t_final / n_t
         s = space_level
@@ -171,7 +207,12 @@ class DenseHierarchy:
         b = L["A"].shape[0]
         for _ in range(nu):
             r = f - L["L"] @ u
-            x = np.linalg.solve(L["A"], r.reshape(L["n_t"], b).T).T.reshape(-1)
+            if self.block_solver == "vcycle":
+                rs = r.reshape(L["n_t"], b)
+                x = np.concatenate([spatial_vcycle(self.p_t, L["tau"], self.dim, L["s"], rs[n],
+                                                   **self.spatial) for n in range(L["n_t"])])
+            else:
+                x = np.linalg.solve(L["A"], r.reshape(L["n_t"], b).T).T.reshape(-1)
             u = u + omega * x
         return u
 

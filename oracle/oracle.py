@@ -33,7 +33,40 @@ class _Params(C.Structure):
 
 class _Cycle(C.Structure):
     _fields_ = [("nu1", C.c_int), ("nu2", C.c_int), ("gamma", C.c_int),
-                ("omega_t", C.c_double)]
+                ("omega_t", C.c_double), ("block_solver", C.c_int),
+                ("omega_x", C.c_double), ("nu1_x", C.c_int), ("nu2_x", C.c_int),
+                ("gamma_x", C.c_int)]
+
+
+class _Smoother(C.Structure):
+    _fields_ = [("omega_t", C.c_double), ("nu", C.c_int), ("block_solver", C.c_int),
+                ("omega_x", C.c_double), ("nu1_x", C.c_int), ("nu2_x", C.c_int),
+                ("gamma_x", C.c_int)]
+
+
+# SmootherConfig defaults (smoother.hpp:15-24): omega_x = 2/3, nu1_x = nu2_x = 2,
+# gamma_x = 1.  block_solver: "exact" (0) or "vcycle" (1, spatial_vcycle).
+SPATIAL_DEFAULTS = dict(omega_x=2.0 / 3.0, nu1_x=2, nu2_x=2, gamma_x=1)
+
+
+def _solver_kind(block_solver) -> int:
+    if block_solver in (0, "exact"):
+        return 0
+    if block_solver in (1, "vcycle", "spatial_vcycle"):
+        return 1
+    raise ValueError("block_solver must be 'exact' or 'vcycle'")
+
+
+def _cycle(nu1, nu2, gamma, omega_t, block_solver="exact", **sp):
+    x = dict(SPATIAL_DEFAULTS, **sp)
+    return _Cycle(nu1, nu2, gamma, omega_t, _solver_kind(block_solver), x["omega_x"],
+                  x["nu1_x"], x["nu2_x"], x["gamma_x"])
+
+
+def _smoother(omega_t=0.5, nu=1, block_solver="exact", **sp):
+    x = dict(SPATIAL_DEFAULTS, **sp)
+    return _Smoother(omega_t, nu, _solver_kind(block_solver), x["omega_x"], x["nu1_x"],
+                     x["nu2_x"], x["gamma_x"])
 
 
 class _LevelInfo(C.Structure):
@@ -68,6 +101,8 @@ def lib():
         L.or_residual.argtypes = [C.c_void_p, C.c_int, P, P, P]
         L.or_norm.argtypes = [C.c_void_p, C.c_int, P]
         L.or_smooth.argtypes = [C.c_void_p, C.c_int, P, P, C.c_double, C.c_int]
+        L.or_smooth_ex.argtypes = [C.c_void_p, C.c_int, P, P, C.POINTER(_Smoother)]
+        L.or_spatial_vcycle.argtypes = [C.c_void_p, C.c_int, P, P, P, C.POINTER(_Smoother)]
         L.or_restrict.argtypes = [C.c_void_p, C.c_int, C.c_int, P, P]
         L.or_prolong.argtypes = [C.c_void_p, C.c_int, C.c_int, P, P]
         L.or_mg_cycle.argtypes = [C.c_void_p, C.c_int, P, P, C.POINTER(_Cycle)]
@@ -197,6 +232,21 @@ class Hierarchy:
         _check(lib().or_smooth(self._h, level, _ptr(u), _ptr(f), omega_t, nu))
         return u
 
+    def block_jacobi_step(self, level, u, f, omega_t=0.5, nu=1, block_solver="exact", **sp):
+        """block_jacobi_step with a full SmootherConfig (smoother.cpp:96-106)."""
+        u = np.ascontiguousarray(u, dtype=np.float64).copy()
+        sc = _smoother(omega_t, nu, block_solver, **sp)
+        _check(lib().or_smooth_ex(self._h, level, _ptr(u), _ptr(f), C.byref(sc)))
+        return u
+
+    def spatial_vcycle(self, level, b, x0=None, **sp):
+        """SpatialVCycleSolver::cycle on every time step (smoother.cpp:71-78)."""
+        x = np.zeros_like(b)
+        sc = _smoother(block_solver="vcycle", **sp)
+        x0p = _ptr(np.ascontiguousarray(x0, np.float64)) if x0 is not None else None
+        _check(lib().or_spatial_vcycle(self._h, level, _ptr(b), x0p, _ptr(x), C.byref(sc)))
+        return x
+
     def coarse_size(self, level, mode=0):
         L = self.levels[level]
         mode = mode or L.coarsen_to_next
@@ -213,16 +263,17 @@ class Hierarchy:
         _check(lib().or_prolong(self._h, level, mode, _ptr(coarse), _ptr(out)))
         return out
 
-    def mg_cycle(self, level, u, f, nu1=1, nu2=1, gamma=1, omega_t=0.5):
+    def mg_cycle(self, level, u, f, nu1=1, nu2=1, gamma=1, omega_t=0.5,
+                 block_solver="exact", **sp):
         u = np.ascontiguousarray(u, dtype=np.float64).copy()
-        cfg = _Cycle(nu1, nu2, gamma, omega_t)
+        cfg = _cycle(nu1, nu2, gamma, omega_t, block_solver, **sp)
         _check(lib().or_mg_cycle(self._h, level, _ptr(u), _ptr(f), C.byref(cfg)))
         return u
 
     def solve(self, f, u=None, nu1=1, nu2=1, gamma=1, omega_t=0.5, eps=1e-8,
-              max_iter=250):
+              max_iter=250, block_solver="exact", **sp):
         u = self.zeros(0) if u is None else np.ascontiguousarray(u, np.float64).copy()
-        cfg = _Cycle(nu1, nu2, gamma, omega_t)
+        cfg = _cycle(nu1, nu2, gamma, omega_t, block_solver, **sp)
         hist = np.zeros(max_iter + 1)
         it, conv, wall = C.c_int(), C.c_int(), C.c_double()
         _check(lib().or_solve(self._h, _ptr(f), _ptr(u), C.byref(cfg), eps, max_iter,

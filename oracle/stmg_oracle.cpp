@@ -313,6 +313,12 @@ struct Level {
   TT tt;
   // exact block solve data: orthonormal DST-I matrix, per-axis eigenvalues
   std::vector<double> S, mval, kval;
+  // SpatialVCycleSolver stack (smoother.cpp:8-27): grids finest..1-node, the
+  // point-block Jacobi block diag(M) K + diag(K) M per grid, and the 1-node
+  // block matrix of the coarsest grid (row-major nl x nl).
+  std::vector<Grid> sgrid;
+  std::vector<std::vector<double>> sjac;
+  std::vector<double> scoarse;
   i64 nl() const { return dg.nl(); }
   i64 slab() const { return grid.nx * dg.nl(); }
   i64 size() const { return n_t * slab(); }
@@ -333,6 +339,23 @@ void init_block_solver(Level& L) {
     L.mval[k] = h / 3.0 * (2.0 + std::cos(th));  // M1 -> (h/3)(2 + c)
     L.kval[k] = 4.0 / h * s * s;                  // K1 -> (2/h)(1 - c)
   }
+  // smoother.cpp:8-27: one level per grid L..0; uniform grid, so one
+  // diagonal value of M and K per level (M(0,0), K(0,0) of the Kronecker
+  // products: md^dim and dim * kd * md^(dim-1)).
+  const int nl = L.dg.nl();
+  L.sgrid.clear();
+  L.sjac.clear();
+  for (int g = L.grid.level; g >= 0; --g) {
+    const Grid G = make_grid(L.grid.dim, g);
+    const double md = 4.0 * G.h / 6.0, kd = 2.0 / G.h;
+    const double mdiag = std::pow(md, G.dim), kdiag = G.dim * kd * std::pow(md, G.dim - 1);
+    std::vector<double> D(nl * nl);
+    for (int i = 0; i < nl * nl; ++i) D[i] = mdiag * L.dg.K[i] + kdiag * L.dg.M[i];
+    L.sgrid.push_back(G);
+    L.sjac.push_back(std::move(D));
+  }
+  // coarsest (1-node) grid: assemble_block_matrix = K (x) M_h + M (x) K_h
+  L.scoarse = L.sjac.back();
 }
 
 struct Hier {
@@ -622,6 +645,105 @@ void prolong_space(const Grid& cg, const Grid& fg, const double* c, double* out)
   std::copy(cur.begin(), cur.end(), out);
 }
 
+// ------------------------------------------------ smoother.cpp:8-92 --
+// SpatialVCycleSolver: one geometric multigrid cycle in space for one
+// time-step block A = K_tau (x) M_h + M_tau (x) K_h (damped point-block
+// Jacobi on every grid, full weighting / linear interpolation per DG
+// component, direct solve on the 1-node grid).  x, b: one slab (nl
+// components of nx values, component-major as BlockVector::step).
+struct SvcCfg {
+  double omega_x = 2.0 / 3.0;
+  int nu1_x = 2, nu2_x = 2, gamma_x = 1;
+};
+
+// st_system.cpp:18-23: y = (M_h X) K^T + (K_h X) M^T.
+void apply_diag_block(const DG& dg, const Grid& g, const double* x, double* y) {
+  const int nl = dg.nl();
+  const i64 nx = g.nx;
+  std::vector<double> MX(nl * nx), KX(nl * nx);
+  for (int l = 0; l < nl; ++l) {
+    space_apply(g, false, x + l * nx, MX.data() + l * nx);
+    space_apply(g, true, x + l * nx, KX.data() + l * nx);
+  }
+  for (int k = 0; k < nl; ++k) {
+    double* yk = y + k * nx;
+    for (i64 r = 0; r < nx; ++r) yk[r] = 0.0;
+    for (int l = 0; l < nl; ++l) {
+      const double a = dg.K[k * nl + l];
+      for (i64 r = 0; r < nx; ++r) yk[r] += MX[l * nx + r] * a;
+    }
+    for (int l = 0; l < nl; ++l) {
+      const double a = dg.M[k * nl + l];
+      for (i64 r = 0; r < nx; ++r) yk[r] += KX[l * nx + r] * a;
+    }
+  }
+}
+
+// smoother.cpp:29-38: count sweeps x += omega D^-1 (b - A x), D per node.
+void svc_jacobi(const Level& L, size_t lev, int count, double omega, double* x, const double* b) {
+  const Grid& g = L.sgrid[lev];
+  const int nl = L.dg.nl();
+  const i64 nx = g.nx;
+  std::vector<double> r(nl * nx), node(nl);
+  for (int s = 0; s < count; ++s) {
+    apply_diag_block(L.dg, g, x, r.data());
+    for (i64 i = 0; i < nl * nx; ++i) r[i] = b[i] - r[i];
+    for (i64 q = 0; q < nx; ++q) {
+      for (int l = 0; l < nl; ++l) node[l] = r[l * nx + q];
+      dense_solve(nl, L.sjac[lev], node.data(), 1);
+      for (int l = 0; l < nl; ++l) x[l * nx + q] += omega * node[l];
+    }
+  }
+}
+
+// smoother.cpp:40-69.
+void svc_recurse(const Level& L, size_t lev, double* x, const double* b, const SvcCfg& cfg) {
+  const Grid& g = L.sgrid[lev];
+  const int nl = L.dg.nl();
+  const i64 nx = g.nx;
+  if (lev + 1 == L.sgrid.size()) {  // 1-node grid: direct solve
+    std::copy(b, b + nl * nx, x);
+    dense_solve(nl, L.scoarse, x, 1);
+    return;
+  }
+  svc_jacobi(L, lev, cfg.nu1_x, cfg.omega_x, x, b);
+  std::vector<double> r(nl * nx);
+  apply_diag_block(L.dg, g, x, r.data());
+  for (i64 i = 0; i < nl * nx; ++i) r[i] = b[i] - r[i];
+  const Grid& cg = L.sgrid[lev + 1];
+  std::vector<double> rc(nl * cg.nx), ec(nl * cg.nx, 0.0), corr(nl * nx);
+  for (int l = 0; l < nl; ++l) restrict_space(g, cg, r.data() + l * nx, rc.data() + l * cg.nx);
+  for (int k = 0; k < cfg.gamma_x; ++k) svc_recurse(L, lev + 1, ec.data(), rc.data(), cfg);
+  for (int l = 0; l < nl; ++l) prolong_space(cg, g, ec.data() + l * cg.nx, corr.data() + l * nx);
+  for (i64 i = 0; i < nl * nx; ++i) x[i] += corr[i];
+  svc_jacobi(L, lev, cfg.nu2_x, cfg.omega_x, x, b);
+}
+
+// SpatialVCycleSolver::cycle (smoother.cpp:71-78): x = cycle from x0.
+void svc_cycle(const Level& L, const double* b, const double* x0, double* x, const SvcCfg& cfg) {
+  const i64 sl = L.slab();
+  if (x0) std::copy(x0, x0 + sl, x);
+  else std::fill(x, x + sl, 0.0);
+  svc_recurse(L, 0, x, b, cfg);
+}
+
+// block_jacobi_step (smoother.cpp:96-106) with block_solver = spatial_vcycle:
+// u_n += omega_t * cycle(r_n, 0) on the frozen residual.
+void smooth_inexact(const Level& L, double* u, const double* f, double omega, int nu,
+                    const SvcCfg& cfg) {
+  const i64 sl = L.slab();
+  std::vector<double> r(L.size());
+  for (int s = 0; s < nu; ++s) {
+    residual(L, u, f, r.data());
+#pragma omp parallel for schedule(static)
+    for (i64 n = 0; n < L.n_t; ++n) {
+      std::vector<double> x(sl);
+      svc_cycle(L, r.data() + n * sl, nullptr, x.data(), cfg);
+      for (i64 i = 0; i < sl; ++i) u[n * sl + i] += omega * x[i];
+    }
+  }
+}
+
 // transfer.cpp:75-85: c_n = U_2n R1^T + U_2n+1 R2^T.
 void restrict_semi(const Level& F, i64 nx, const double* fine, double* coarse) {
   if (F.n_t % 2 != 0) throw std::invalid_argument("restrict_semi requires an even step count");
@@ -710,6 +832,26 @@ void prolong_level(const Hier& H, int lev, int mode, const double* coarse, doubl
 }
 
 // --------------------------------------------------------------------- mg --
+SvcCfg svc_of(double omega_x, int nu1_x, int nu2_x, int gamma_x) {
+  SvcCfg c;
+  c.omega_x = omega_x;
+  c.nu1_x = nu1_x;
+  c.nu2_x = nu2_x;
+  c.gamma_x = gamma_x;
+  if (nu1_x < 0 || nu2_x < 0 || gamma_x < 1)
+    throw std::invalid_argument("spatial smoothing counts must be >= 0 and gamma_x >= 1");
+  return c;
+}
+
+// block_jacobi_step dispatch on SmootherConfig::block_solver (smoother.cpp:82-92).
+void smooth_cfg(const Level& L, double* u, const double* f, const or_cycle& cfg, int nu) {
+  if (cfg.block_solver == 1)
+    smooth_inexact(L, u, f, cfg.omega_t, nu,
+                   svc_of(cfg.omega_x, cfg.nu1_x, cfg.nu2_x, cfg.gamma_x));
+  else
+    smooth(L, u, f, cfg.omega_t, nu);
+}
+
 // mg.cpp:96-132.
 void mg_cycle(const Hier& H, size_t lev, double* u, const double* f, const or_cycle& cfg) {
   const Level& L = H.levels[lev];
@@ -717,7 +859,7 @@ void mg_cycle(const Hier& H, size_t lev, double* u, const double* f, const or_cy
     forward_substitution(L, f, u);
     return;
   }
-  smooth(L, u, f, cfg.omega_t, cfg.nu1);
+  smooth_cfg(L, u, f, cfg, cfg.nu1);
   std::vector<double> r(L.size());
   residual(L, u, f, r.data());
   const Level& C = H.levels[lev + 1];
@@ -728,7 +870,7 @@ void mg_cycle(const Hier& H, size_t lev, double* u, const double* f, const or_cy
   const i64 sz = L.size();
 #pragma omp parallel for schedule(static)
   for (i64 i = 0; i < sz; ++i) u[i] += corr[i];
-  smooth(L, u, f, cfg.omega_t, cfg.nu2);
+  smooth_cfg(L, u, f, cfg, cfg.nu2);
 }
 
 uint64_t mix64(uint64_t z) {
@@ -858,6 +1000,31 @@ int or_forward_substitution(const or_hier* h, int level, const double* f, double
 
 int or_smooth(const or_hier* h, int level, double* u, const double* f, double omega_t, int nu) {
   return guard([&] { smooth(level_of(h, level), u, f, omega_t, nu); });
+}
+
+int or_smooth_ex(const or_hier* h, int level, double* u, const double* f, const or_smoother* sc) {
+  return guard([&] {
+    if (!sc) throw std::invalid_argument("null smoother config");
+    const Level& L = level_of(h, level);
+    if (sc->block_solver == 1)
+      smooth_inexact(L, u, f, sc->omega_t, sc->nu,
+                     svc_of(sc->omega_x, sc->nu1_x, sc->nu2_x, sc->gamma_x));
+    else
+      smooth(L, u, f, sc->omega_t, sc->nu);
+  });
+}
+
+int or_spatial_vcycle(const or_hier* h, int level, const double* b, const double* x0, double* x,
+                      const or_smoother* sc) {
+  return guard([&] {
+    if (!sc) throw std::invalid_argument("null smoother config");
+    const Level& L = level_of(h, level);
+    const SvcCfg cfg = svc_of(sc->omega_x, sc->nu1_x, sc->nu2_x, sc->gamma_x);
+    const i64 sl = L.slab();
+#pragma omp parallel for schedule(static)
+    for (i64 n = 0; n < L.n_t; ++n)
+      svc_cycle(L, b + n * sl, x0 ? x0 + n * sl : nullptr, x + n * sl, cfg);
+  });
 }
 
 int or_restrict(const or_hier* h, int level, int mode, const double* fine, double* coarse) {

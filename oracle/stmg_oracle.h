@@ -38,10 +38,24 @@ typedef struct {
   int two_grid;     /* 0 full ladder; 1 semi two-grid; 2 full two-grid */
 } or_params;
 
+/* CycleConfig + its SmootherConfig (mg.hpp:66-71, smoother.hpp:15-24).
+ * block_solver: 0 exact, 1 spatial_vcycle (omega_x, nu1_x, nu2_x, gamma_x). */
 typedef struct {
   int nu1, nu2, gamma;
   double omega_t;
+  int block_solver;
+  double omega_x;
+  int nu1_x, nu2_x, gamma_x;
 } or_cycle;
+
+/* SmootherConfig (smoother.hpp:15-24). */
+typedef struct {
+  double omega_t;
+  int nu;
+  int block_solver;
+  double omega_x;
+  int nu1_x, nu2_x, gamma_x;
+} or_smoother;
 
 typedef struct {
   int64_t n_t, n_x, n_loc, n1;
@@ -75,6 +89,13 @@ int or_forward_substitution(const or_hier* h, int level, const double* f,
 /* smoother.cpp:96-106 */
 int or_smooth(const or_hier* h, int level, double* u, const double* f,
               double omega_t, int nu);
+/* block_jacobi_step with a full SmootherConfig (smoother.cpp:96-106). */
+int or_smooth_ex(const or_hier* h, int level, double* u, const double* f,
+                 const or_smoother* cfg);
+/* SpatialVCycleSolver::cycle (smoother.cpp:71-78) on every time step of the
+ * level: x_n = cycle(b_n, x0_n) (x0 may be NULL = zero guess). */
+int or_spatial_vcycle(const or_hier* h, int level, const double* b,
+                      const double* x0, double* x, const or_smoother* cfg);
 /* transfer.cpp: mode 1 semi, 2 full, 0 = level's coarsen_to_next */
 int or_restrict(const or_hier* h, int level, int mode, const double* fine,
                 double* coarse);

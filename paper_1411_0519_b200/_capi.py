@@ -29,7 +29,13 @@ class HierarchyParams(C.Structure):
 
 class CycleConfig(C.Structure):
     _fields_ = [("nu1", C.c_int), ("nu2", C.c_int), ("gamma", C.c_int),
-                ("omega_t", D), ("path", C.c_int)]
+                ("omega_t", D), ("path", C.c_int), ("block_solver", C.c_int),
+                ("omega_x", D), ("nu1_x", C.c_int), ("nu2_x", C.c_int), ("gamma_x", C.c_int)]
+
+
+class SmootherConfig(C.Structure):
+    _fields_ = [("omega_t", D), ("nu", C.c_int), ("block_solver", C.c_int), ("omega_x", D),
+                ("nu1_x", C.c_int), ("nu2_x", C.c_int), ("gamma_x", C.c_int)]
 
 
 class SolveReport(C.Structure):
@@ -80,6 +86,10 @@ SIGNATURES = [
     ("stmg_norm", C.c_int, [VP, C.c_int, VP, PD]),
     ("stmg_block_solve", C.c_int, [VP, C.c_int, VP, VP]),
     ("stmg_smooth", C.c_int, [VP, C.c_int, VP, VP, D, C.c_int]),
+    ("stmg_block_jacobi_step", C.c_int, [VP, C.c_int, VP, VP, C.POINTER(SmootherConfig)]),
+    ("stmg_spatial_vcycle", C.c_int, [VP, C.c_int, VP, VP, VP, C.POINTER(SmootherConfig)]),
+    ("stmg_cycle_config_init", C.c_int, [C.POINTER(CycleConfig)]),
+    ("stmg_smoother_config_init", C.c_int, [C.POINTER(SmootherConfig)]),
     ("stmg_restrict", C.c_int, [VP, C.c_int, C.c_int, VP, VP]),
     ("stmg_prolong", C.c_int, [VP, C.c_int, C.c_int, VP, VP]),
     ("stmg_forward_substitution", C.c_int, [VP, C.c_int, VP, VP]),

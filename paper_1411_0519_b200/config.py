@@ -3,9 +3,10 @@ io.cpp:9-46): one JSON document per run, validated field by field with the
 reference's field names and messages; JSON / CSV reports.
 
 Differences from the reference, by design of this library: ``dim`` may also be 3
-(the GPU path has 3D Q1); ``block_solver = "vcycle"`` parses (it is part of the
-format) but building a hierarchy with it raises, because the inexact spatial
-V-cycle block solver is not implemented on the GPU path.
+(the GPU path has 3D Q1).  ``block_solver = "vcycle"`` selects the inexact
+spatial-V-cycle block solver: on the B200 path it is a field
+of the cycle configuration (no per-level setup), so ``cycle_config`` carries it
+together with ``omega_x``, ``nu1_x`` and ``nu2_x``.
 """
 from __future__ import annotations
 
@@ -140,9 +141,6 @@ def dump_config(c: RunConfig) -> str:
 
 def hierarchy_params(c: RunConfig) -> dict:
     """Keyword arguments of stmg.Hierarchy (config.cpp:132-143; mu* = critical_mu)."""
-    if c.block_solver != "exact":
-        raise ValueError("config field 'block_solver': 'vcycle' (inexact spatial V-cycle block "
-                         "solves) is not implemented on the GPU path")
     return {"p_t": c.p_t, "dim": c.dim, "space_level": c.space_levels,
             "time_level": c.time_levels, "t_final": c.t_final, "mu_star": 0.0,
             "policy": _POLICY[c.coarsening]}
@@ -150,7 +148,9 @@ def hierarchy_params(c: RunConfig) -> dict:
 
 def cycle_config(c: RunConfig) -> CycleConfig:
     """config.cpp:145-156."""
-    return CycleConfig(nu1=c.nu1, nu2=c.nu2, gamma=c.gamma, omega_t=c.omega_t)
+    return CycleConfig(nu1=c.nu1, nu2=c.nu2, gamma=c.gamma, omega_t=c.omega_t,
+                       block_solver=c.block_solver, omega_x=c.omega_x, nu1_x=c.nu1_x,
+                       nu2_x=c.nu2_x)
 
 
 def solve_report_json(c: RunConfig, r: SolveReport) -> str:

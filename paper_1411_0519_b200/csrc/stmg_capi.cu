@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -141,12 +142,19 @@ struct stmg_ctx {
   struct GraphKey {
     int nu1, nu2, gamma, cur0;
     double omega;
+    int bs, nu1x, nu2x, gx;
+    double omx;
     bool operator<(const GraphKey& o) const {
       if (nu1 != o.nu1) return nu1 < o.nu1;
       if (nu2 != o.nu2) return nu2 < o.nu2;
       if (gamma != o.gamma) return gamma < o.gamma;
       if (cur0 != o.cur0) return cur0 < o.cur0;
-      return omega < o.omega;
+      if (omega != o.omega) return omega < o.omega;
+      if (bs != o.bs) return bs < o.bs;
+      if (nu1x != o.nu1x) return nu1x < o.nu1x;
+      if (nu2x != o.nu2x) return nu2x < o.nu2x;
+      if (gx != o.gx) return gx < o.gx;
+      return omx < o.omx;
     }
   };
   struct GraphEntry {
@@ -181,6 +189,10 @@ struct stmg_ctx {
   double* d_r0 = nullptr;
   bool use_device_loop = true;
   bool use_fused = true;  // fused level-0 schedule for V(1,1) solves
+  // inexact block solver: sine tables per spatial grid level and one
+  // workspace (X, B per sub-level) shared by all levels, sized for level 0
+  std::map<int, double*> space_tab;
+  DevBuf svc_pool;
 };
 
 namespace {
@@ -254,11 +266,11 @@ void prof_collect_graph(stmg_ctx* c) {
   }
 }
 
-void build_level_tables(Level& L) {
-  const i64 n1 = L.spec.n1();
-  const double h = L.spec.h, N = double(n1 + 1);
+// Sine tables of one grid: mval | kval | rfac (n1 each), then `extra` zeros.
+std::vector<double> sine_tables(i64 n1, double h, size_t extra) {
+  const double N = double(n1 + 1);
   const i64 G = (n1 + 1) / 2;
-  std::vector<double> tab(3 * n1 + 2 * stmg::kMaxNL, 0.0);
+  std::vector<double> tab(3 * n1 + extra, 0.0);
   const long double pi = 3.141592653589793238462643383279502884L;
   for (i64 q = 0; q < n1; ++q) {
     const long double th = pi * (long double)(q + 1) / (long double)N;
@@ -270,6 +282,14 @@ void build_level_tables(Level& L) {
     const double f = 2.0 * c2 * c2 / std::sqrt(2.0);  // (1 + cos)/sqrt(2)
     tab[2 * n1 + q] = q < G - 1 ? f : (q == G - 1 ? 0.0 : -f);
   }
+  return tab;
+}
+
+void build_level_tables(Level& L) {
+  const i64 n1 = L.spec.n1();
+  const double h = L.spec.h, N = double(n1 + 1);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  std::vector<double> tab = sine_tables(n1, h, 2 * stmg::kMaxNL);
   {  // N_tau = a b^T with a_k = psi_k(0), b_l = psi_l(tau) (Legendre: psi_0 = 1)
     const stmg::DGBlock dg0 = stmg::dg_block(L.spec.p_t, L.spec.tau);
     const int nl = L.spec.p_t + 1;
@@ -324,14 +344,17 @@ void ensure(DevBuf& b, i64 n, i64 halo = 0) {
 }
 
 // ----------------------------------------------------- physical operators
+// out = DST(in) over all axes.  accumulate: out += alpha DST(in); then `in`
+// is overwritten (it holds the partial transforms of the first dim-1 axes).
 void dst_all(stmg_ctx* c, Level& L, const double* in, double* out, bool accumulate = false,
              double alpha = 1.0) {
   const int dim = L.spec.dim;
   prof_begin(c, 2);
+  double* mid = accumulate ? const_cast<double*>(in) : out;
   for (int a = 0; a < dim; ++a) {
     const bool last = a + 1 == dim;
-    CK(stmg::launch_dst_axis(L.view, a, a == 0 ? in : out, out, last && accumulate, alpha,
-                             L.d_twiddle, c->stream));
+    CK(stmg::launch_dst_axis(L.view, a, a == 0 ? in : mid, last ? out : mid, last && accumulate,
+                             alpha, L.d_twiddle, c->stream));
     count(c);
   }
   prof_end(c, 2, 16.0 * double(L.view.size()) * dim);
@@ -368,7 +391,16 @@ void residual(stmg_ctx* c, Level& L, const double* u, const double* f, double* r
   count(c);
 }
 
-void smooth_phys(stmg_ctx* c, int level, double* u, const double* f, double omega, int nu) {
+struct Spatial;
+void svc_smooth_phys(stmg_ctx* c, int level, double* u, const double* f, double omega, int nu,
+                     const Spatial& sp);
+
+void smooth_phys(stmg_ctx* c, int level, double* u, const double* f, double omega, int nu,
+                 const Spatial* inexact = nullptr) {
+  if (inexact) {
+    svc_smooth_phys(c, level, u, f, omega, nu, *inexact);
+    return;
+  }
   Level& L = c->levels[level];
   ensure(L.R, L.view.size());
   for (int s = 0; s < nu; ++s) {
@@ -395,13 +427,16 @@ void fwdsub_phys(stmg_ctx* c, Level& L, const double* f, double* u) {
   dst_all(c, L, u, u);
 }
 
+const Spatial* phys_spatial(const stmg_cycle_config& cfg);
+
 void phys_cycle(stmg_ctx* c, int level, double* u, const double* f, const stmg_cycle_config& cfg) {
   Level& L = c->levels[level];
   if (level + 1 == int(c->levels.size())) {
     fwdsub_phys(c, L, f, u);
     return;
   }
-  smooth_phys(c, level, u, f, cfg.omega_t, cfg.nu1);
+  const Spatial* ix = phys_spatial(cfg);
+  smooth_phys(c, level, u, f, cfg.omega_t, cfg.nu1, ix);
   ensure(L.R, L.view.size());
   residual(c, L, u, f, L.R.base);
   Level& C = c->levels[level + 1];
@@ -417,7 +452,7 @@ void phys_cycle(stmg_ctx* c, int level, double* u, const double* f, const stmg_c
   count(c);
   CK(stmg::launch_axpy(u, L.CORR.base, 1.0, L.view.size(), c->stream));
   count(c);
-  smooth_phys(c, level, u, f, cfg.omega_t, cfg.nu2);
+  smooth_phys(c, level, u, f, cfg.omega_t, cfg.nu2, ix);
 }
 
 double norm_phys(stmg_ctx* c, Level& L, const double* v) {
@@ -545,8 +580,15 @@ stmg::ModalArgs modal_args(const Level& L, const Level* C, double omega, bool gr
 // Enqueue one gamma-cycle from `level` on the spectral buffers.  zero_guess:
 // the level's iterate is 0 (coarse levels).  want_resid: compute the residual
 // norm partials of the finest result (returns their count via *np).
+void inexact_cycle(stmg_ctx* c, int level, bool zero_guess, const stmg_cycle_config& cfg,
+                   bool want_resid, i64* np);
+
 void spectral_cycle(stmg_ctx* c, int level, bool zero_guess, const stmg_cycle_config& cfg,
                     bool want_resid, i64* np) {
+  if (cfg.block_solver == STMG_BLOCK_VCYCLE) {
+    inexact_cycle(c, level, zero_guess, cfg, want_resid, np);
+    return;
+  }
   Level& L = c->levels[level];
   int& cur = c->cur[level];
   if (zero_guess) cur = 0;
@@ -621,11 +663,228 @@ void spectral_cycle(stmg_ctx* c, int level, bool zero_guess, const stmg_cycle_co
   }
 }
 
+// ------------------------------------------- inexact block solver (f2)
+// SpatialVCycleSolver (smoother.cpp:8-78) on every time step of a level, in
+// the sine basis (kernels: stmg_spatial.cu).  Sub-level sigma = 0..s of a
+// level with space level s is the grid of level s - sigma; the workspace
+// holds X_sigma, B_sigma for every sub-level.
+struct Spatial {
+  double omega_x = 2.0 / 3.0;
+  int nu1_x = 2, nu2_x = 2, gamma_x = 1;
+};
+
+Spatial spatial_of(const stmg_cycle_config& c) { return {c.omega_x, c.nu1_x, c.nu2_x, c.gamma_x}; }
+Spatial spatial_of(const stmg_smoother_config& c) {
+  return {c.omega_x, c.nu1_x, c.nu2_x, c.gamma_x};
+}
+
+const double* space_tables(stmg_ctx* c, int g) {
+  auto it = c->space_tab.find(g);
+  if (it != c->space_tab.end()) return it->second;
+  const i64 n1 = (i64(1) << (g + 1)) - 1;
+  const std::vector<double> tab = sine_tables(n1, std::ldexp(1.0, -(g + 1)), 0);
+  double* d = nullptr;
+  CK(cudaMalloc(&d, tab.size() * sizeof(double)));
+  CK(cudaMemcpy(d, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+  c->space_tab[g] = d;
+  return d;
+}
+
+// Kronecker diagonals of M_h and K_h on grid level g (uniform grid: one value
+// each, smoother.cpp:16-20): M(0,0) = md^dim, K(0,0) = dim kd md^(dim-1).
+void space_diag(int dim, int g, double& md, double& kd) {
+  const double h = std::ldexp(1.0, -(g + 1));
+  const double m1 = 4.0 * h / 6.0, k1 = 2.0 / h;
+  md = std::pow(m1, dim);
+  kd = dim * k1 * std::pow(m1, dim - 1);
+}
+
+stmg::SvcArgs svc_args(stmg_ctx* c, int dim, int g, const Spatial& sp, int nu) {
+  stmg::SvcArgs a;
+  const i64 n1 = (i64(1) << (g + 1)) - 1;
+  const double* tab = space_tables(c, g);
+  a.sp.dim = dim;
+  a.sp.n1 = n1;
+  a.sp.nx = 1;
+  for (int d = 0; d < dim; ++d) a.sp.nx *= n1;
+  a.sp.h = std::ldexp(1.0, -(g + 1));
+  a.sp.mval = tab;
+  a.sp.kval = tab + n1;
+  a.sp.rfac = tab + 2 * n1;
+  a.n1c = g > 0 ? (i64(1) << g) - 1 : 1;
+  space_diag(dim, g, a.md, a.kd);
+  space_diag(dim, 0, a.mc, a.kc);  // the 1-node grid: its block is diagonal
+  a.omega_x = sp.omega_x;
+  a.nu = nu;
+  return a;
+}
+
+// Workspace doubles of level L's sub-levels (X and B each).
+i64 svc_sub_size(const Level& L, int sigma) {
+  const int g = L.spec.space_level - sigma;
+  i64 nx = 1;
+  for (int d = 0; d < L.spec.dim; ++d) nx *= (i64(1) << (g + 1)) - 1;
+  return L.spec.n_t * (L.spec.p_t + 1) * nx;
+}
+
+struct SvcBufs {
+  std::vector<double*> X, B;
+};
+
+SvcBufs svc_bufs(stmg_ctx* c, const Level& L) {
+  if (!c->svc_pool.base) {  // once, for the largest level (never grows: graphs bake pointers)
+    i64 need = 0;
+    for (const Level& K : c->levels) {
+      i64 t = 0;
+      for (int sg = 0; sg <= K.spec.space_level; ++sg) t += 2 * svc_sub_size(K, sg);
+      need = std::max(need, t);
+    }
+    c->svc_pool.alloc(need, 0);
+  }
+  SvcBufs b;
+  double* p = c->svc_pool.base;
+  for (int sg = 0; sg <= L.spec.space_level; ++sg) {
+    const i64 n = svc_sub_size(L, sg);
+    b.X.push_back(p);
+    b.B.push_back(p + n);
+    p += 2 * n;
+  }
+  require(p - c->svc_pool.base <= c->svc_pool.count, "internal: spatial workspace too small");
+  return b;
+}
+
+// Workspace and sine tables of every grid, outside any graph capture.
+void ensure_svc(stmg_ctx* c, const stmg_cycle_config& cfg) {
+  if (cfg.block_solver != STMG_BLOCK_VCYCLE) return;
+  svc_bufs(c, c->levels[0]);
+  for (int g = 0; g <= c->levels[0].spec.space_level; ++g) space_tables(c, g);
+}
+
+// One spatial cycle per time step of level L.  f != null: B_0 = f - L u (u =
+// u_in, sine basis); else B_0 is set by the caller.  zero0: X_0 starts at 0
+// (else the caller set it).  u_final != null: u_final += omega_t x, else the
+// result is left in X_0.
+void svc_run(stmg_ctx* c, Level& L, const Spatial& sp, const double* f, const double* u_in,
+             double* u_final, bool zero0, double omega_t) {
+  const SvcBufs w = svc_bufs(c, L);
+  const int s = L.spec.space_level, dim = L.spec.dim;
+  if (s == 0) {
+    const stmg::SvcArgs a = svc_args(c, dim, 0, sp, 0);
+    CK(stmg::launch_svc_direct(L.view, a, f != nullptr, f, u_in, w.B[0], w.X[0], u_final, omega_t,
+                               c->stream));
+    count(c);
+    return;
+  }
+  std::function<void(int, bool)> rec = [&](int sg, bool zero) {
+    const int g = s - sg;
+    const bool to_c = g - 1 == 0;
+    const stmg::SvcArgs down = svc_args(c, dim, g, sp, sp.nu1_x);
+    CK(stmg::launch_svc_down(L.view, down, sg == 0 && f, zero, to_c, f, u_in, w.B[sg], w.X[sg],
+                             to_c ? w.X[sg + 1] : w.B[sg + 1], c->stream));
+    count(c);
+    if (!to_c)
+      for (int k = 0; k < sp.gamma_x; ++k) rec(sg + 1, k == 0);
+    const stmg::SvcArgs up = svc_args(c, dim, g, sp, sp.nu2_x);
+    CK(stmg::launch_svc_up(L.view, up, w.X[sg + 1], w.B[sg], w.X[sg], sg == 0 ? u_final : nullptr,
+                           omega_t, c->stream));
+    count(c);
+  };
+  rec(0, zero0);
+}
+
+// block_jacobi_step with spatial-V-cycle blocks on the spectral iterate.
+void svc_smooth_spectral(stmg_ctx* c, Level& L, const Spatial& sp, const double* f, double* u,
+                         double omega_t, int nu) {
+  for (int k = 0; k < nu; ++k) svc_run(c, L, sp, f, u, u, true, omega_t);
+}
+
+// mg_cycle (mg.cpp:96-132) on the sine coefficients with inexact block
+// solves: smoothing by svc_smooth_spectral; residual + restriction and
+// prolongation + correction by the fused level kernels with omega = 0
+// (their smoothing sweep is then the identity).
+void inexact_cycle(stmg_ctx* c, int level, bool zero_guess, const stmg_cycle_config& cfg,
+                   bool want_resid, i64* np) {
+  Level& L = c->levels[level];
+  int& cur = c->cur[level];
+  const Spatial sp = spatial_of(cfg);
+  if (zero_guess) {
+    cur = 0;
+    CK(cudaMemsetAsync(L.U[0].base, 0, size_t(L.view.size()) * sizeof(double), c->stream));
+  }
+  if (level + 1 == int(c->levels.size())) {
+    CK(stmg::launch_modal_fwdsub(L.view, L.F.base, L.U[cur].base, c->stream));
+    count(c);
+    if (want_resid) {
+      stmg::ModalArgs a = modal_args(L, nullptr, cfg.omega_t, false);
+      CK(stmg::launch_resnorm(L.view, a, L.U[cur].base, L.F.base, c->partials.base, c->stream));
+      count(c);
+      *np = a.n_partials;
+    }
+    return;
+  }
+  Level& C = c->levels[level + 1];
+  svc_smooth_spectral(c, L, sp, L.F.base, L.U[cur].base, cfg.omega_t, std::max(cfg.nu1, 0));
+  {
+    stmg::ModalArgs a = modal_args(L, &C, 0.0, true);
+    CK(stmg::launch_down(L.view, a, false, L.F.base, L.U[cur].base, L.U[1 - cur].base, C.F.base,
+                         c->stream));
+    count(c);
+    cur ^= 1;
+  }
+  for (int g = 0; g < std::max(cfg.gamma, 1); ++g)
+    inexact_cycle(c, level + 1, g == 0, cfg, false, nullptr);
+  {
+    stmg::ModalArgs a = modal_args(L, &C, 0.0, true);
+    CK(stmg::launch_up(L.view, a, C.U[c->cur[level + 1]].base, L.U[cur].base, L.F.base,
+                       L.U[1 - cur].base, nullptr, c->stream));
+    count(c);
+    cur ^= 1;
+  }
+  svc_smooth_spectral(c, L, sp, L.F.base, L.U[cur].base, cfg.omega_t, std::max(cfg.nu2, 0));
+  if (want_resid) {
+    stmg::ModalArgs a = modal_args(L, &C, cfg.omega_t, false);
+    CK(stmg::launch_resnorm(L.view, a, L.U[cur].base, L.F.base, c->partials.base, c->stream));
+    count(c);
+    *np = a.n_partials;
+  }
+}
+
+void check_spatial(double omega_x, int nu1_x, int nu2_x, int gamma_x) {
+  require(nu1_x >= 0 && nu2_x >= 0, "spatial smoothing step counts must be >= 0");
+  require(gamma_x >= 1, "gamma_x must be >= 1");
+  require(std::isfinite(omega_x), "omega_x must be finite");
+}
+
+// Physical path: residual -> DST -> spatial cycles -> inverse DST, u += w x.
+void svc_smooth_phys(stmg_ctx* c, int level, double* u, const double* f, double omega, int nu,
+                     const Spatial& sp) {
+  Level& L = c->levels[level];
+  ensure(L.R, L.view.size());
+  for (int k = 0; k < nu; ++k) {
+    residual(c, L, u, f, L.R.base);
+    const SvcBufs w = svc_bufs(c, L);
+    dst_all(c, L, L.R.base, w.B[0]);
+    svc_run(c, L, sp, nullptr, nullptr, nullptr, true, omega);
+    dst_all(c, L, w.X[0], u, true, omega);
+  }
+}
+
+const Spatial* phys_spatial(const stmg_cycle_config& cfg) {
+  static thread_local Spatial sp;
+  if (cfg.block_solver != STMG_BLOCK_VCYCLE) return nullptr;
+  sp = spatial_of(cfg);
+  return &sp;
+}
+
 void check_cfg(const stmg_cycle_config* cfg) {
   require(cfg != nullptr, "null cycle config");
   require(cfg->nu1 >= 0 && cfg->nu2 >= 0, "smoothing step counts must be >= 0");
   require(cfg->gamma >= 1, "gamma must be >= 1");
   require(cfg->path == STMG_PATH_SPECTRAL || cfg->path == STMG_PATH_PHYSICAL, "unknown cycle path");
+  require(cfg->block_solver == STMG_BLOCK_EXACT || cfg->block_solver == STMG_BLOCK_VCYCLE,
+          "block_solver must be 'exact' or 'vcycle'");
+  if (cfg->block_solver == STMG_BLOCK_VCYCLE)
+    check_spatial(cfg->omega_x, cfg->nu1_x, cfg->nu2_x, cfg->gamma_x);
 }
 
 void ensure_hist(stmg_ctx* c, int n) {
@@ -654,7 +913,10 @@ double spectral_resnorm(stmg_ctx* c, int level) {
 // One full V-cycle from level 0 + residual norm into d_norm/h_norm, as a
 // captured graph (replayed every iteration).
 stmg_ctx::GraphEntry& cycle_graph(stmg_ctx* c, const stmg_cycle_config& cfg) {
-  stmg_ctx::GraphKey key{cfg.nu1, cfg.nu2, cfg.gamma, c->cur[0], cfg.omega_t};
+  const bool ix = cfg.block_solver == STMG_BLOCK_VCYCLE;
+  stmg_ctx::GraphKey key{cfg.nu1,          cfg.nu2,           cfg.gamma,         c->cur[0],
+                         cfg.omega_t,      cfg.block_solver,  ix ? cfg.nu1_x : 0, ix ? cfg.nu2_x : 0,
+                         ix ? cfg.gamma_x : 0, ix ? cfg.omega_x : 0.0};
   auto it = c->graphs.find(key);
   if (it != c->graphs.end()) return it->second;
   const int cur0 = c->cur[0];
@@ -737,10 +999,16 @@ cudaGraphExec_t device_loop(stmg_ctx* c, const std::string& key, double eps, int
 
 std::string loop_key(const char* kind, const stmg_cycle_config& cfg, int cur0, double eps,
                      int max_iter) {
-  char b[160];
+  char b[256];
   std::snprintf(b, sizeof(b), "%s/%d/%d/%d/%.17g/%d/%.17g/%d", kind, cfg.nu1, cfg.nu2, cfg.gamma,
                 cfg.omega_t, cur0, eps, max_iter);
-  return b;
+  std::string k(b);
+  if (cfg.block_solver == STMG_BLOCK_VCYCLE) {
+    std::snprintf(b, sizeof(b), "/vc/%d/%d/%d/%.17g", cfg.nu1_x, cfg.nu2_x, cfg.gamma_x,
+                  cfg.omega_x);
+    k += b;
+  }
+  return k;
 }
 
 // Run the remaining cycles on the device; fills r and history from the device.
@@ -769,7 +1037,8 @@ void run_device_loop(stmg_ctx* c, cudaGraphExec_t exec, int max_iter, double* hi
 // norm, stop test (+ swap of the level-0 buffers); suffix: up(0) of the last
 // cycle recomputed from its inputs (still intact) to produce the result.
 bool fused_eligible(const stmg_ctx* c, const stmg_cycle_config& cfg) {
-  return c->use_fused && cfg.path == STMG_PATH_SPECTRAL && cfg.nu1 == 1 && cfg.nu2 == 1 &&
+  return c->use_fused && cfg.path == STMG_PATH_SPECTRAL && cfg.block_solver == STMG_BLOCK_EXACT &&
+         cfg.nu1 == 1 && cfg.nu2 == 1 &&
          cfg.gamma == 1 && c->levels.size() >= 2 && c->levels[0].spec.coarsen != 0;
 }
 
@@ -930,6 +1199,7 @@ void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config
   } else {
     ensure_spectral(c, 0);
     ensure_tail(c);
+    ensure_svc(c, cfg);
     c->cur[0] = 0;
     // a zero initial guess (the usual case) needs no transform
     CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
@@ -1511,6 +1781,8 @@ void solve_sharded(stmg_ctx* c, const double* f, double* u, const stmg_cycle_con
   require(f != nullptr && u != nullptr, "null vector");
   require(max_iter >= 0, "max_iter must be >= 0");
   require(cfg.path == STMG_PATH_SPECTRAL, "sharded solves run on the spectral path");
+  require(cfg.block_solver == STMG_BLOCK_EXACT,
+          "sharded solves use exact block solves (block_solver = 'exact')");
   require(cfg.gamma == 1 && cfg.nu1 >= 1 && cfg.nu2 >= 1,
           "sharded solves support V(nu1, nu2) cycles with nu1, nu2 >= 1");
   build_shards(c);
@@ -1770,6 +2042,8 @@ int stmg_destroy(stmg_ctx* c) {
     }
     c->partials.release();
     c->partials_phys.release();
+    c->svc_pool.release();
+    for (auto& kv : c->space_tab) cudaFree(kv.second);
     c->user_f.release();
     c->user_u.release();
     for (auto& s : c->prof) {
@@ -1951,6 +2225,55 @@ int stmg_smooth(stmg_ctx* c, int level, double* u, const double* f, double omega
     require(u && f, "null vector");
     require(nu >= 0, "nu must be >= 0");
     smooth_phys(c, level, u, f, omega_t, nu);
+  });
+}
+
+int stmg_cycle_config_init(stmg_cycle_config* cfg) {
+  return guard([&] {
+    require(cfg != nullptr, "null cycle config");
+    *cfg = stmg_cycle_config{2, 2, 1, 0.5, STMG_PATH_SPECTRAL, STMG_BLOCK_EXACT, 2.0 / 3.0, 2, 2, 1};
+  });
+}
+
+int stmg_smoother_config_init(stmg_smoother_config* cfg) {
+  return guard([&] {
+    require(cfg != nullptr, "null smoother config");
+    *cfg = stmg_smoother_config{0.5, 1, STMG_BLOCK_EXACT, 2.0 / 3.0, 2, 2, 1};
+  });
+}
+
+int stmg_block_jacobi_step(stmg_ctx* c, int level, double* u, const double* f,
+                           const stmg_smoother_config* cfg) {
+  return guard([&] {
+    lev(c, level);
+    require(cfg != nullptr, "null smoother config");
+    require(u && f, "null vector");
+    require(cfg->nu >= 0, "nu must be >= 0");
+    require(cfg->block_solver == STMG_BLOCK_EXACT || cfg->block_solver == STMG_BLOCK_VCYCLE,
+            "block_solver must be 'exact' or 'vcycle'");
+    if (cfg->block_solver == STMG_BLOCK_VCYCLE) {
+      check_spatial(cfg->omega_x, cfg->nu1_x, cfg->nu2_x, cfg->gamma_x);
+      const Spatial sp = spatial_of(*cfg);
+      smooth_phys(c, level, u, f, cfg->omega_t, cfg->nu, &sp);
+    } else {
+      smooth_phys(c, level, u, f, cfg->omega_t, cfg->nu);
+    }
+  });
+}
+
+int stmg_spatial_vcycle(stmg_ctx* c, int level, const double* b, const double* x0, double* x,
+                        const stmg_smoother_config* cfg) {
+  return guard([&] {
+    Level& L = lev(c, level);
+    require(cfg != nullptr, "null smoother config");
+    require(b && x, "null vector");
+    check_spatial(cfg->omega_x, cfg->nu1_x, cfg->nu2_x, cfg->gamma_x);
+    const Spatial sp = spatial_of(*cfg);
+    const SvcBufs w = svc_bufs(c, L);
+    dst_all(c, L, b, w.B[0]);
+    if (x0) dst_all(c, L, x0, w.X[0]);
+    svc_run(c, L, sp, nullptr, nullptr, nullptr, x0 == nullptr, 1.0);
+    dst_all(c, L, w.X[0], x);
   });
 }
 
@@ -2320,8 +2643,15 @@ int stmg_measure_convergence_factor(const stmg_rho_problem* pr, const stmg_cycle
       if (rk <= floor) break;
     }
     m.measured_rho = rho;
-    m.predicted_rho = stmg::lfa::twogrid_factor(pr->p_t, pr->mu, cfg->omega_t, cfg->nu1, cfg->nu2,
-                                                pr->mode, n_theta_x, n_theta_t);
+    // exact blocks: lfa::twogrid_factor (bench.cpp:142-143); inexact blocks
+    // (an extension of the reference harness): the inexact-block symbol
+    m.predicted_rho =
+        cfg->block_solver == STMG_BLOCK_VCYCLE
+            ? stmg::lfa::twogrid_factor_inexact(pr->p_t, pr->mu, cfg->omega_t, cfg->nu1, cfg->nu2,
+                                                cfg->omega_x, cfg->nu1_x, cfg->nu2_x, pr->mode,
+                                                n_theta_x, n_theta_t)
+            : stmg::lfa::twogrid_factor(pr->p_t, pr->mu, cfg->omega_t, cfg->nu1, cfg->nu2,
+                                        pr->mode, n_theta_x, n_theta_t);
     *out = m;
   });
   if (c) {

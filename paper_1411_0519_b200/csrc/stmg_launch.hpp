@@ -130,6 +130,32 @@ cudaError_t build_tail_table(const TailSpec* levels, int nlev, void** dev_table,
                              void** host_table);
 cudaError_t launch_tail(int dim, int nl, const void* dev_table, const void* host_table, int nlev,
                         double omega, size_t smem_bytes, cudaStream_t st);
+// ---- inexact block solver: spatial V-cycle in the sine basis --------------
+// (SpatialVCycleSolver, smoother.cpp:8-78; kernels in stmg_spatial.cu.)  The
+// LevelView supplies n_t and the DG blocks of the space-time level; SvcArgs
+// one spatial sub-level of its cycle.
+struct SvcArgs {
+  SpaceConsts sp;          // the sub-level's grid and sine tables
+  int64_t n1c = 1;         // nodes per axis of the next (coarser) sub-level
+  double md = 0.0, kd = 0.0;  // diagonals of M_h, K_h: Jacobi block D = md K + kd M
+  double mc = 0.0, kc = 0.0;  // 1-node grid eigenvalues (its direct solve)
+  double omega_x = 2.0 / 3.0;
+  int nu = 2;              // sweeps (nu1_x down, nu2_x up)
+};
+// first: B = f - L u (space-time residual of u in the sine basis) instead of
+// reading B.  zero: start from x = 0.  to_coarsest: C receives the next
+// sub-level's direct solution (the 1-node grid) instead of its rhs.
+cudaError_t launch_svc_down(const LevelView& L, const SvcArgs& a, bool first, bool zero,
+                            bool to_coarsest, const double* f, const double* u, double* B,
+                            double* X, double* C, cudaStream_t st);
+// X += P E, nu sweeps; u != null: u += omega_t x instead of writing X.
+cudaError_t launch_svc_up(const LevelView& L, const SvcArgs& a, const double* E, const double* B,
+                          double* X, double* u, double omega_t, cudaStream_t st);
+// Level grid of one node: x = A^-1 b; u_final != null: u_final += omega_t x.
+cudaError_t launch_svc_direct(const LevelView& L, const SvcArgs& a, bool first, const double* f,
+                              const double* u, double* B, double* X, double* u_final,
+                              double omega_t, cudaStream_t st);
+
 // flag[0] = 1 if any v[i] != 0 (flag must be zeroed before).
 cudaError_t launch_nonzero(const double* v, int64_t n, int* flag, cudaStream_t st);
 

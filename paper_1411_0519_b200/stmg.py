@@ -67,12 +67,48 @@ class CycleConfig:
     gamma: int = 1
     omega_t: float = 0.5
     path: str = "spectral"  # or "physical"
+    block_solver: str = "exact"  # or "vcycle" (BlockSolverKind::spatial_vcycle)
+    omega_x: float = 2.0 / 3.0
+    nu1_x: int = 2
+    nu2_x: int = 2
+    gamma_x: int = 1
 
     def c(self) -> A.CycleConfig:
         if self.path not in ("spectral", "physical"):
             raise ValueError("unknown cycle path")
         return A.CycleConfig(self.nu1, self.nu2, self.gamma, self.omega_t,
-                             A.PATH_SPECTRAL if self.path == "spectral" else A.PATH_PHYSICAL)
+                             A.PATH_SPECTRAL if self.path == "spectral" else A.PATH_PHYSICAL,
+                             block_solver_kind(self.block_solver), self.omega_x, self.nu1_x,
+                             self.nu2_x, self.gamma_x)
+
+
+def block_solver_kind(name) -> int:
+    """'exact' -> 0, 'vcycle' -> 1 (config.cpp:64-70 spellings)."""
+    if name in ("exact", 0):
+        return BLOCK_EXACT
+    if name in ("vcycle", "spatial_vcycle", 1):
+        return BLOCK_VCYCLE
+    raise ValueError("block_solver must be 'exact' or 'vcycle'")
+
+
+BLOCK_EXACT = 0
+BLOCK_VCYCLE = 1
+
+
+@dataclass
+class SmootherConfig:
+    """SmootherConfig (smoother.hpp:15-24)."""
+    omega_t: float = 0.5
+    nu: int = 1
+    block_solver: str = "exact"
+    omega_x: float = 2.0 / 3.0
+    nu1_x: int = 2
+    nu2_x: int = 2
+    gamma_x: int = 1
+
+    def c(self) -> A.SmootherConfig:
+        return A.SmootherConfig(self.omega_t, self.nu, block_solver_kind(self.block_solver),
+                                self.omega_x, self.nu1_x, self.nu2_x, self.gamma_x)
 
 
 @dataclass
@@ -225,9 +261,25 @@ class Hierarchy:
         return x
 
     def block_jacobi_step(self, level: int, u: BlockVector, f: BlockVector,
-                          omega_t: float = 0.5, nu: int = 1) -> BlockVector:
-        check(A.lib().stmg_smooth(self._ctx, level, u.ptr, f.ptr, omega_t, nu))
+                          omega_t: float = 0.5, nu: int = 1,
+                          cfg: Optional[SmootherConfig] = None) -> BlockVector:
+        """block_jacobi_step (smoother.cpp:96-106); cfg selects the block solver."""
+        if cfg is None:
+            check(A.lib().stmg_smooth(self._ctx, level, u.ptr, f.ptr, omega_t, nu))
+        else:
+            sc = cfg.c()
+            check(A.lib().stmg_block_jacobi_step(self._ctx, level, u.ptr, f.ptr, C.byref(sc)))
         return u
+
+    def spatial_vcycle(self, level: int, b: BlockVector, x0: Optional[BlockVector] = None,
+                       x: Optional[BlockVector] = None,
+                       cfg: Optional[SmootherConfig] = None) -> BlockVector:
+        """SpatialVCycleSolver::cycle on every time step (smoother.cpp:71-78)."""
+        x = x or self.vector(level)
+        sc = (cfg or SmootherConfig(block_solver="vcycle")).c()
+        check(A.lib().stmg_spatial_vcycle(self._ctx, level, b.ptr, x0.ptr if x0 else None,
+                                          x.ptr, C.byref(sc)))
+        return x
 
     def restrict(self, level: int, fine: BlockVector, mode: int = 0) -> BlockVector:
         out = self.coarse_vector(level, mode)

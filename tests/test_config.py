@@ -61,8 +61,10 @@ def test_mapping_to_library_params(Cfg):
     assert hp["policy"] == 1 and hp["space_level"] == 4 and hp["time_level"] == 5
     cc = Cfg.cycle_config(c)
     assert (cc.nu1, cc.nu2, cc.gamma, cc.omega_t) == (2, 1, 2, 0.5)
-    with pytest.raises(ValueError, match="vcycle"):
-        Cfg.hierarchy_params(Cfg.parse_config(json.dumps(dict(GOOD, block_solver="vcycle"))))
+    ci = Cfg.cycle_config(Cfg.parse_config(json.dumps(dict(GOOD, block_solver="vcycle",
+                                                          omega_x=0.6, nu1_x=1, nu2_x=3))))
+    assert (ci.block_solver, ci.omega_x, ci.nu1_x, ci.nu2_x) == ("vcycle", 0.6, 1, 3)
+    assert ci.c().block_solver == 1 and cc.c().block_solver == 0
 
 
 def test_reports_and_csv(Cfg):
@@ -85,16 +87,19 @@ def test_reports_and_csv(Cfg):
 
 
 @pytest.mark.gpu
-def test_solve_from_config_matches_oracle(Cfg):
+@pytest.mark.parametrize("solver", ["exact", "vcycle"])
+def test_solve_from_config_matches_oracle(Cfg, solver):
     from oracle import oracle as O
     from paper_1411_0519_b200 import stmg
-    c = Cfg.parse_config(json.dumps(dict(GOOD, dim=1, space_levels=5, time_levels=6)))
+    c = Cfg.parse_config(json.dumps(dict(GOOD, dim=1, space_levels=5, time_levels=6,
+                                         block_solver=solver)))
     h = stmg.Hierarchy(**Cfg.hierarchy_params(c))
     o = O.Hierarchy(c.p_t, c.dim, c.space_levels, c.time_levels, t_final=c.t_final)
     f = O.fill_uniform(o.levels[0].size, c.seed, 0)
     u = h.vector(0)
     r = h.solve(h.upload(f), u, Cfg.cycle_config(c), c.eps_mg, c.max_iter)
-    u_o, rep_o = o.solve(f, nu1=c.nu1, nu2=c.nu2, eps=c.eps_mg)
+    u_o, rep_o = o.solve(f, nu1=c.nu1, nu2=c.nu2, eps=c.eps_mg, block_solver=solver,
+                         omega_x=c.omega_x, nu1_x=c.nu1_x, nu2_x=c.nu2_x)
     assert r.iterations == rep_o["iterations"]
     assert np.abs(u.numpy() - u_o).max() <= 1e-10 * np.abs(u_o).max()
     j = json.loads(Cfg.solve_report_json(c, r))

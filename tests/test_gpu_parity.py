@@ -258,6 +258,9 @@ def test_cpp_shim_solves_c1(S):
     o = O.Hierarchy(1, 1, 5, 6)
     _, rep_o = o.solve(O.make_inputs(o, 42))
     assert rep["iterations"] == rep_o["iterations"]
+    _, rep_i = o.solve(O.make_inputs(o, 42), block_solver="vcycle")
+    assert rep["inexact_iterations"] == rep_i["iterations"]
+    assert rep["vcycle_size"] == o.levels[0].size
 
 
 @pytest.mark.parametrize("case", [
