@@ -186,6 +186,11 @@ struct stmg_ctx {
   int* d_par = nullptr;
   std::map<std::string, cudaGraphExec_t> fused_bodies;  // per-cycle graphs (profiling)
   int* d_iter = nullptr;
+  unsigned* d_counter = nullptr;  // last-CTA ticket of the fused k_updown epilogue
+  // norm + stop test inside k_updown's last CTA (fused schedule).  Measured
+  // neutral on B200 (PDL already hides the two tiny kernels): off by default.
+  bool fuse_final = false;
+  cudaGraphConditionalHandle loop_h = 0;  // handle of the while node being captured
   double* d_r0 = nullptr;
   bool use_device_loop = true;
   bool use_fused = true;  // fused level-0 schedule for V(1,1) solves
@@ -193,6 +198,9 @@ struct stmg_ctx {
   // workspace (X, B per sub-level) shared by all levels, sized for level 0
   std::map<int, double*> space_tab;
   DevBuf svc_pool;
+  // coarse operator: the tail's V(1,1) map F -> U as a dense matrix per omega_t
+  std::map<double, double*> cop;
+  bool use_cop = true;
 };
 
 namespace {
@@ -568,6 +576,64 @@ void ensure_tail(stmg_ctx* c) {
   c->tail_smem = size_t(bytes + tab);
 }
 
+// ---- coarse operator ------------------------------------------------------
+// The tail (levels >= tail_start, V(1,1), zero initial guess) is a fixed
+// linear map F -> U of the tail's first level.  When that level has at most
+// kCopMax unknowns it is precomputed once per omega_t (column i = the tail
+// kernel applied to e_i) and applied as one multi-CTA GEMV, which replaces the
+// tail's ~20 dependent single-CTA phases.  Exact in exact arithmetic;
+// rounding-level differences only (tests: STMG_COARSE_OP=0 vs 1).
+constexpr i64 kCopMax = 3200;
+
+i64 cop_size(const stmg_ctx* c) {
+  if (c->tail_start <= 0) return 0;
+  return c->levels[c->tail_start].view.size();
+}
+
+bool v11_exact(const stmg_cycle_config& cfg) {
+  return cfg.path == STMG_PATH_SPECTRAL && cfg.block_solver == STMG_BLOCK_EXACT && cfg.nu1 == 1 &&
+         cfg.nu2 == 1 && cfg.gamma == 1;
+}
+
+void launch_tail_kernel(stmg_ctx* c, double omega) {
+  CK(stmg::launch_tail(c->dim, c->p_t + 1, c->tail_table, c->tail_host,
+                       int(c->levels.size()) - c->tail_start, omega, c->tail_smem, c->stream));
+  count(c);
+}
+
+// Build the operator for omega (outside any graph capture).
+void ensure_cop(stmg_ctx* c, double omega) {
+  if (!c->use_cop || !c->tail_table || c->cop.count(omega)) return;
+  const i64 n = cop_size(c);
+  if (n <= 0 || n > kCopMax) return;
+  Level& T = c->levels[c->tail_start];
+  double* B = nullptr;
+  CK(cudaMalloc(&B, size_t(n * n) * sizeof(double)));
+  const double one = 1.0;
+  for (i64 i = 0; i < n; ++i) {
+    CK(cudaMemsetAsync(T.F.base, 0, size_t(n) * sizeof(double), c->stream));
+    CK(cudaMemcpyAsync(T.F.base + i, &one, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    launch_tail_kernel(c, omega);
+    CK(cudaMemcpy2DAsync(B + i, size_t(n) * sizeof(double), T.U[0].base, sizeof(double),
+                         sizeof(double), size_t(n), cudaMemcpyDeviceToDevice, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  c->cop[omega] = B;
+}
+
+// The tail of a V(1,1) cycle: the coarse operator if built, else the kernel.
+void run_tail(stmg_ctx* c, double omega) {
+  auto it = c->cop.find(omega);
+  if (it != c->cop.end()) {
+    Level& T = c->levels[c->tail_start];
+    CK(stmg::launch_cop_gemv(it->second, T.F.base, T.U[0].base, int(cop_size(c)), c->stream));
+    count(c);
+  } else {
+    launch_tail_kernel(c, omega);
+  }
+  for (int l = c->tail_start; l < int(c->levels.size()); ++l) c->cur[l] = 0;
+}
+
 stmg::ModalArgs modal_args(const Level& L, const Level* C, double omega, bool grouped) {
   stmg::ModalArgs a;
   a.omega = omega;
@@ -627,11 +693,7 @@ void spectral_cycle(stmg_ctx* c, int level, bool zero_guess, const stmg_cycle_co
   }
   const bool fused = nu1 == 1 && nu2 == 1 && cfg.gamma == 1;
   if (fused && c->tail_table && level + 1 == c->tail_start) {
-    CK(stmg::launch_tail(L.spec.dim, L.spec.p_t + 1, c->tail_table, c->tail_host,
-                         int(c->levels.size()) - c->tail_start, cfg.omega_t, c->tail_smem,
-                         c->stream));
-    count(c);
-    for (int l = c->tail_start; l < int(c->levels.size()); ++l) c->cur[l] = 0;
+    run_tail(c, cfg.omega_t);
   } else {
     for (int g = 0; g < std::max(cfg.gamma, 1); ++g)
       spectral_cycle(c, level + 1, g == 0, cfg, false, nullptr);
@@ -955,7 +1017,7 @@ int nu_flips(const stmg_cycle_config& cfg) { return std::max(cfg.nu1, 1) + std::
 // iterate in the buffer it started from (true for V(1,1), any nu1 + nu2 even).
 template <class Body>
 cudaGraphExec_t device_loop(stmg_ctx* c, const std::string& key, double eps, int max_iter,
-                            Body&& body, int* parity = nullptr) {
+                            Body&& body, int* parity = nullptr, bool body_decides = false) {
   auto it = c->loops.find(key);
   if (it != c->loops.end()) return it->second;
   cudaGraph_t g;
@@ -975,11 +1037,16 @@ cudaGraphExec_t device_loop(stmg_ctx* c, const std::string& key, double eps, int
   CK(cudaStreamBeginCaptureToGraph(c->stream, bodyg, nullptr, nullptr, 0,
                                    cudaStreamCaptureModeThreadLocal));
   try {
+    c->loop_h = h;
     body();
-    CK(stmg::launch_decide(h, c->d_norm, c->d_r0, c->d_hist, c->d_iter, eps, max_iter, parity,
-                           c->stream));
-    count(c);
+    c->loop_h = 0;
+    if (!body_decides) {
+      CK(stmg::launch_decide(h, c->d_norm, c->d_r0, c->d_hist, c->d_iter, eps, max_iter, parity,
+                             c->stream));
+      count(c);
+    }
   } catch (...) {
+    c->loop_h = 0;
     cudaGraph_t dummy;
     cudaStreamEndCapture(c->stream, &dummy);
     c->capturing = false;
@@ -1045,31 +1112,44 @@ bool fused_eligible(const stmg_ctx* c, const stmg_cycle_config& cfg) {
 // Coarse part (levels >= 1) of one V(1,1) cycle, zero initial guess.
 void coarse_cycle(stmg_ctx* c, const stmg_cycle_config& cfg) {
   if (c->tail_table && c->tail_start == 1) {
-    CK(stmg::launch_tail(c->dim, c->p_t + 1, c->tail_table, c->tail_host,
-                         int(c->levels.size()) - 1, cfg.omega_t, c->tail_smem, c->stream));
-    count(c);
-    for (int l = 1; l < int(c->levels.size()); ++l) c->cur[l] = 0;
+    run_tail(c, cfg.omega_t);
   } else {
     spectral_cycle(c, 1, true, cfg, false, nullptr);
   }
 }
 
-// One fused cycle body (captured): coarse(k), k_updown, norm.
-void fused_body(stmg_ctx* c, const stmg_cycle_config& cfg, i64* np) {
+// One fused cycle body (captured): coarse(k), k_updown, norm (+ the stop
+// test when `decide`: then k_updown's last CTA does norm and stop test).
+void fused_body(stmg_ctx* c, const stmg_cycle_config& cfg, i64* np, bool decide = false,
+                double eps = 0.0, int max_iter = 0) {
   Level& L = c->levels[0];
   Level& C = c->levels[1];
   prof_begin(c, 4);
   coarse_cycle(c, cfg);
   prof_end(c, 4, 0.0);
   stmg::ModalArgs a = modal_args(L, &C, cfg.omega_t, true);
+  stmg::Finalize fin;
+  if (decide) {
+    fin.counter = c->d_counter;
+    fin.norm = c->d_norm;
+    fin.r0 = c->d_r0;
+    fin.hist = c->d_hist;
+    fin.iter = c->d_iter;
+    fin.parity = c->d_par;
+    fin.eps = eps;
+    fin.max_iter = max_iter;
+    fin.handle = c->loop_h;
+  }
   prof_begin(c, 0);
   CK(stmg::launch_updown(L.view, a, C.U[c->cur[1]].base, c->d_pp, c->d_par, L.F.base, C.F.base,
-                         c->partials.base, c->stream));
+                         c->partials.base, c->stream, 0, fin));
   prof_end(c, 0, 8.0 * double(3 * L.view.size() + 2 * C.view.size()));
   count(c);
   *np = a.n_partials;
-  CK(stmg::launch_norm_final(c->partials.base, *np, c->d_norm, nullptr, 0, c->stream));
-  count(c);
+  if (!decide) {
+    CK(stmg::launch_norm_final(c->partials.base, *np, c->d_norm, nullptr, 0, c->stream));
+    count(c);
+  }
 }
 
 // Runs the cycles of a solve whose finest iterate is in U0[0] (r0 known and
@@ -1096,17 +1176,19 @@ void run_fused(stmg_ctx* c, const stmg_cycle_config& cfg, double eps, int max_it
   CK(cudaMemsetAsync(c->d_iter, 0, sizeof(int), c->stream));
   int iters = 0;
   if (c->use_device_loop && !c->profile) {
+    const bool fd = c->fuse_final;
     cudaGraphExec_t ex = device_loop(
-        c, loop_key("fused", cfg, 0, eps, max_iter), eps, max_iter,
+        c, loop_key(fd ? "fusedfin" : "fused", cfg, 0, eps, max_iter), eps, max_iter,
         [&] {
           i64 np = 0;
-          fused_body(c, cfg, &np);
+          fused_body(c, cfg, &np, fd, eps, max_iter);
         },
-        c->d_par);
+        c->d_par, fd);
     CK(cudaGraphLaunch(ex, c->stream));
     CK(cudaMemcpyAsync(&iters, c->d_iter, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    c->launches += iters * c->loop_kernels[loop_key("fused", cfg, 0, eps, max_iter)];
+    c->launches +=
+        iters * c->loop_kernels[loop_key(fd ? "fusedfin" : "fused", cfg, 0, eps, max_iter)];
   } else {  // host-driven cycles (profiling: event records around k_updown)
     const std::string key = loop_key("fusedbody", cfg, 0, eps, max_iter);
     auto it = c->fused_bodies.find(key);
@@ -1199,6 +1281,7 @@ void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config
   } else {
     ensure_spectral(c, 0);
     ensure_tail(c);
+    if (v11_exact(cfg)) ensure_cop(c, cfg.omega_t);
     ensure_svc(c, cfg);
     c->cur[0] = 0;
     // a zero initial guess (the usual case) needs no transform
@@ -1576,10 +1659,7 @@ void sharded_cycle(stmg_ctx* c, const stmg_cycle_config& cfg, bool copy_norm = t
   for (Shard& sh : ss.local) have_root |= sh.g == 0;
   if (have_root) {
     if (c->tail_table && lg == c->tail_start && nu1 == 1 && nu2 == 1) {  // tail = V(1,1)
-      CK(stmg::launch_tail(c->dim, c->p_t + 1, c->tail_table, c->tail_host,
-                           int(c->levels.size()) - lg, cfg.omega_t, c->tail_smem, c->stream));
-      count(c);
-      for (int l = lg; l < int(c->levels.size()); ++l) c->cur[l] = 0;
+      run_tail(c, cfg.omega_t);
     } else {
       spectral_cycle(c, lg, true, cfg, false, nullptr);
     }
@@ -1786,6 +1866,7 @@ void solve_sharded(stmg_ctx* c, const double* f, double* u, const stmg_cycle_con
   require(cfg.gamma == 1 && cfg.nu1 >= 1 && cfg.nu2 >= 1,
           "sharded solves support V(nu1, nu2) cycles with nu1, nu2 >= 1");
   build_shards(c);
+  if (v11_exact(cfg)) ensure_cop(c, cfg.omega_t);
   ShardSet& ss = *c->shards;
   stmg_solve_report r{};
   int nh = 0;
@@ -1999,11 +2080,15 @@ int stmg_create(const stmg_hierarchy_params* p, stmg_ctx** out) {
     CK(cudaMallocHost(&c->h_norm, sizeof(double)));
     CK(cudaMalloc(&c->d_flag, sizeof(int)));
     CK(cudaMalloc(&c->d_iter, sizeof(int)));
+    CK(cudaMalloc(&c->d_counter, sizeof(unsigned)));
+    CK(cudaMemset(c->d_counter, 0, sizeof(unsigned)));
     CK(cudaMalloc(&c->d_pp, 2 * sizeof(double*)));
     CK(cudaMalloc(&c->d_par, sizeof(int)));
     CK(cudaMalloc(&c->d_r0, sizeof(double)));
     if (const char* e = std::getenv("STMG_DEVICE_LOOP")) c->use_device_loop = std::atoi(e) != 0;
     if (const char* e = std::getenv("STMG_FUSED")) c->use_fused = std::atoi(e) != 0;
+    if (const char* e = std::getenv("STMG_COARSE_OP")) c->use_cop = std::atoi(e) != 0;
+    if (const char* e = std::getenv("STMG_FUSE_FINAL")) c->fuse_final = std::atoi(e) != 0;
     CK(cudaMallocHost(&c->h_flag, sizeof(int)));
     CK(cudaEventCreate(&c->ev_solve[0]));
     CK(cudaEventCreate(&c->ev_solve[1]));
@@ -2044,6 +2129,7 @@ int stmg_destroy(stmg_ctx* c) {
     c->partials_phys.release();
     c->svc_pool.release();
     for (auto& kv : c->space_tab) cudaFree(kv.second);
+    for (auto& kv : c->cop) cudaFree(kv.second);
     c->user_f.release();
     c->user_u.release();
     for (auto& s : c->prof) {
@@ -2060,6 +2146,7 @@ int stmg_destroy(stmg_ctx* c) {
     cudaFree(c->d_hist);
     cudaFree(c->d_flag);
     cudaFree(c->d_iter);
+    cudaFree(c->d_counter);
     cudaFree(c->d_pp);
     cudaFree(c->d_par);
     for (auto& kv : c->fused_bodies) cudaGraphExecDestroy(kv.second);
@@ -2317,6 +2404,7 @@ int stmg_mg_cycle(stmg_ctx* c, int level, double* u, const double* f,
     }
     ensure_spectral(c, 0);
     ensure_tail(c);
+    if (v11_exact(*cfg)) ensure_cop(c, cfg->omega_t);
     c->cur[level] = 0;
     dst_all(c, L, f, L.F.base);
     dst_all(c, L, u, L.U[0].base);

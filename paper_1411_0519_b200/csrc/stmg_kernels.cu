@@ -564,6 +564,22 @@ __device__ __forceinline__ double updown_body(const i64 tid, const i64 n0, const
   return sumsq;
 }
 
+// sqrt of the sum of partial[0..n) in k_norm_final's order (256 strided
+// partial sums, then a tree), computed by a 128-thread block: bitwise equal.
+__device__ double norm_final_128(const double* partial, const i64 n, double* sh256) {
+  double a = 0.0, b = 0.0;
+  for (i64 i = threadIdx.x; i < n; i += 256) a += __ldcg(partial + i);
+  for (i64 i = threadIdx.x + 128; i < n; i += 256) b += __ldcg(partial + i);
+  sh256[threadIdx.x] = a;
+  sh256[threadIdx.x + 128] = b;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (int(threadIdx.x) < w) sh256[threadIdx.x] += sh256[threadIdx.x + w];
+    __syncthreads();
+  }
+  return sqrt(sh256[0]);
+}
+
 template <int DIM, int NL, int CO>
 __global__ void __launch_bounds__(128) k_updown(const double* __restrict__ ec, const PingPong pp,
                                                 const double* __restrict__ f,
@@ -571,8 +587,9 @@ __global__ void __launch_bounds__(128) k_updown(const double* __restrict__ ec, c
                                                 double* __restrict__ partials, const TM<NL> t,
                                                 const SP s, const i64 n_t, const int C,
                                                 const i64 n1c, const double omega,
-                                                const i64 s0) {
-  __shared__ double sh[32];
+                                                const i64 s0, const Finalize fin) {
+  __shared__ double sh[256];
+  __shared__ bool last;
   extern __shared__ double ring[];
   const unsigned bx = blockIdx.x, by = blockIdx.y;
   const i64 tid = i64(bx) * blockDim.x + threadIdx.x;
@@ -583,6 +600,27 @@ __global__ void __launch_bounds__(128) k_updown(const double* __restrict__ ec, c
   pdl_trigger();
   const double tot = block_sum(sumsq, sh);
   if (threadIdx.x == 0) partials[i64(by) * gridDim.x + bx] = tot;
+  if (!fin.counter) return;
+  // last CTA: norm of the stop-test residual + stop test (k_norm_final + k_decide)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned total = gridDim.x * gridDim.y;
+    last = atomicAdd(fin.counter, 1u) == total - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const double rk = norm_final_128(partials, i64(gridDim.x) * gridDim.y, sh);
+  if (threadIdx.x == 0) {
+    *fin.counter = 0u;
+    *fin.norm = rk;
+    const int k = *fin.iter + 1;
+    *fin.iter = k;
+    fin.hist[k] = rk;
+    const bool more = !(rk <= fin.eps * (*fin.r0)) && k < fin.max_iter;
+    if (fin.parity) *fin.parity = 1 - *fin.parity;
+    if (fin.handle) cudaGraphSetConditional(fin.handle, more ? 1u : 0u);
+  }
 }
 
 // Per-mode forward substitution u_n = A_j^-1 (f_n + M_j N u_{n-1})
@@ -689,6 +727,19 @@ template <int DIM, int NL>
 __global__ void __launch_bounds__(kTailThreads) k_tail(const TailLevel<NL>* __restrict__ lv,
                                                const int nlev, const double omega,
                                                const __grid_constant__ TailParams<NL> P) {
+#ifdef STMG_TAIL_STAMPS
+  unsigned long long ts[32];
+  int nts = 0;
+  auto stamp = [&] {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (nts < 32) ts[nts++] = t;
+  };
+  stamp();
+#define TAIL_STAMP() stamp()
+#else
+#define TAIL_STAMP() (void)0
+#endif
   extern __shared__ double smem[];
   __shared__ TailLevel<NL> lvs[kTailMaxLevels];
   __shared__ i64 off[kTailMaxLevels + 1];
@@ -728,12 +779,15 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(const TailLevel<NL>* __re
     }
   }
   const int sz0 = int(lv[0].n_t * NL * lv[0].s.nx);
+  TAIL_STAMP();
   pdl_wait();  // the tables above are constants; the rhs is the previous kernel's output
+  TAIL_STAMP();
   {  // stage the first level's rhs
     const double* g = lv[0].F;
     for (int i = threadIdx.x; i < sz0; i += T) smem[i] = g[i];
   }
   __syncthreads();
+  TAIL_STAMP();
   for (int k = 0; k + 1 < nlev; ++k) {
     const TailLevel<NL>& A = lvs[k];
     const TailLevel<NL>& B = lvs[k + 1];
@@ -755,6 +809,7 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(const TailLevel<NL>* __re
                                           A.s.n1, omega, n0 > 0, n0 - 1 > 0);
     }
     __syncthreads();
+    TAIL_STAMP();
   }
   {
     const TailLevel<NL>& A = lvs[nlev - 1];
@@ -762,6 +817,7 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(const TailLevel<NL>* __re
       fwdsub_body<DIM, NL, true>(r, A.F, A.U0, P.t[nlev - 1], A.s, A.n_t);
   }
   __syncthreads();
+  TAIL_STAMP();
   for (int k = nlev - 2; k >= 0; --k) {
     const TailLevel<NL>& A = lvs[k];
     const TailLevel<NL>& B = lvs[k + 1];
@@ -781,11 +837,21 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(const TailLevel<NL>* __re
                                          A.s.n1, omega, n0 > 0, n0 - 1 > 0);
     }
     __syncthreads();
+    TAIL_STAMP();
   }
   {  // hand the first level's iterate back
     double* g = lv[0].U0;
     for (int i = threadIdx.x; i < sz0; i += T) g[i] = smem[sz0 + i];
   }
+#ifdef STMG_TAIL_STAMPS
+  __syncthreads();
+  stamp();
+  if (threadIdx.x == 0) {
+    printf("TAIL");
+    for (int i = 1; i < nts; ++i) printf(" %llu", ts[i] - ts[i - 1]);
+    printf("\n");
+  }
+#endif
 }
 
 // Plain damped block-Jacobi sweep per mode (ping-pong: u_out != u_in).
@@ -1666,6 +1732,48 @@ __global__ void k_decide(cudaGraphConditionalHandle h, const double* __restrict_
   if (h) cudaGraphSetConditional(h, more ? 1u : 0u);
 }
 
+// Coarse operator: y = B x with B (n x n, row-major) the precomputed linear
+// map of the coarse tail's V(1,1) cycle (levels >= tail start, zero initial
+// guess), rhs -> iterate.  One warp per row; the block's rows are staged into
+// shared memory with cp.async BEFORE the PDL wait (B is a constant), so their
+// HBM traffic overlaps the previous kernel; after the wait only x (L2) is
+// read.  Fixed summation order: deterministic.
+constexpr int kCopRows = 8;
+__global__ void __launch_bounds__(kCopRows * 32) k_cop_gemv(const double* __restrict__ B,
+                                                            const double* __restrict__ x,
+                                                            double* __restrict__ y, const int n) {
+  extern __shared__ double rows[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = blockIdx.x * kCopRows;
+  const int nr = min(kCopRows, n - r0);
+  for (int i = threadIdx.x; i < nr * n; i += blockDim.x)
+    cp_async8(rows + i, B + i64(r0) * n + i, true);
+  cp_async_commit();
+  pdl_wait();
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  double xv[4];
+  cp_async_wait<0>();
+  __syncthreads();
+  if (w < nr) {
+    const double* br = rows + w * n;
+    int j = lane;
+    for (; j + 96 < n; j += 128) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) xv[q] = x[j + 32 * q];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(br[j + 32 * q], xv[q], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+      if (j + 32 * q < n) acc[q] = fma(br[j + 32 * q], x[j + 32 * q], acc[q]);
+  }
+  pdl_trigger();
+  double v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (w < nr && lane == 0) y[r0 + w] = v;
+}
+
 __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, const double a,
                        const i64 n) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1841,7 +1949,7 @@ cudaError_t launch_decide(cudaGraphConditionalHandle h, const double* norm, cons
 
 cudaError_t launch_updown(const LevelView& L, ModalArgs& a, const double* ec,
                           double* const* tbl, const int* par, const double* f, double* fc,
-                          double* partials, cudaStream_t st, int64_t s0) {
+                          double* partials, cudaStream_t st, int64_t s0, const Finalize& fin) {
   const SP s = make_sp(L.sp);
   const i64 lanes = ipow(s.G, L.sp.dim) << L.sp.dim;
   const dim3 grid(grid1(lanes, 128), unsigned((L.n_t + a.chunk - 1) / a.chunk));
@@ -1851,11 +1959,20 @@ cudaError_t launch_updown(const LevelView& L, ModalArgs& a, const double* ec,
     const TM<NL> t = make_tm<NL>(L.tc);
     if (a.mode == 2)
       PDLK(k_updown<DIM, NL, 2>, grid, 128, ring_bytes(5 * NL), st, ec, pp, f, fc, partials, t,
-           s, L.n_t, a.chunk, a.n1c, a.omega, i64(s0));
+           s, L.n_t, a.chunk, a.n1c, a.omega, i64(s0), fin);
     else
       PDLK(k_updown<DIM, NL, 1>, grid, 128, ring_bytes(5 * NL), st, ec, pp, f, fc, partials, t,
-           s, L.n_t, a.chunk, L.sp.n1, a.omega, i64(s0));
+           s, L.n_t, a.chunk, L.sp.n1, a.omega, i64(s0), fin);
   });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cop_gemv(const double* B, const double* x, double* y, int n,
+                            cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const size_t smem = size_t(kCopRows) * n * sizeof(double);
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  PDLK(k_cop_gemv, grid1(n, kCopRows), kCopRows * 32, smem, st, B, x, y, n);
   return cudaGetLastError();
 }
 

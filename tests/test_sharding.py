@@ -189,3 +189,38 @@ def test_virtual_shards_fused_nonzero_guess_vs_oracle(S):
     u_o, rep_o = o.solve(f, u0, nu1=1, nu2=1, eps=1e-9)
     assert rep_o["iterations"] == rs.iterations
     assert np.abs(us.numpy() - u_o).max() <= 1e-10 * np.abs(u_o).max()
+
+
+def _solve_with_env(env, p, dim, sl, tl, f):
+    from paper_1411_0519_b200 import stmg
+    for k, v in env.items():
+        os.environ[k] = v
+    try:
+        g = stmg.Hierarchy(p, dim, sl, tl)
+    finally:
+        for k in env:
+            os.environ.pop(k, None)
+    u = g.vector(0)
+    r = g.solve(g.upload(f), u, stmg.CycleConfig(nu1=1, nu2=1), 1e-8)
+    return r, u.numpy()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", [(1, 1, 5, 6), (1, 2, 6, 8), (2, 2, 4, 6), (1, 3, 3, 5)])
+def test_schedule_switches_agree(cfg):
+    """The coarse operator (tail as a precomputed matrix, STMG_COARSE_OP) agrees
+    with the tail kernel to rounding; the in-kernel stop test (STMG_FUSE_FINAL)
+    is bitwise equal to the separate norm / decide kernels."""
+    from oracle import oracle as O
+    from paper_1411_0519_b200 import build
+    build.build()
+    p, dim, sl, tl = cfg
+    o = O.Hierarchy(p, dim, sl, tl)
+    f = O.make_inputs(o, 42, random_u0=(dim == 2))
+    r_ref, u_ref = _solve_with_env({"STMG_COARSE_OP": "0"}, p, dim, sl, tl, f)
+    r_op, u_op = _solve_with_env({}, p, dim, sl, tl, f)
+    assert r_op.iterations == r_ref.iterations
+    assert np.abs(u_op - u_ref).max() <= 1e-12 * np.abs(u_ref).max()
+    r_fin, u_fin = _solve_with_env({"STMG_FUSE_FINAL": "1"}, p, dim, sl, tl, f)
+    assert r_fin.residual_history == r_op.residual_history
+    assert np.array_equal(u_fin, u_op)

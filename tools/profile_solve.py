@@ -16,7 +16,10 @@ if cfg["random_u0"]:
     u0 = stmg.BlockVector(h, L0["n_x"], (L0["n_x"],))
     h.fill_uniform(u0, SEED, 1)
     h.fold_u0(f, u0)
-cc = stmg.CycleConfig(nu1=1, nu2=1)
+cc = stmg.CycleConfig(nu1=1, nu2=1, block_solver=os.environ.get("STMG_BLOCK", "exact"))
+# host-driven cycle graphs (profiling mode): ncu sees every kernel; the
+# device-side while loop body is not expanded by ncu
+h.profile(os.environ.get("STMG_HOSTLOOP", "1") == "1")
 for k in range(2):
     u = h.vector(0)
     rep = h.solve(f, u, cc, 1e-8)
