@@ -1212,6 +1212,234 @@ __global__ void __launch_bounds__(ResTile<DIM>::THREADS) k_apply(
   }
 }
 
+// Register-blocked Q1 apply/residual for 2D and 3D.  A CTA of 32 x 4 threads
+// owns a tile of 32 (x) x 4 (y) x R (z) nodes in 3D, or 32 (x) x 4R (y) in 2D;
+// every thread computes R consecutive outputs along the blocked axis (y in
+// 2D, z in 3D) with a rolling window of the 1D row (2D) or 2D plane (3D)
+// stencil combinations, so one staged value feeds ~3 outputs instead of one:
+// (R + 2) / R x 3 shared-memory loads per output in 2D (9 before), x 9 in 3D
+// (27 before).  Staging: cp.async ring of STAGES slabs (tile + halo of u and
+// the tile of f), zero fill outside the Dirichlet domain; the rank-one jump
+// reuses the previous step's M-stencil traces kept in registers.
+template <int DIM>
+struct RbTile {
+  static constexpr int TX = 32, TYT = DIM == 2 ? 8 : 4;
+  static constexpr int R = 4;   // outputs per thread along the blocked axis
+  static constexpr int YB = DIM == 3 ? 2 : 1;  // 3D: y rows per thread (shared plane rows)
+  static constexpr int NO = R * YB;            // outputs per thread
+  static constexpr int TY = DIM == 2 ? TYT * R : TYT * YB;
+  static constexpr int TZ = DIM == 3 ? R : 1;
+  static constexpr int HX = TX + 2, HY = TY + 2, HZ = DIM == 3 ? TZ + 2 : 1;
+  static constexpr int HALO = HX * HY * HZ;
+  static constexpr int OUT = TX * TY * TZ;
+  static constexpr int THREADS = TX * TYT;
+  static constexpr int STAGES = 2;
+};
+
+#ifndef STMG_RB_MINB
+#define STMG_RB_MINB 2
+#endif
+template <int DIM, int NL, bool RES>
+__global__ void __launch_bounds__(RbTile<DIM>::THREADS, DIM == 3 ? STMG_RB_MINB : 1) k_apply_rb(
+    const double* __restrict__ u, const double* __restrict__ f, double* __restrict__ y,
+    const TM<NL> t, const i64 n1_, const i64 nx, const double h, const i64 n_t, const int C,
+    const bool first_global, const double* __restrict__ ab) {
+  using T = RbTile<DIM>;
+  constexpr int R = T::R;
+  extern __shared__ double dsm[];
+  constexpr int BS = NL * T::HALO;
+  constexpr int FS = RES ? NL * T::OUT : 0;
+  constexpr int SS = BS + FS;
+  constexpr int NS = T::STAGES;
+  const int n1 = int(n1_);
+  const int tilesx = (n1 + T::TX - 1) / T::TX;
+  const int tilesy = (n1 + T::TY - 1) / T::TY;
+  int tile = blockIdx.x;
+  const int bx = tile % tilesx;
+  tile /= tilesx;
+  const int by = tile % tilesy;
+  const int bz = tile / tilesy;
+  const int x0 = bx * T::TX, y0 = by * T::TY, z0 = bz * T::TZ;
+  const int tx = threadIdx.x % T::TX, ty = threadIdx.x / T::TX;
+  const int x = x0 + tx;
+  const i64 n0 = i64(blockIdx.y) * C;
+  const i64 nend = min(n0 + i64(C), n_t);
+  const i64 slab = NL * nx;
+  const double m0 = 4.0 * h / 6.0, m1 = h / 6.0, k0 = 2.0 / h, k1 = -1.0 / h;
+  double a[NL], b[NL];
+#pragma unroll
+  for (int k = 0; k < NL; ++k) {
+    a[k] = ab[k];
+    b[k] = ab[kMaxNL + k];
+  }
+  // output j = yb * R + i of this thread: tile-local (tx, oy, oz)
+  constexpr int YB = T::YB, NO = T::NO;
+  auto out_y = [&](int j) { return DIM == 2 ? ty * R + j : ty * YB + j / R; };
+  auto out_z = [&](int j) { return DIM == 3 ? j % R : 0; };
+  auto out_inside = [&](int j) {
+    return x < n1 && y0 + out_y(j) < n1 && (DIM < 3 || z0 + out_z(j) < n1);
+  };
+  auto out_off = [&](int j) {
+    return (i64(DIM == 3 ? z0 + out_z(j) : 0) * n1 + (y0 + out_y(j))) * n1 + x;
+  };
+  auto stage = [&](int m) { return dsm + ((m + NS) % NS) * SS; };
+  // staging plan: slab-relative offsets of this thread's (tile + halo) and f
+  // elements, computed once (-1: outside the Dirichlet domain -> zero fill)
+  constexpr int IH = (BS + T::THREADS - 1) / T::THREADS;
+  constexpr int IF = RES ? (FS + T::THREADS - 1) / T::THREADS : 0;
+  int offh[IH], offf[IF > 0 ? IF : 1];
+#pragma unroll
+  for (int i = 0; i < IH; ++i) {
+    const int e = threadIdx.x + i * T::THREADS;
+    int o = -1;
+    if (e < BS) {
+      const int l = e / T::HALO;
+      const int hh = e - l * T::HALO;
+      const int hx = hh % T::HX, hy = (hh / T::HX) % T::HY, hz = hh / (T::HX * T::HY);
+      const int gx = x0 + hx - 1, gy = y0 + hy - 1, gz = DIM == 3 ? z0 + hz - 1 : 0;
+      if (gx >= 0 && gx < n1 && gy >= 0 && gy < n1 && gz >= 0 && gz < n1)
+        o = int(l * nx + (i64(gz) * n1 + gy) * n1 + gx);
+    }
+    offh[i] = o;
+  }
+#pragma unroll
+  for (int i = 0; i < IF; ++i) {
+    const int e = threadIdx.x + i * T::THREADS;
+    int o = -1;
+    if (e < FS) {
+      const int l = e / T::OUT;
+      const int q = e - l * T::OUT;
+      const int gx = x0 + q % T::TX, gy = y0 + (q / T::TX) % T::TY;
+      const int gz = DIM == 3 ? z0 + q / (T::TX * T::TY) : 0;
+      if (gx < n1 && gy < n1 && gz < n1) o = int(l * nx + (i64(gz) * n1 + gy) * n1 + gx);
+    }
+    offf[i] = o;
+  }
+  auto issue = [&](i64 n) {  // slab n -> stage (n - n0 + 1) mod NS
+    double* st = stage(int(n - n0 + 1));
+    const double* base = u + n * slab;
+#pragma unroll
+    for (int i = 0; i < IH; ++i) {
+      const int e = threadIdx.x + i * T::THREADS;
+      if (IH * T::THREADS == BS || e < BS)
+        cp_async8(st + e, base + (offh[i] >= 0 ? offh[i] : 0), offh[i] >= 0);
+    }
+    if (RES) {
+      const double* fb = f + n * slab;
+#pragma unroll
+      for (int i = 0; i < IF; ++i) {
+        const int e = threadIdx.x + i * T::THREADS;
+        if (IF * T::THREADS == FS || e < FS)
+          cp_async8(st + BS + e, fb + (offf[i] >= 0 ? offf[i] : 0), offf[i] >= 0);
+      }
+    }
+  };
+  // 1D row combination of staged component s at halo (hy, hz), this thread's x
+  auto row = [&](const double* s, int hy, int hz, double& Mr, double& Kr) {
+    const double* p = s + (hz * T::HY + hy) * T::HX + tx + 1;
+    const double aa = p[-1] + p[1], c = p[0];
+    Mr = m1 * aa + m0 * c;
+    Kr = k1 * aa + k0 * c;
+  };
+  // units along the blocked axis: a row (2D, halo y = w) or the YB y-plane
+  // combinations of this thread's rows (3D, halo z = w; YB + 2 rows loaded)
+  auto unit = [&](const double* s, int w, double (&Mu)[YB], double (&Ku)[YB]) {
+    if (DIM == 2) {
+      row(s, w, 0, Mu[0], Ku[0]);
+    } else {
+      double Mr[YB + 2], Kr[YB + 2];
+#pragma unroll
+      for (int q = 0; q < YB + 2; ++q) row(s, ty * YB + q, w, Mr[q], Kr[q]);
+#pragma unroll
+      for (int yb = 0; yb < YB; ++yb) {
+        const double ms = Mr[yb] + Mr[yb + 2];
+        Mu[yb] = m1 * ms + m0 * Mr[yb + 1];
+        Ku[yb] = m1 * (Kr[yb] + Kr[yb + 2]) + m0 * Kr[yb + 1] + k1 * ms + k0 * Mr[yb + 1];
+      }
+    }
+  };
+  const int w0 = DIM == 2 ? ty * R : 0;  // first halo unit of this thread's window
+  double mw_prev[NO];
+#pragma unroll
+  for (int j = 0; j < NO; ++j) mw_prev[j] = 0.0;
+  const bool has_prev = n0 > 0 || !first_global;
+  if (has_prev) issue(n0 - 1);
+  cp_async_commit();
+#pragma unroll
+  for (int q = 0; q < NS - 1; ++q) {
+    if (n0 + q < nend) issue(n0 + q);
+    cp_async_commit();
+  }
+  cp_async_wait<NS - 1>();
+  __syncthreads();
+  // Streams the outputs of this thread along the blocked axis: per output the
+  // M / K stencils of every component from a rolling window of 3 units.
+  auto sweep = [&](const double* st, auto&& emit) {
+    double M0[NL][YB], K0[NL][YB], M1[NL][YB], K1[NL][YB];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      unit(st + l * T::HALO, w0, M0[l], K0[l]);
+      unit(st + l * T::HALO, w0 + 1, M1[l], K1[l]);
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      double MU[YB][NL], KU[YB][NL];
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        double M2[YB], K2[YB];
+        unit(st + l * T::HALO, w0 + i + 2, M2, K2);
+#pragma unroll
+        for (int yb = 0; yb < YB; ++yb) {
+          const double ms = M0[l][yb] + M2[yb];
+          MU[yb][l] = m1 * ms + m0 * M1[l][yb];
+          KU[yb][l] = m1 * (K0[l][yb] + K2[yb]) + m0 * K1[l][yb] + k1 * ms + k0 * M1[l][yb];
+          M0[l][yb] = M1[l][yb];
+          K0[l][yb] = K1[l][yb];
+          M1[l][yb] = M2[yb];
+          K1[l][yb] = K2[yb];
+        }
+      }
+#pragma unroll
+      for (int yb = 0; yb < YB; ++yb) emit(yb * R + i, MU[yb], KU[yb]);
+    }
+  };
+  if (has_prev) {
+    sweep(stage(0), [&](int j, const double (&MU)[NL], const double (&)[NL]) {
+      double mw = 0.0;
+#pragma unroll
+      for (int l = 0; l < NL; ++l) mw += b[l] * MU[l];
+      mw_prev[j] = mw;
+    });
+  }
+  for (i64 n = n0; n < nend; ++n) {
+    const int jst = int(n - n0 + 1);
+    cp_async_wait<NS - 2>();
+    __syncthreads();
+    if (n + NS - 1 < nend) issue(n + NS - 1);
+    cp_async_commit();
+    const double* st = stage(jst);
+    sweep(st, [&](int j, const double (&MU)[NL], const double (&KU)[NL]) {
+      double mw = 0.0;
+#pragma unroll
+      for (int l = 0; l < NL; ++l) mw += b[l] * MU[l];
+      if (out_inside(j)) {
+        const i64 r = out_off(j);
+        const int q = (out_z(j) * T::TY + out_y(j)) * T::TX + tx;
+#pragma unroll
+        for (int k = 0; k < NL; ++k) {
+          double acc = 0.0;
+#pragma unroll
+          for (int l = 0; l < NL; ++l) acc += MU[l] * t.K[k][l] + KU[l] * t.M[k][l];
+          acc -= a[k] * mw_prev[j];
+          const i64 o = n * slab + k * nx + r;
+          __stcs(y + o, RES ? st[BS + k * T::OUT + q] - acc : acc);
+        }
+      }
+      mw_prev[j] = mw;
+    });
+  }
+}
+
 // restrict_semi / restrict_full (transfer.cpp:75-85, 138-149): one thread per
 // coarse (step, node): full weighting 1/2{1 2 1} per axis of the time
 // restriction c_n = U_2n R1^T + U_2n+1 R2^T.
@@ -1782,9 +2010,64 @@ __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, con
 
 }  // namespace
 
+// Register-blocked 2D/3D kernel (k_apply_rb); STMG_APPLY_RB=0 selects the
+// one-output-per-thread kernel (kept for 1D and A/B runs).
+template <int DIM, int NL>
+cudaError_t launch_apply_rb(const LevelView& L, const double* u, const double* f, double* y,
+                            bool residual, const double* ab, cudaStream_t st) {
+  using T = RbTile<DIM>;
+  const i64 n1 = L.sp.n1;
+  const i64 tiles = ((n1 + T::TX - 1) / T::TX) * ((n1 + T::TY - 1) / T::TY) *
+                    (DIM == 3 ? (n1 + T::TZ - 1) / T::TZ : 1);
+  i64 C = 64;
+  while (C > 4 && tiles * ((L.n_t + C - 1) / C) < 148 * 4) C /= 2;
+  C = std::min<i64>(C, L.n_t);
+  const dim3 g(unsigned(tiles), unsigned((L.n_t + C - 1) / C));
+  const size_t smem = size_t(T::STAGES) *
+                      (size_t(NL) * T::HALO + (residual ? size_t(NL) * T::OUT : 0)) *
+                      sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    const int most = int(size_t(T::STAGES) * (size_t(NL) * T::HALO + size_t(NL) * T::OUT) *
+                         sizeof(double));
+    cudaFuncSetAttribute(k_apply_rb<DIM, NL, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, most);
+    cudaFuncSetAttribute(k_apply_rb<DIM, NL, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, most);
+    attr = true;
+  }
+  const TM<NL> t = make_tm<NL>(L.tc);
+  if (residual)
+    k_apply_rb<DIM, NL, true><<<g, T::THREADS, smem, st>>>(u, f, y, t, n1, L.sp.nx, L.sp.h,
+                                                              L.n_t, int(C), L.first_global, ab);
+  else
+    k_apply_rb<DIM, NL, false><<<g, T::THREADS, smem, st>>>(u, f, y, t, n1, L.sp.nx, L.sp.h,
+                                                               L.n_t, int(C), L.first_global, ab);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_apply(const LevelView& L, const double* u, const double* f, double* y,
                          bool residual, const double* ab, cudaStream_t st) {
   if (L.n_t * L.sp.nx == 0) return cudaSuccess;
+  // register-blocked kernel: measured faster in 3D (27-point stencil), slower
+  // in 2D (profiles/r01_v8_residual_ab.txt); STMG_APPLY_RB=0/1 forces either
+  static const int rb = [] {
+    const char* e = std::getenv("STMG_APPLY_RB");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (L.sp.dim == 3 ? rb != 0 : (L.sp.dim == 2 && rb == 1)) {
+    switch (L.sp.dim * 8 + L.tc.nl) {
+      case 2 * 8 + 1: return launch_apply_rb<2, 1>(L, u, f, y, residual, ab, st);
+      case 2 * 8 + 2: return launch_apply_rb<2, 2>(L, u, f, y, residual, ab, st);
+      case 2 * 8 + 3: return launch_apply_rb<2, 3>(L, u, f, y, residual, ab, st);
+      case 2 * 8 + 4: return launch_apply_rb<2, 4>(L, u, f, y, residual, ab, st);
+      case 3 * 8 + 1: return launch_apply_rb<3, 1>(L, u, f, y, residual, ab, st);
+      case 3 * 8 + 2: return launch_apply_rb<3, 2>(L, u, f, y, residual, ab, st);
+      case 3 * 8 + 3: return launch_apply_rb<3, 3>(L, u, f, y, residual, ab, st);
+      case 3 * 8 + 4: return launch_apply_rb<3, 4>(L, u, f, y, residual, ab, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   STMG_DISPATCH(L.sp.dim, L.tc.nl, {
     using T = ResTile<DIM>;
     const i64 n1 = L.sp.n1;
