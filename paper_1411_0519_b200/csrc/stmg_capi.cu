@@ -186,11 +186,6 @@ struct stmg_ctx {
   int* d_par = nullptr;
   std::map<std::string, cudaGraphExec_t> fused_bodies;  // per-cycle graphs (profiling)
   int* d_iter = nullptr;
-  unsigned* d_counter = nullptr;  // last-CTA ticket of the fused k_updown epilogue
-  // norm + stop test inside k_updown's last CTA (fused schedule).  Measured
-  // neutral on B200 (PDL already hides the two tiny kernels): off by default.
-  bool fuse_final = false;
-  cudaGraphConditionalHandle loop_h = 0;  // handle of the while node being captured
   double* d_r0 = nullptr;
   bool use_device_loop = true;
   bool use_fused = true;  // fused level-0 schedule for V(1,1) solves
@@ -1017,7 +1012,7 @@ int nu_flips(const stmg_cycle_config& cfg) { return std::max(cfg.nu1, 1) + std::
 // iterate in the buffer it started from (true for V(1,1), any nu1 + nu2 even).
 template <class Body>
 cudaGraphExec_t device_loop(stmg_ctx* c, const std::string& key, double eps, int max_iter,
-                            Body&& body, int* parity = nullptr, bool body_decides = false) {
+                            Body&& body, int* parity = nullptr) {
   auto it = c->loops.find(key);
   if (it != c->loops.end()) return it->second;
   cudaGraph_t g;
@@ -1037,16 +1032,11 @@ cudaGraphExec_t device_loop(stmg_ctx* c, const std::string& key, double eps, int
   CK(cudaStreamBeginCaptureToGraph(c->stream, bodyg, nullptr, nullptr, 0,
                                    cudaStreamCaptureModeThreadLocal));
   try {
-    c->loop_h = h;
     body();
-    c->loop_h = 0;
-    if (!body_decides) {
-      CK(stmg::launch_decide(h, c->d_norm, c->d_r0, c->d_hist, c->d_iter, eps, max_iter, parity,
-                             c->stream));
-      count(c);
-    }
+    CK(stmg::launch_decide(h, c->d_norm, c->d_r0, c->d_hist, c->d_iter, eps, max_iter, parity,
+                           c->stream));
+    count(c);
   } catch (...) {
-    c->loop_h = 0;
     cudaGraph_t dummy;
     cudaStreamEndCapture(c->stream, &dummy);
     c->capturing = false;
@@ -1118,38 +1108,22 @@ void coarse_cycle(stmg_ctx* c, const stmg_cycle_config& cfg) {
   }
 }
 
-// One fused cycle body (captured): coarse(k), k_updown, norm (+ the stop
-// test when `decide`: then k_updown's last CTA does norm and stop test).
-void fused_body(stmg_ctx* c, const stmg_cycle_config& cfg, i64* np, bool decide = false,
-                double eps = 0.0, int max_iter = 0) {
+// One fused cycle body (captured): coarse(k), k_updown, norm.
+void fused_body(stmg_ctx* c, const stmg_cycle_config& cfg, i64* np) {
   Level& L = c->levels[0];
   Level& C = c->levels[1];
   prof_begin(c, 4);
   coarse_cycle(c, cfg);
   prof_end(c, 4, 0.0);
   stmg::ModalArgs a = modal_args(L, &C, cfg.omega_t, true);
-  stmg::Finalize fin;
-  if (decide) {
-    fin.counter = c->d_counter;
-    fin.norm = c->d_norm;
-    fin.r0 = c->d_r0;
-    fin.hist = c->d_hist;
-    fin.iter = c->d_iter;
-    fin.parity = c->d_par;
-    fin.eps = eps;
-    fin.max_iter = max_iter;
-    fin.handle = c->loop_h;
-  }
   prof_begin(c, 0);
   CK(stmg::launch_updown(L.view, a, C.U[c->cur[1]].base, c->d_pp, c->d_par, L.F.base, C.F.base,
-                         c->partials.base, c->stream, 0, fin));
+                         c->partials.base, c->stream));
   prof_end(c, 0, 8.0 * double(3 * L.view.size() + 2 * C.view.size()));
   count(c);
   *np = a.n_partials;
-  if (!decide) {
-    CK(stmg::launch_norm_final(c->partials.base, *np, c->d_norm, nullptr, 0, c->stream));
-    count(c);
-  }
+  CK(stmg::launch_norm_final(c->partials.base, *np, c->d_norm, nullptr, 0, c->stream));
+  count(c);
 }
 
 // Runs the cycles of a solve whose finest iterate is in U0[0] (r0 known and
@@ -1176,19 +1150,17 @@ void run_fused(stmg_ctx* c, const stmg_cycle_config& cfg, double eps, int max_it
   CK(cudaMemsetAsync(c->d_iter, 0, sizeof(int), c->stream));
   int iters = 0;
   if (c->use_device_loop && !c->profile) {
-    const bool fd = c->fuse_final;
     cudaGraphExec_t ex = device_loop(
-        c, loop_key(fd ? "fusedfin" : "fused", cfg, 0, eps, max_iter), eps, max_iter,
+        c, loop_key("fused", cfg, 0, eps, max_iter), eps, max_iter,
         [&] {
           i64 np = 0;
-          fused_body(c, cfg, &np, fd, eps, max_iter);
+          fused_body(c, cfg, &np);
         },
-        c->d_par, fd);
+        c->d_par);
     CK(cudaGraphLaunch(ex, c->stream));
     CK(cudaMemcpyAsync(&iters, c->d_iter, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    c->launches +=
-        iters * c->loop_kernels[loop_key(fd ? "fusedfin" : "fused", cfg, 0, eps, max_iter)];
+    c->launches += iters * c->loop_kernels[loop_key("fused", cfg, 0, eps, max_iter)];
   } else {  // host-driven cycles (profiling: event records around k_updown)
     const std::string key = loop_key("fusedbody", cfg, 0, eps, max_iter);
     auto it = c->fused_bodies.find(key);
@@ -2080,15 +2052,12 @@ int stmg_create(const stmg_hierarchy_params* p, stmg_ctx** out) {
     CK(cudaMallocHost(&c->h_norm, sizeof(double)));
     CK(cudaMalloc(&c->d_flag, sizeof(int)));
     CK(cudaMalloc(&c->d_iter, sizeof(int)));
-    CK(cudaMalloc(&c->d_counter, sizeof(unsigned)));
-    CK(cudaMemset(c->d_counter, 0, sizeof(unsigned)));
     CK(cudaMalloc(&c->d_pp, 2 * sizeof(double*)));
     CK(cudaMalloc(&c->d_par, sizeof(int)));
     CK(cudaMalloc(&c->d_r0, sizeof(double)));
     if (const char* e = std::getenv("STMG_DEVICE_LOOP")) c->use_device_loop = std::atoi(e) != 0;
     if (const char* e = std::getenv("STMG_FUSED")) c->use_fused = std::atoi(e) != 0;
     if (const char* e = std::getenv("STMG_COARSE_OP")) c->use_cop = std::atoi(e) != 0;
-    if (const char* e = std::getenv("STMG_FUSE_FINAL")) c->fuse_final = std::atoi(e) != 0;
     CK(cudaMallocHost(&c->h_flag, sizeof(int)));
     CK(cudaEventCreate(&c->ev_solve[0]));
     CK(cudaEventCreate(&c->ev_solve[1]));
@@ -2146,7 +2115,6 @@ int stmg_destroy(stmg_ctx* c) {
     cudaFree(c->d_hist);
     cudaFree(c->d_flag);
     cudaFree(c->d_iter);
-    cudaFree(c->d_counter);
     cudaFree(c->d_pp);
     cudaFree(c->d_par);
     for (auto& kv : c->fused_bodies) cudaGraphExecDestroy(kv.second);

@@ -564,22 +564,6 @@ __device__ __forceinline__ double updown_body(const i64 tid, const i64 n0, const
   return sumsq;
 }
 
-// sqrt of the sum of partial[0..n) in k_norm_final's order (256 strided
-// partial sums, then a tree), computed by a 128-thread block: bitwise equal.
-__device__ double norm_final_128(const double* partial, const i64 n, double* sh256) {
-  double a = 0.0, b = 0.0;
-  for (i64 i = threadIdx.x; i < n; i += 256) a += __ldcg(partial + i);
-  for (i64 i = threadIdx.x + 128; i < n; i += 256) b += __ldcg(partial + i);
-  sh256[threadIdx.x] = a;
-  sh256[threadIdx.x + 128] = b;
-  __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (int(threadIdx.x) < w) sh256[threadIdx.x] += sh256[threadIdx.x + w];
-    __syncthreads();
-  }
-  return sqrt(sh256[0]);
-}
-
 template <int DIM, int NL, int CO>
 __global__ void __launch_bounds__(128) k_updown(const double* __restrict__ ec, const PingPong pp,
                                                 const double* __restrict__ f,
@@ -587,9 +571,8 @@ __global__ void __launch_bounds__(128) k_updown(const double* __restrict__ ec, c
                                                 double* __restrict__ partials, const TM<NL> t,
                                                 const SP s, const i64 n_t, const int C,
                                                 const i64 n1c, const double omega,
-                                                const i64 s0, const Finalize fin) {
-  __shared__ double sh[256];
-  __shared__ bool last;
+                                                const i64 s0) {
+  __shared__ double sh[32];
   extern __shared__ double ring[];
   const unsigned bx = blockIdx.x, by = blockIdx.y;
   const i64 tid = i64(bx) * blockDim.x + threadIdx.x;
@@ -600,27 +583,6 @@ __global__ void __launch_bounds__(128) k_updown(const double* __restrict__ ec, c
   pdl_trigger();
   const double tot = block_sum(sumsq, sh);
   if (threadIdx.x == 0) partials[i64(by) * gridDim.x + bx] = tot;
-  if (!fin.counter) return;
-  // last CTA: norm of the stop-test residual + stop test (k_norm_final + k_decide)
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned total = gridDim.x * gridDim.y;
-    last = atomicAdd(fin.counter, 1u) == total - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  const double rk = norm_final_128(partials, i64(gridDim.x) * gridDim.y, sh);
-  if (threadIdx.x == 0) {
-    *fin.counter = 0u;
-    *fin.norm = rk;
-    const int k = *fin.iter + 1;
-    *fin.iter = k;
-    fin.hist[k] = rk;
-    const bool more = !(rk <= fin.eps * (*fin.r0)) && k < fin.max_iter;
-    if (fin.parity) *fin.parity = 1 - *fin.parity;
-    if (fin.handle) cudaGraphSetConditional(fin.handle, more ? 1u : 0u);
-  }
 }
 
 // Per-mode forward substitution u_n = A_j^-1 (f_n + M_j N u_{n-1})
@@ -1974,14 +1936,41 @@ __global__ void __launch_bounds__(kCopRows * 32) k_cop_gemv(const double* __rest
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = blockIdx.x * kCopRows;
   const int nr = min(kCopRows, n - r0);
-  for (int i = threadIdx.x; i < nr * n; i += blockDim.x)
-    cp_async8(rows + i, B + i64(r0) * n + i, true);
-  cp_async_commit();
+  __shared__ alignas(8) unsigned long long bar;
+  const double* src = B + i64(r0) * n;
+  const unsigned bar_s = static_cast<unsigned>(__cvta_generic_to_shared(&bar));
+  const bool bulk = (n & 1) == 0;  // rows are 16-byte multiples: one TMA bulk copy
+  if (bulk) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s));
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      const unsigned bytes = unsigned(nr) * unsigned(n) * 8u;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s),
+                   "r"(bytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+          "[%3];\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(rows))),
+          "l"(src), "r"(bytes), "r"(bar_s)
+          : "memory");
+    }
+  } else {
+    for (int i = threadIdx.x; i < nr * n; i += blockDim.x) cp_async8(rows + i, src + i, true);
+    cp_async_commit();
+  }
   pdl_wait();
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   double xv[4];
-  cp_async_wait<0>();
-  __syncthreads();
+  if (bulk) {
+    __syncthreads();  // barrier initialised before anyone polls it
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(bar_s)
+        : "memory");
+  } else {
+    cp_async_wait<0>();
+    __syncthreads();
+  }
   if (w < nr) {
     const double* br = rows + w * n;
     int j = lane;
@@ -2232,7 +2221,7 @@ cudaError_t launch_decide(cudaGraphConditionalHandle h, const double* norm, cons
 
 cudaError_t launch_updown(const LevelView& L, ModalArgs& a, const double* ec,
                           double* const* tbl, const int* par, const double* f, double* fc,
-                          double* partials, cudaStream_t st, int64_t s0, const Finalize& fin) {
+                          double* partials, cudaStream_t st, int64_t s0) {
   const SP s = make_sp(L.sp);
   const i64 lanes = ipow(s.G, L.sp.dim) << L.sp.dim;
   const dim3 grid(grid1(lanes, 128), unsigned((L.n_t + a.chunk - 1) / a.chunk));
@@ -2242,10 +2231,10 @@ cudaError_t launch_updown(const LevelView& L, ModalArgs& a, const double* ec,
     const TM<NL> t = make_tm<NL>(L.tc);
     if (a.mode == 2)
       PDLK(k_updown<DIM, NL, 2>, grid, 128, ring_bytes(5 * NL), st, ec, pp, f, fc, partials, t,
-           s, L.n_t, a.chunk, a.n1c, a.omega, i64(s0), fin);
+           s, L.n_t, a.chunk, a.n1c, a.omega, i64(s0));
     else
       PDLK(k_updown<DIM, NL, 1>, grid, 128, ring_bytes(5 * NL), st, ec, pp, f, fc, partials, t,
-           s, L.n_t, a.chunk, L.sp.n1, a.omega, i64(s0), fin);
+           s, L.n_t, a.chunk, L.sp.n1, a.omega, i64(s0));
   });
   return cudaGetLastError();
 }
@@ -2255,6 +2244,11 @@ cudaError_t launch_cop_gemv(const double* B, const double* x, double* y, int n,
   if (n <= 0) return cudaSuccess;
   const size_t smem = size_t(kCopRows) * n * sizeof(double);
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {  // two 100 KB CTAs per SM: all rows of B in flight in one wave
+    cudaFuncSetAttribute(k_cop_gemv, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    attr = true;
+  }
   PDLK(k_cop_gemv, grid1(n, kCopRows), kCopRows * 32, smem, st, B, x, y, n);
   return cudaGetLastError();
 }

@@ -100,28 +100,12 @@ cudaError_t launch_up(const LevelView& L, ModalArgs& a, const double* ec,
 cudaError_t launch_smooth(const LevelView& L, ModalArgs& a, bool zero_guess,
                           const double* f, const double* u_in, double* u_out,
                           cudaStream_t st);
-// Optional epilogue of the fused level-0 kernel: its last CTA reduces the
-// stop-test partials (k_norm_final's order, so results are bitwise those of
-// the separate kernels) and runs the stop test (k_decide): norm -> *norm and
-// hist[++*iter], parity flip, conditional handle (0 = host-driven loop).
-struct Finalize {
-  unsigned* counter = nullptr;  // nullptr: no epilogue (separate kernels)
-  double* norm = nullptr;
-  const double* r0 = nullptr;
-  double* hist = nullptr;
-  int* iter = nullptr;
-  int* parity = nullptr;
-  double eps = 0.0;
-  int max_iter = 0;
-  cudaGraphConditionalHandle handle = 0;
-};
 // Fused level-0 kernel: post-smooth of cycle k + pre-smooth/residual/restriction of
 // cycle k+1 (+ stop-test partials).  Buffers: A = tbl[*par] (in), B = tbl[1 - *par] (out).
 // s0: global index of local step 0 (time-slab shards read steps -3..-1 from halos).
 cudaError_t launch_updown(const LevelView& L, ModalArgs& a, const double* ec,
                           double* const* tbl, const int* par, const double* f, double* fc,
-                          double* partials, cudaStream_t st, int64_t s0 = 0,
-                          const Finalize& fin = Finalize());
+                          double* partials, cudaStream_t st, int64_t s0 = 0);
 // Residual sum-of-squares partials of f - L u.
 cudaError_t launch_resnorm(const LevelView& L, ModalArgs& a, const double* u,
                            const double* f, double* partials, cudaStream_t st);
