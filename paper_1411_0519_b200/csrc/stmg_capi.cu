@@ -2034,6 +2034,7 @@ int stmg_create(const stmg_hierarchy_params* p, stmg_ctx** out) {
     auto c = std::make_unique<stmg_ctx>();
     c->device = p->device;
     CK(cudaSetDevice(c->device));
+    CK(stmg::init_kernel_tables());
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->p_t = p->p_t;
     c->dim = p->dim;

@@ -1849,6 +1849,106 @@ __global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK, (LOG2N >= 4 ? 5 : 1)) 
 }
 
 // ================================================================ misc
+// ---- dense DST-I for n1 = 63 (3D C4 and every 63-node axis) --------------
+// For N = 64 the transform as a dense contraction on the FP64 tensor cores
+// (mma.sync m8n8k4 f64, DMMA) beats the radix-16 FFT, whose shared-memory
+// passes are L1-pipe bound at this size.  One even/odd butterfly first halves
+// the work: with X_j (j = 1..63) and mirrors X_{64-j},
+//   Y_{2c+1} = sum_j' Sodd[j'][c] (X_{j'+1} + X_{63-j'}),  (j' < 31; j' = 31: X_32)
+//   Y_{2c+2} = sum_j' Seven[j'][c] (X_{j'+1} - X_{63-j'}),
+// two 32 x 32 contractions per line instead of one 64 x 64.  A warp owns 16
+// lines: A fragments (s, d) are formed in registers from global loads, B
+// fragments (Sodd | Seven, 16 KB, L1-resident) come through the read-only
+// path, C fragments go straight to global memory: no shared memory at all.
+__device__ double g_dst64[2 * 32 * 32];  // Sodd | Seven, [j'][c]
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+template <bool STRIDED>
+__global__ void __launch_bounds__(128) k_dst_dense64(const double* __restrict__ in,
+                                                     double* __restrict__ out, const i64 n_lines,
+                                                     const i64 stride, const double alpha,
+                                                     const int accumulate) {
+  constexpr int n1 = 63;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ar = lane >> 2, ac = lane & 3;  // A: row (line), col (j'); B: row (j') = ac, col = ar
+  const i64 L0 = (i64(blockIdx.x) * 4 + warp) * 16;
+  i64 base[2];
+  bool ok[2];
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    const i64 line = L0 + m * 8 + ar;
+    ok[m] = line < n_lines;
+    const i64 l = ok[m] ? line : 0;
+    if (STRIDED) {
+      const i64 o = l / stride;
+      base[m] = o * stride * n1 + (l - o * stride);
+    } else {
+      base[m] = l * n1;
+    }
+  }
+  const i64 js = STRIDED ? stride : 1;
+  double sv[8][2], dv[8][2];
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int j = ks * 4 + ac;  // j' (0-based X index j', mirror 62 - j')
+      double lo = 0.0, hi = 0.0;
+      if (ok[m]) {
+        lo = __ldcs(in + base[m] + j * js);
+        if (j < 31) hi = __ldcs(in + base[m] + (62 - j) * js);
+      }
+      sv[ks][m] = lo + hi;
+      dv[ks][m] = j < 31 ? lo - hi : 0.0;
+    }
+  double ao[2][4][2], ae[2][4][2];
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int n = 0; n < 4; ++n) ao[m][n][0] = ao[m][n][1] = ae[m][n][0] = ae[m][n][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    double bo[4], be[4];
+    const double* so = g_dst64 + (ks * 4 + ac) * 32 + ar;
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      bo[n] = __ldg(so + n * 8);
+      be[n] = __ldg(so + 1024 + n * 8);
+    }
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        dmma(ao[m][n], sv[ks][m], bo[n]);
+        dmma(ae[m][n], dv[ks][m], be[n]);
+      }
+  }
+  // C fragment: row = lane >> 2, cols c = n * 8 + (lane & 3) * 2 + q -> Y[2c] (odd k), Y[2c+1]
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    if (!ok[m]) continue;
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int c = n * 8 + ac * 2 + q;
+        double* p = out + base[m] + (2 * c) * js;
+        if (accumulate) {
+          p[0] += alpha * ao[m][n][q];
+          if (c < 31) p[js] += alpha * ae[m][n][q];
+        } else {
+          __stcs(p, ao[m][n][q]);
+          if (c < 31) __stcs(p + js, ae[m][n][q]);
+        }
+      }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_step_sumsq(const double* __restrict__ v, const i64 slab,
                                                     double* __restrict__ partial) {
   __shared__ double sh[32];
@@ -2142,6 +2242,19 @@ cudaError_t launch_dst_axis(const LevelView& L, int axis, const double* in, doub
   if ((i64(1) << log2n) != n1 + 1) return cudaErrorInvalidValue;
   const double scale = std::sqrt(2.0 / double(n1 + 1));
   const double2* tw = static_cast<const double2*>(twiddles);
+  static const bool dense = [] {
+    const char* e = std::getenv("STMG_DST_DENSE");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (log2n == 6 && dense) {
+    const unsigned g = unsigned((n_lines + 63) / 64);
+    if (stride == 1)
+      k_dst_dense64<false><<<g, 128, 0, st>>>(in, out, n_lines, stride, alpha,
+                                              accumulate ? 1 : 0);
+    else
+      k_dst_dense64<true><<<g, 128, 0, st>>>(in, out, n_lines, stride, alpha, accumulate ? 1 : 0);
+    return cudaGetLastError();
+  }
   switch (log2n) {
 #define STMG_DST_CASE(K)                                                                   \
   case K: {                                                                                \
@@ -2171,6 +2284,21 @@ cudaError_t launch_dst_axis(const LevelView& L, int axis, const double* in, doub
       return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
+}
+
+cudaError_t init_kernel_tables() {
+  // Sodd[j'][c] = S(2c+1, j'+1) (j' < 31), S(2c+1, 32) (j' = 31);
+  // Seven[j'][c] = S(2c+2, j'+1) (j' < 31, c < 31), else 0; S(k, j) = sqrt(2/64) sin(pi k j / 64)
+  std::vector<double> T(2 * 32 * 32, 0.0);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  const double sc = std::sqrt(2.0 / 64.0);
+  auto S = [&](int k, int j) { return sc * double(std::sin(pi * (long double)(k * j) / 64.0L)); };
+  for (int jp = 0; jp < 32; ++jp)
+    for (int c = 0; c < 32; ++c) {
+      T[jp * 32 + c] = S(2 * c + 1, jp < 31 ? jp + 1 : 32);
+      if (jp < 31 && c < 31) T[1024 + jp * 32 + c] = S(2 * c + 2, jp + 1);
+    }
+  return cudaMemcpyToSymbol(g_dst64, T.data(), T.size() * sizeof(double));
 }
 
 cudaError_t launch_modal_solve(const LevelView& L, double* x, cudaStream_t st) {

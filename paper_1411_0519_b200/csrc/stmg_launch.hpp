@@ -58,6 +58,8 @@ cudaError_t launch_fold_u0(const LevelView& L, double* f, const double* u0,
 cudaError_t launch_dst_axis(const LevelView& L, int axis, const double* in,
                             double* out, bool accumulate, double alpha,
                             const void* twiddles, cudaStream_t st);
+// Constant tables of the kernels (dense DST-I matrix); once per process/device.
+cudaError_t init_kernel_tables();
 // Per-mode exact block solve in the sine basis, in place.
 cudaError_t launch_modal_solve(const LevelView& L, double* x, cudaStream_t st);
 // Per-mode sequential forward substitution in the sine basis.

@@ -308,3 +308,20 @@ def test_distributed_api_single_rank(S):
     _, rep_o = o.solve(f)
     rep = g.solve(g.upload(f), g.vector(0), S.CycleConfig(nu1=1, nu2=1), 1e-8)
     assert rep.iterations == rep_o["iterations"]
+
+
+@pytest.mark.parametrize("p,dim,tl", [(1, 1, 3), (1, 2, 2), (2, 2, 1), (1, 3, 1)])
+def test_n63_transforms_match_oracle(S, p, dim, tl):
+    """63-node axes (C4's grid) use the dense tensor-core DST-I: the exact block
+    solve (forward + inverse transforms on every axis), the physical smoother
+    and a solve against the oracle."""
+    g, o = pair(S, p, dim, 5, tl, 0.05, 1, 1)
+    n = o.levels[0].size
+    b = O.fill_uniform(n, 31, 0)
+    u = O.fill_uniform(n, 32, 0)
+    assert rel(g.block_solve(0, g.upload(b)).numpy(), o.block_solve(0, b)) < 1e-12
+    us = g.block_jacobi_step(0, g.upload(u), g.upload(b), 0.5, 1).numpy()
+    assert rel(us, o.smooth(0, u, b, 0.5, 1)) < 1e-11
+    du = g.upload(u)
+    g.mg_cycle(0, du, g.upload(b), S.CycleConfig(nu1=1, nu2=1))
+    assert rel(du.numpy(), o.mg_cycle(0, u, b)) < 1e-10
