@@ -1715,58 +1715,66 @@ __global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK, (LOG2N >= 4 ? 5 : 1)) 
   }
   for (int f = threadIdx.x; f < F; f += BLK) sm[f * BUF + dst_pad(0)] = make_double2(0.0, 0.0);
   __syncthreads();
-  // ---- load: items = (line pair f, element j); z_{j+1} = (a_j, b_j)
-  constexpr int ITEMS_ALL = F * n1;
+  // ---- load fused with the pre-processing: items (line pair f, j = 1..N/2)
+  // load z_j = (a, b)_{j-1} and its mirror z_{N-j}, write
+  //   X_j = sin(j pi/N)(z_j + z_{N-j}) + (z_j - z_{N-j})/2,  X_{N-j} = ... - ...
+  // (one shared-memory store per value; the middle j = N/2 is its own mirror)
+  constexpr int H = N / 2;
+  constexpr int ITEMS_ALL = F * H;
   constexpr int ITEMS = (ITEMS_ALL + BLK - 1) / BLK;
-  double2 vals[ITEMS];
+  double2 lo[ITEMS], hi[ITEMS];
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int e = threadIdx.x + i * BLK;
-    int f, j;
+    int f, jj;
     if (stride == 1) {
-      f = e / n1;
-      j = e - f * n1;
+      f = e / H;
+      jj = e - f * H;
     } else {
-      j = e / F;
-      f = e - j * F;
+      jj = e / F;
+      f = e - jj * F;
     }
-    double a = 0.0, b = 0.0;
+    double al = 0.0, bl = 0.0, ah = 0.0, bh = 0.0;
     if (e < ITEMS_ALL) {
-      if (2 * f < nt) a = __ldcs(in + lbase[2 * f] + i64(j) * stride);
-      if (2 * f + 1 < nt) b = __ldcs(in + lbase[2 * f + 1] + i64(j) * stride);
+      const i64 pl = i64(jj) * stride, ph = i64(N - 2 - jj) * stride;  // j - 1, N - j - 1
+      if (2 * f < nt) {
+        al = __ldcs(in + lbase[2 * f] + pl);
+        ah = __ldcs(in + lbase[2 * f] + ph);
+      }
+      if (2 * f + 1 < nt) {
+        bl = __ldcs(in + lbase[2 * f + 1] + pl);
+        bh = __ldcs(in + lbase[2 * f + 1] + ph);
+      }
     }
-    vals[i] = make_double2(a, b);
+    lo[i] = make_double2(al, bl);
+    hi[i] = make_double2(ah, bh);
   }
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const int e = threadIdx.x + i * BLK;
     if (e >= ITEMS_ALL) continue;
-    int f, j;
+    int f, jj;
     if (stride == 1) {
-      f = e / n1;
-      j = e - f * n1;
+      f = e / H;
+      jj = e - f * H;
     } else {
-      j = e / F;
-      f = e - j * F;
+      jj = e / F;
+      f = e - jj * F;
     }
-    sm[f * BUF + dst_pad(j + 1)] = vals[i];
-  }
-  __syncthreads();
-  // ---- pre-processing: pairs (j, N-j), j = 1..N/2
-  for (int e = threadIdx.x; e < F * (N / 2); e += BLK) {
-    const int f = e / (N / 2), j = e - f * (N / 2) + 1;
+    const int j = jj + 1;
     double2* X = sm + f * BUF;
-    const double2 zj = X[dst_pad(j)], zm = X[dst_pad(N - j)];
     const double sj = -__ldg(tw + j).y;  // sin(j pi / N)
-    const double2 sum = make_double2(zj.x + zm.x, zj.y + zm.y);
-    const double2 dif = make_double2(0.5 * (zj.x - zm.x), 0.5 * (zj.y - zm.y));
+    const double2 sum = make_double2(lo[i].x + hi[i].x, lo[i].y + hi[i].y);
+    const double2 dif = make_double2(0.5 * (lo[i].x - hi[i].x), 0.5 * (lo[i].y - hi[i].y));
     X[dst_pad(j)] = make_double2(sj * sum.x + dif.x, sj * sum.y + dif.y);
-    if (j != N / 2) X[dst_pad(N - j)] = make_double2(sj * sum.x - dif.x, sj * sum.y - dif.y);
+    if (j != H) X[dst_pad(N - j)] = make_double2(sj * sum.x - dif.x, sj * sum.y - dif.y);
   }
   __syncthreads();
   // ---- FFT of length N per pair
   const int team = threadIdx.x / TS, tt = threadIdx.x % TS;
+#ifndef STMG_DST_SKIP_FFT
   dst_passes<LOG2N, 0, 1>(sm + team * BUF, tt, tw);
+#endif
   __syncthreads();
   // ---- post-processing: split a/b, X_{2k} = I_k, X_{2k+1} = prefix sum of R
   double2* X = sm + team * BUF;
@@ -1823,8 +1831,9 @@ __global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK, (LOG2N >= 4 ? 5 : 1)) 
   __syncthreads();
 
   // ---- store: X_{j+1} of both lines of the pair
+  constexpr int OUT_ALL = F * n1;
 #pragma unroll 4
-  for (int e = threadIdx.x; e < ITEMS_ALL; e += BLK) {
+  for (int e = threadIdx.x; e < OUT_ALL; e += BLK) {
     int f, j;
     if (stride == 1) {
       f = e / n1;
