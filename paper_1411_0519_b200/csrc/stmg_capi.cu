@@ -83,10 +83,14 @@ struct DevBuf {
   double* raw = nullptr;
   double* base = nullptr;
   i64 count = 0;
+  // kTailPad zeroed doubles after the vector: the TMA-staged k_updown copies
+  // whole 16-byte aligned row runs, which may end up to 2 elements past the
+  // last mode
+  static constexpr i64 kTailPad = 16;
   void alloc(i64 n, i64 halo_elems) {
     release();
-    CK(cudaMalloc(&raw, size_t(n + halo_elems) * sizeof(double)));
-    CK(cudaMemset(raw, 0, size_t(n + halo_elems) * sizeof(double)));
+    CK(cudaMalloc(&raw, size_t(n + halo_elems + kTailPad) * sizeof(double)));
+    CK(cudaMemset(raw, 0, size_t(n + halo_elems + kTailPad) * sizeof(double)));
     base = raw + halo_elems;
     count = n;
   }

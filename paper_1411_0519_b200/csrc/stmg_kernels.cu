@@ -564,6 +564,542 @@ __device__ __forceinline__ double updown_body(const i64 tid, const i64 n0, const
   return sumsq;
 }
 
+#ifndef STMG_UPDOWN_PTR
+#define STMG_UPDOWN_PTR 1
+#endif
+
+// The same pass with the explicit per-mode operators (ModeOps): one
+// g = w A^-1 f per step serves both sweeps, and the residual of the
+// pre-smoothed iterate follows from the stop-test residual without another
+// block apply:
+//   res = f - A x + ma S(x_{n-1}) = (1-w) r + ma (S(x_{n-1}) - S(w_{n-1}))
+// (substitute x = (1-w) w + g + h S(w_{n-1}) and A g = w f, A h = w ma).
+// 45 instead of 82 FP64 operations per mode and step for p_t = 1, and
+// shorter dependent chains (no substitutions).
+template <int DIM, int NL, int CO>
+__device__ __forceinline__ double updown_body_ops(const i64 tid, const i64 n0, const i64 nend,
+                                                  const double* ec, const PingPong pp,
+                                                  const double* f, double* fc,
+                                                  const TM<NL>& t, const SP& s, const i64 n1c,
+                                                  const double omega, double* ring,
+                                                  const i64 s0) {
+  const Member me = make_member<DIM>(s, tid, n1c, CO == 2);
+  const i64 nx = s.nx, slab = NL * nx;
+  const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
+  const double om1 = 1.0 - omega;
+  const ModeOps<NL> op_(t, me.Mj, me.Kj, omega);
+  const double fac = (CO == 2) ? me.fac : 1.0;
+  const bool has_c = (CO == 2) ? me.cok : me.ok;
+  const double* ep = ec + ((CO == 2) ? me.cidx : me.idx);
+  const double* fp = f + me.idx;
+  pdl_wait();  // after the constant-only setup above (see down_body)
+  const int par = *pp.par;
+  const double* up = pp.tbl[par] + me.idx;
+  double* op = pp.tbl[1 - par] + me.idx;
+  double sumsq = 0.0;
+
+  // one step: corrected v, post-smoothed w, its residual r, pre-smoothed x
+  // (the previous step's traces sv, sw, sx in, this step's out)
+  auto step = [&](const double (&u)[NL], const double (&fv)[NL], const double (&c)[NL],
+                  double& sv, double& sw, double& sx, double (&r)[NL], double (&x)[NL]) {
+    double v[NL], g[NL], w[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) v[l] = fma(fac, c[l], u[l]);
+    op_.solve_w(fv, g);
+    op_.sweep(v, g, sv, om1, w);
+    op_.residual(fv, w, sw, r);
+    op_.sweep(w, g, sw, om1, x);
+    sv = trace_sum<NL>(v);
+    sw = trace_sum<NL>(w);
+    sx = trace_sum<NL>(x);
+  };
+
+  double svp = 0.0, swp = 0.0, sxp = 0.0;  // traces of step n-1
+  constexpr int Q = 5 * NL;  // u, f of two steps + e of the coarse step
+  constexpr int T = 128;     // launch_updown's block (immediate ring offsets)
+#if STMG_UPDOWN_PTR
+  // running offsets of the next pair to issue (strength-reduced addressing)
+  const unsigned rs = static_cast<unsigned>(__cvta_generic_to_shared(ring + threadIdx.x));
+  i64 uoff = n0 * slab, eoff = (n0 >> 1) * cslab;
+  const double* eb = has_c ? ep : fp;
+  const i64 estep = has_c ? cslab : 0;
+  auto issue = [&](int st) {
+    const unsigned r = rs + unsigned(st * Q * T) * 8u;
+    const double* ub = up + uoff;
+    const double* fb = fp + uoff;
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        cp_async8s(r + unsigned((e * NL + l) * T) * 8u, ub + e * slab + l * nx, me.ok);
+        cp_async8s(r + unsigned(((2 + e) * NL + l) * T) * 8u, fb + e * slab + l * nx, me.ok);
+      }
+#pragma unroll
+    for (int l = 0; l < NL; ++l)
+      cp_async8s(r + unsigned((4 * NL + l) * T) * 8u, eb + eoff + l * nxc, has_c);
+    uoff += 2 * slab;
+    eoff += estep;
+  };
+#pragma unroll
+  for (int q = 0; q < kRing - 1; ++q) {
+    if (n0 + 2 * q < nend) issue(q);
+    cp_async_commit();
+  }
+#else
+  auto issue = [&](i64 n, int st) {
+    double* r = ring + i64(st) * Q * T + threadIdx.x;
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        cp_async8(r + (e * NL + l) * T, up + (n + e) * slab + l * nx, me.ok);
+        cp_async8(r + ((2 + e) * NL + l) * T, fp + (n + e) * slab + l * nx, me.ok);
+      }
+#pragma unroll
+    for (int l = 0; l < NL; ++l)
+      cp_async8(r + (4 * NL + l) * T, has_c ? ep + (n >> 1) * cslab + l * nxc : fp, has_c);
+  };
+#pragma unroll
+  for (int q = 0; q < kRing - 1; ++q) {
+    if (n0 + 2 * q < nend) issue(n0 + 2 * q, q);
+    cp_async_commit();
+  }
+#endif
+  // warm-up: steps n0-3 .. n0-1 (s0: global index of local step 0; sharded:
+  // steps -1..-3 are halo slabs).  Step n0-3 contributes its corrected trace
+  // only; n0-2 its post-smoothed one; n0-1 all three.
+  if (me.ok && s0 + n0 > 0) {
+    // all loads first (one memory latency, not three); n0 is even, so steps
+    // n0-2, n0-1 share a coarse step and n0-3 has the one before
+    double u[3][NL], fv[3][NL], e[2][NL], c[NL], r[NL], x[NL];
+    double sv = 0.0, sw = 0.0, sx = 0.0;
+    const bool h3 = s0 + n0 - 3 >= 0;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) e[0][l] = e[1][l] = u[0][l] = fv[0][l] = 0.0;
+    if (h3) load_nl<NL>(up + (n0 - 3) * slab, nx, u[0]);
+    load_nl<NL>(up + (n0 - 2) * slab, nx, u[1]);
+    load_nl<NL>(up + (n0 - 1) * slab, nx, u[2]);
+    load_nl<NL>(fp + (n0 - 2) * slab, nx, fv[1]);  // step n0-3: only v is used
+    load_nl<NL>(fp + (n0 - 1) * slab, nx, fv[2]);
+    if (has_c) {
+      if (h3) load_nl<NL>(ep + ((n0 >> 1) - 2) * cslab, nxc, e[0]);
+      load_nl<NL>(ep + ((n0 >> 1) - 1) * cslab, nxc, e[1]);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (k == 0 && !h3) continue;
+      if (k == 1) matvec_t<NL>(t.R1, e[1], c);
+      else matvec_t<NL>(t.R2, e[k == 0 ? 0 : 1], c);
+      step(u[k], fv[k], c, sv, sw, sx, r, x);
+    }
+    svp = sv;
+    swp = sw;
+    sxp = sx;
+  }
+
+  // rotating ring stages (no modulo in the loop); x and the coarse rhs go
+  // out with st.global (the ping-pong pointers come from a device table, so
+  // plain stores would be generic); alias-group sums with a full-warp mask
+  // (every lane of the block runs every pair)
+  int st_use = 0, st_iss = kRing - 1;
+  double* opn = op + n0 * slab;
+  double* fcn = fc + (n0 >> 1) * cslab + ((CO == 2) ? me.cidx : me.idx);
+  const bool cst = (CO == 2) ? (me.cok && (tid & ((1 << DIM) - 1)) == 0) : me.ok;
+  for (i64 n = n0; n < nend; n += 2) {
+    double u2[2][NL], f2[2][NL], ev[NL];
+    cp_async_wait<kRing - 2>();
+    {
+      const double* r = ring + st_use * Q * T + threadIdx.x;
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          u2[e][l] = r[(e * NL + l) * T];
+          f2[e][l] = r[((2 + e) * NL + l) * T];
+        }
+#pragma unroll
+      for (int l = 0; l < NL; ++l) ev[l] = r[(4 * NL + l) * T];
+    }
+#if STMG_UPDOWN_PTR
+    if (n + 2 * (kRing - 1) < nend) issue(st_iss);
+#else
+    if (n + 2 * (kRing - 1) < nend) issue(n + 2 * (kRing - 1), st_iss);
+#endif
+    cp_async_commit();
+    st_use = (st_use == kRing - 1) ? 0 : st_use + 1;
+    st_iss = (st_iss == kRing - 1) ? 0 : st_iss + 1;
+    double acc[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) acc[l] = 0.0;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double c[NL], r[NL], x[NL], res[NL], rt[NL];
+      if (e == 0) matvec_t<NL>(t.R1, ev, c);
+      else matvec_t<NL>(t.R2, ev, c);
+      const double swq = swp, sxq = sxp;  // traces of step m-1
+      step(u2[e], f2[e], c, svp, swp, sxp, r, x);
+      if (me.ok) {
+#pragma unroll
+        for (int l = 0; l < NL; ++l) st_global(opn + e * slab + l * nx, x[l]);
+      }
+      const double d = sxq - swq;
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        sumsq = fma(r[l], r[l], sumsq);
+        res[l] = fma(op_.ma[l], d, om1 * r[l]);
+      }
+      if (e == 0) matvec<NL>(t.R1, res, rt);
+      else matvec<NL>(t.R2, res, rt);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) acc[l] += (CO == 2) ? me.fac * rt[l] : rt[l];
+    }
+    opn += 2 * slab;
+    if (CO == 2) {
+#pragma unroll
+      for (int l = 0; l < NL; ++l) acc[l] = group_sum_full<DIM>(me.ok ? acc[l] : 0.0);
+    }
+    if (cst) {
+#pragma unroll
+      for (int l = 0; l < NL; ++l) st_global(fcn + l * nxc, acc[l]);
+    }
+    fcn += cslab;
+  }
+  return me.ok ? sumsq : 0.0;
+}
+
+// ---- Row-run staging (full coarsening, rows of whole alias-group blocks)
+// The cp.async ring above moves every value through L1 (LDGSTS.ca, 8 B per
+// thread): the in-flight lines need L1 capacity, and measured solves slow
+// down by 25 % when the shared-memory carveout squeezes L1.  Here the block's
+// loads go L2 -> shared memory without L1 allocation (16-byte cp.async.cg by
+// all threads, or TMA bulk copies) as whole row segments: when the 128 / 2^DIM groups of a block lie in one
+// row of the group grid (G a multiple of that), every member b of the block
+// reads one contiguous run of GPB fine modes per (array, step, DG component),
+// ascending or mirrored, and the coarse correction one run of GPB coarse
+// modes.  Each run is copied from its 16-byte aligned-down start (GPB + 2
+// doubles) into a slot of the stage; a thread reads slot[o_b + shift] with
+// o_b its distance from the run's first mode.  Stages complete on an
+// mbarrier; one __syncthreads per step pair frees the stage reissued next.
+// 0: per-thread cp.async ring (updown_body_ops); 1: TMA bulk runs (measured
+// slower: ~35-65 small copies per stage, the TMA issue rate bounds it);
+// 2: the same runs in 16-byte cp.async.cg chunks by all threads (default:
+// C3 114 -> 105 ms, C4 82 -> 72 ms, C5 151 -> 140 ms per solve)
+#ifndef STMG_UPDOWN_TMA
+#define STMG_UPDOWN_TMA 2
+#endif
+#ifndef STMG_TMA_STAGES
+#define STMG_TMA_STAGES 3
+#endif
+constexpr int kTmaStages = STMG_TMA_STAGES;
+
+template <int DIM, int NL>
+struct TmaShape {
+  static constexpr int NM = 1 << DIM;       // members per alias group
+  static constexpr int GPB = 128 / NM;      // groups per block (one row run)
+  static constexpr int SEG = GPB + 2;       // doubles per slot
+  static constexpr int NU = 2 * NL * NM;    // u slots (2 steps) = f slots
+  static constexpr int NC = 2 * NU + NL;    // copies per stage
+  static constexpr int STAGE = NC * SEG;    // doubles per stage
+  static constexpr size_t smem = size_t(kTmaStages) * STAGE * sizeof(double);
+};
+
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes,
+                                         unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async16cg(unsigned dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
+// 16-byte aligned-down start of a run and the run's first element's shift
+__device__ __forceinline__ const double* align16(const double* p) {
+  return reinterpret_cast<const double*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15));
+}
+__device__ __forceinline__ int shift16(const double* p) {
+  return int((reinterpret_cast<uintptr_t>(p) >> 3) & 1);
+}
+
+template <int DIM, int NL>
+__device__ __forceinline__ double updown_body_tma(const i64 tid, const i64 n0, const i64 nend,
+                                                  const double* ec, const PingPong pp,
+                                                  const double* f, double* fc,
+                                                  const TM<NL>& t, const SP& s, const i64 n1c,
+                                                  const double omega, double* ring,
+                                                  const i64 s0) {
+  using S = TmaShape<DIM, NL>;
+  constexpr int NM = S::NM, GPB = S::GPB, SEG = S::SEG, NU = S::NU;
+  __shared__ alignas(8) unsigned long long bars[kTmaStages];
+  __shared__ i64 segb[NM + 1];  // run start (fine mode) per member; coarse run start
+  const Member me = make_member<DIM>(s, tid, n1c, true);
+  const i64 nx = s.nx, slab = NL * nx;
+  const i64 nxc = ipow(n1c, DIM), cslab = NL * nxc;
+  const double om1 = 1.0 - omega;
+  const ModeOps<NL> op_(t, me.Mj, me.Kj, omega);
+  const double fac = me.fac;
+  const bool has_c = me.cok;
+  const int b = int(threadIdx.x) & (NM - 1);
+  if (threadIdx.x < NM) {  // group 0 of the block, member b: its run's first mode
+    segb[b] = (b & 1) ? me.idx - (GPB - 1) : me.idx;
+    if (b == 0) segb[NM] = me.cidx;
+  }
+  const unsigned bar0 = static_cast<unsigned>(__cvta_generic_to_shared(bars));
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kTmaStages; ++q) mbar_init(bar0 + 8u * q, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const i64 sb = segb[b], cb = segb[NM];
+  const int ob = int(me.idx - sb);          // offset in the member's run
+  const int oc = int(me.cidx - cb);         // offset in the coarse run
+  pdl_wait();
+  const int par = *pp.par;
+  const double* ub = pp.tbl[par];
+  double* op = pp.tbl[1 - par] + me.idx;
+  const double* up = ub + me.idx;
+  const double* fp = f + me.idx;
+  const double* ep = ec + me.cidx;
+  // per-slot shifts of this thread's runs (n is even: constant over pairs)
+  unsigned shu = 0, shf = 0;
+#pragma unroll
+  for (int e = 0; e < 2; ++e)
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      shu |= unsigned(shift16(ub + e * slab + l * nx + sb)) << (e * NL + l);
+      shf |= unsigned(shift16(f + e * slab + l * nx + sb)) << (e * NL + l);
+    }
+  const unsigned ring_s = static_cast<unsigned>(__cvta_generic_to_shared(ring));
+  const int lane = threadIdx.x & 31;
+  // warp 0 issues stage st for the pair starting at n: lane i copies slots i, i+32, ...
+  auto issue = [&](i64 n, int st) {
+    const unsigned bar = bar0 + 8u * st;
+    if (lane == 0) mbar_expect(bar, unsigned(S::NC * SEG * 8));
+    __syncwarp();
+    const unsigned base = ring_s + unsigned(st * S::STAGE) * 8u;
+    for (int c = lane; c < S::NC; c += 32) {
+      const double* src;
+      if (c < 2 * NU) {
+        const int arr = c / NU, r = c - arr * NU;        // r = (e * NL + l) * NM + m
+        const int m = r % NM, el = r / NM, e = el / NL, l = el - e * NL;
+        src = (arr ? f : ub) + (n + e) * slab + l * nx;
+        src += segb[m];
+      } else {
+        const int l = c - 2 * NU;
+        src = ec + (n >> 1) * cslab + l * nxc + cb;
+      }
+      bulk_g2s(base + unsigned(c * SEG) * 8u, align16(src), unsigned(SEG * 8), bar);
+    }
+  };
+  // CG (STMG_UPDOWN_TMA == 2): the same runs, copied by all threads in
+  // 16-byte cp.async.cg chunks (L2 -> shared, no L1 allocation); chunk
+  // k = threadIdx.x + 128 i of a stage.  Fine-run sources at n = 0 are
+  // precomputed (n is even, so n * slab keeps the 16-byte alignment).
+  constexpr bool CG = STMG_UPDOWN_TMA == 2;
+  constexpr int HC = SEG / 2, NCH = S::NC * HC, KPT = (NCH + 127) / 128;
+  const double* csrc[KPT];
+  unsigned cdst[KPT];
+  if (CG) {
+#pragma unroll
+    for (int i = 0; i < KPT; ++i) {
+      const int k = int(threadIdx.x) + 128 * i;
+      const int c = k / HC, j = k - c * HC;
+      cdst[i] = unsigned(c * SEG + 2 * j) * 8u;
+      csrc[i] = nullptr;
+      if (c < 2 * NU) {
+        const int arr = c / NU, r = c - arr * NU;
+        const int m = r % NM, el = r / NM, e = el / NL, l = el - e * NL;
+        csrc[i] = align16((arr ? f : ub) + e * slab + l * nx + segb[m]) + 2 * j;
+      }
+    }
+  }
+  auto issue_cg = [&](i64 n, int st) {
+    const unsigned base = ring_s + unsigned(st * S::STAGE) * 8u;
+#pragma unroll
+    for (int i = 0; i < KPT; ++i) {
+      const int k = int(threadIdx.x) + 128 * i;
+      if (k >= NCH) break;
+      const int c = k / HC;
+      const double* src;
+      if (c < 2 * NU) {
+        src = csrc[i] + n * slab;
+      } else {
+        const int l = c - 2 * NU, j = k - c * HC;
+        src = align16(ec + (n >> 1) * cslab + l * nxc + cb) + 2 * j;
+      }
+      cp_async16cg(base + cdst[i], src);
+    }
+  };
+  unsigned phase = 0;  // bit q: parity of stage q's next completion
+  if (CG) {
+#pragma unroll
+    for (int q = 0; q < kTmaStages - 1; ++q) {
+      if (n0 + 2 * q < nend) issue_cg(n0 + 2 * q, q);
+      cp_async_commit();
+    }
+  } else if (threadIdx.x < 32) {
+#pragma unroll
+    for (int q = 0; q < kTmaStages - 1; ++q)
+      if (n0 + 2 * q < nend) issue(n0 + 2 * q, q);
+  }
+
+  double sumsq = 0.0;
+  auto step = [&](const double (&u)[NL], const double (&fv)[NL], const double (&c)[NL],
+                  double& sv, double& sw, double& sx, double (&r)[NL], double (&x)[NL]) {
+    double v[NL], g[NL], w[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) v[l] = fma(fac, c[l], u[l]);
+    op_.solve_w(fv, g);
+    op_.sweep(v, g, sv, om1, w);
+    op_.residual(fv, w, sw, r);
+    op_.sweep(w, g, sw, om1, x);
+    sv = trace_sum<NL>(v);
+    sw = trace_sum<NL>(w);
+    sx = trace_sum<NL>(x);
+  };
+  double svp = 0.0, swp = 0.0, sxp = 0.0;
+  if (me.ok && s0 + n0 > 0) {  // warm-up, as in updown_body_ops
+    double u[3][NL], fv[3][NL], e[2][NL], c[NL], r[NL], x[NL];
+    double sv = 0.0, sw = 0.0, sx = 0.0;
+    const bool h3 = s0 + n0 - 3 >= 0;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) e[0][l] = e[1][l] = u[0][l] = fv[0][l] = 0.0;
+    if (h3) load_nl<NL>(up + (n0 - 3) * slab, nx, u[0]);
+    load_nl<NL>(up + (n0 - 2) * slab, nx, u[1]);
+    load_nl<NL>(up + (n0 - 1) * slab, nx, u[2]);
+    load_nl<NL>(fp + (n0 - 2) * slab, nx, fv[1]);
+    load_nl<NL>(fp + (n0 - 1) * slab, nx, fv[2]);
+    if (has_c) {
+      if (h3) load_nl<NL>(ep + ((n0 >> 1) - 2) * cslab, nxc, e[0]);
+      load_nl<NL>(ep + ((n0 >> 1) - 1) * cslab, nxc, e[1]);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (k == 0 && !h3) continue;
+      if (k == 1) matvec_t<NL>(t.R1, e[1], c);
+      else matvec_t<NL>(t.R2, e[k == 0 ? 0 : 1], c);
+      step(u[k], fv[k], c, sv, sw, sx, r, x);
+    }
+    svp = sv;
+    swp = sw;
+    sxp = sx;
+  }
+
+  int st_use = 0, st_iss = kTmaStages - 1;
+  double* opn = op + n0 * slab;
+  double* fcn = fc + (n0 >> 1) * cslab + me.cidx;
+  const bool cst = me.cok && (tid & (NM - 1)) == 0;
+  for (i64 n = n0; n < nend; n += 2) {
+    if (CG) {
+      cp_async_wait<kTmaStages - 2>();  // this thread's chunks of stage st_use landed
+      __syncthreads();  // everyone's landed; everyone is done with stage st_iss
+      if (n + 2 * (kTmaStages - 1) < nend) issue_cg(n + 2 * (kTmaStages - 1), st_iss);
+      cp_async_commit();
+    } else {
+      __syncthreads();  // every thread is done with stage st_iss (read last pair)
+      if (threadIdx.x < 32 && n + 2 * (kTmaStages - 1) < nend)
+        issue(n + 2 * (kTmaStages - 1), st_iss);
+      mbar_wait(bar0 + 8u * st_use, (phase >> st_use) & 1u);
+      phase ^= 1u << st_use;
+    }
+    double u2[2][NL], f2[2][NL], ev[NL];
+    {
+      const double* r = ring + st_use * S::STAGE;
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          const int k = e * NL + l;
+          u2[e][l] = r[(k * NM + b) * SEG + ob + int((shu >> k) & 1u)];
+          f2[e][l] = r[(NU + k * NM + b) * SEG + ob + int((shf >> k) & 1u)];
+        }
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        const int sh = shift16(ec + (n >> 1) * cslab + l * nxc + cb);
+        const double v = r[(2 * NU + l) * SEG + oc + sh];
+        ev[l] = has_c ? v : 0.0;
+      }
+    }
+    st_use = (st_use == kTmaStages - 1) ? 0 : st_use + 1;
+    st_iss = (st_iss == kTmaStages - 1) ? 0 : st_iss + 1;
+    double acc[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) acc[l] = 0.0;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double c[NL], r[NL], x[NL], res[NL], rt[NL];
+      if (e == 0) matvec_t<NL>(t.R1, ev, c);
+      else matvec_t<NL>(t.R2, ev, c);
+      const double swq = swp, sxq = sxp;
+      step(u2[e], f2[e], c, svp, swp, sxp, r, x);
+      if (me.ok) {
+#pragma unroll
+        for (int l = 0; l < NL; ++l) st_global(opn + e * slab + l * nx, x[l]);
+      }
+      const double d = sxq - swq;
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        sumsq = fma(r[l], r[l], sumsq);
+        res[l] = fma(op_.ma[l], d, om1 * r[l]);
+      }
+      if (e == 0) matvec<NL>(t.R1, res, rt);
+      else matvec<NL>(t.R2, res, rt);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) acc[l] += me.fac * rt[l];
+    }
+    opn += 2 * slab;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) acc[l] = group_sum_full<DIM>(me.ok ? acc[l] : 0.0);
+    if (cst) {
+#pragma unroll
+      for (int l = 0; l < NL; ++l) st_global(fcn + l * nxc, acc[l]);
+    }
+    fcn += cslab;
+  }
+  return me.ok ? sumsq : 0.0;
+}
+
+template <int DIM, int NL>
+__global__ void __launch_bounds__(128) k_updown_tma(const double* __restrict__ ec,
+                                                    const PingPong pp,
+                                                    const double* __restrict__ f,
+                                                    double* __restrict__ fc,
+                                                    double* __restrict__ partials, const TM<NL> t,
+                                                    const SP s, const i64 n_t, const int C,
+                                                    const i64 n1c, const double omega,
+                                                    const i64 s0) {
+  __shared__ double sh[32];
+  extern __shared__ __align__(16) double ring[];
+  const unsigned bx = blockIdx.x, by = blockIdx.y;
+  const i64 tid = i64(bx) * blockDim.x + threadIdx.x;
+  const i64 n0 = i64(by) * C;
+  const i64 nend = min(n0 + i64(C), n_t);
+  const double sumsq =
+      updown_body_tma<DIM, NL>(tid, n0, nend, ec, pp, f, fc, t, s, n1c, omega, ring, s0);
+  pdl_trigger();
+  const double tot = block_sum(sumsq, sh);
+  if (threadIdx.x == 0) partials[i64(by) * gridDim.x + bx] = tot;
+}
+
+#ifndef STMG_UPDOWN_OPS
+#define STMG_UPDOWN_OPS 1
+#endif
+
 template <int DIM, int NL, int CO>
 __global__ void __launch_bounds__(128) k_updown(const double* __restrict__ ec, const PingPong pp,
                                                 const double* __restrict__ f,
@@ -579,7 +1115,9 @@ __global__ void __launch_bounds__(128) k_updown(const double* __restrict__ ec, c
   const i64 n0 = i64(by) * C;
   const i64 nend = min(n0 + i64(C), n_t);
   const double sumsq =
-      updown_body<DIM, NL, CO>(tid, n0, nend, ec, pp, f, fc, t, s, n1c, omega, ring, s0);
+      STMG_UPDOWN_OPS
+          ? updown_body_ops<DIM, NL, CO>(tid, n0, nend, ec, pp, f, fc, t, s, n1c, omega, ring, s0)
+          : updown_body<DIM, NL, CO>(tid, n0, nend, ec, pp, f, fc, t, s, n1c, omega, ring, s0);
   pdl_trigger();
   const double tot = block_sum(sumsq, sh);
   if (threadIdx.x == 0) partials[i64(by) * gridDim.x + bx] = tot;
@@ -2356,6 +2894,13 @@ cudaError_t launch_decide(cudaGraphConditionalHandle h, const double* norm, cons
   return cudaGetLastError();
 }
 
+#ifndef STMG_UPDOWN_SMEM_MIN
+#define STMG_UPDOWN_SMEM_MIN 0
+#endif
+// dynamic shared memory of k_updown: the ring, padded to STMG_UPDOWN_SMEM_MIN
+// bytes (caps the resident CTAs per SM; A/B knob)
+size_t updown_smem(int nl) { return std::max<size_t>(ring_bytes(5 * nl), STMG_UPDOWN_SMEM_MIN); }
+
 cudaError_t launch_updown(const LevelView& L, ModalArgs& a, const double* ec,
                           double* const* tbl, const int* par, const double* f, double* fc,
                           double* partials, cudaStream_t st, int64_t s0) {
@@ -2366,11 +2911,20 @@ cudaError_t launch_updown(const LevelView& L, ModalArgs& a, const double* ec,
   const PingPong pp{tbl, par};
   STMG_DISPATCH(L.sp.dim, L.tc.nl, {
     const TM<NL> t = make_tm<NL>(L.tc);
-    if (a.mode == 2)
-      PDLK(k_updown<DIM, NL, 2>, grid, 128, ring_bytes(5 * NL), st, ec, pp, f, fc, partials, t,
+#ifdef STMG_UPDOWN_CARVEOUT
+    cudaFuncSetAttribute(k_updown<DIM, NL, 2>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         STMG_UPDOWN_CARVEOUT);
+    cudaFuncSetAttribute(k_updown<DIM, NL, 1>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         STMG_UPDOWN_CARVEOUT);
+#endif
+    if (a.mode == 2 && STMG_UPDOWN_TMA && s.G % TmaShape<DIM, NL>::GPB == 0)
+      PDLK(k_updown_tma<DIM, NL>, grid, 128, TmaShape<DIM, NL>::smem, st, ec, pp, f, fc,
+           partials, t, s, L.n_t, a.chunk, a.n1c, a.omega, i64(s0));
+    else if (a.mode == 2)
+      PDLK(k_updown<DIM, NL, 2>, grid, 128, updown_smem(NL), st, ec, pp, f, fc, partials, t,
            s, L.n_t, a.chunk, a.n1c, a.omega, i64(s0));
     else
-      PDLK(k_updown<DIM, NL, 1>, grid, 128, ring_bytes(5 * NL), st, ec, pp, f, fc, partials, t,
+      PDLK(k_updown<DIM, NL, 1>, grid, 128, updown_smem(NL), st, ec, pp, f, fc, partials, t,
            s, L.n_t, a.chunk, L.sp.n1, a.omega, i64(s0));
   });
   return cudaGetLastError();

@@ -118,6 +118,82 @@ struct ModeLU {
   }
 };
 
+// Explicit per-mode operators of one damped Jacobi step, for the time-marching
+// kernels whose per-step chains are latency bound.  The DG jump is rank one,
+// N_tau = a 1^T with a_k = psi_k(0) and psi_l(tau) = 1 (stmg_setup.cpp:75), so
+//   sweep:    out = (1-w) cur + wAi f + h S(prev),   h = w A^-1 (M_j a)
+//   residual: r   = f - A cur + ma S(prev),          ma = M_j a
+// with S(v) = sum_l v_l (the end-of-step trace).  A^-1 comes from the same
+// elimination as ModeLU (column by column), once per thread.  Algebraically
+// identical to ModeLU::solve on f + M_j N prev; rounding differs at 1e-16.
+template <int NL>
+struct ModeOps {
+  double wAi[NL][NL];  // omega * A_j^-1
+  double A[NL][NL];    // A_j
+  double h[NL];        // omega * A_j^-1 (M_j a)
+  double ma[NL];       // M_j a
+  __device__ __forceinline__ ModeOps(const TM<NL>& t, double Mj, double Kj, double omega) {
+    const ModeLU<NL> lu(t, Mj, Kj);
+#pragma unroll
+    for (int i = 0; i < NL; ++i)
+#pragma unroll
+      for (int j = 0; j < NL; ++j) A[i][j] = Mj * t.K[i][j] + Kj * t.M[i][j];
+#pragma unroll
+    for (int c = 0; c < NL; ++c) {
+      double e[NL], x[NL];
+#pragma unroll
+      for (int i = 0; i < NL; ++i) e[i] = (i == c) ? 1.0 : 0.0;
+      lu.solve(e, x);
+#pragma unroll
+      for (int i = 0; i < NL; ++i) wAi[i][c] = omega * x[i];
+    }
+#pragma unroll
+    for (int i = 0; i < NL; ++i) ma[i] = Mj * t.N[i][0];
+#pragma unroll
+    for (int i = 0; i < NL; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < NL; ++j) s += wAi[i][j] * ma[j];
+      h[i] = s;
+    }
+  }
+  // g = omega A^-1 f (shared by the sweeps of one step)
+  __device__ __forceinline__ void solve_w(const double (&f)[NL], double (&g)[NL]) const {
+#pragma unroll
+    for (int i = 0; i < NL; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < NL; ++j) s = fma(wAi[i][j], f[j], s);
+      g[i] = s;
+    }
+  }
+  // out = (1-w) cur + g + h * sprev
+  __device__ __forceinline__ void sweep(const double (&cur)[NL], const double (&g)[NL],
+                                        double sprev, double om1, double (&out)[NL]) const {
+#pragma unroll
+    for (int i = 0; i < NL; ++i) out[i] = fma(h[i], sprev, fma(om1, cur[i], g[i]));
+  }
+  // r = f - A cur + ma * sprev
+  __device__ __forceinline__ void residual(const double (&f)[NL], const double (&cur)[NL],
+                                           double sprev, double (&r)[NL]) const {
+#pragma unroll
+    for (int i = 0; i < NL; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < NL; ++j) s = fma(A[i][j], cur[j], s);
+      r[i] = fma(ma[i], sprev, f[i] - s);
+    }
+  }
+};
+
+template <int NL>
+__device__ __forceinline__ double trace_sum(const double (&v)[NL]) {
+  double s = v[0];
+#pragma unroll
+  for (int l = 1; l < NL; ++l) s += v[l];
+  return s;
+}
+
 // y = A_j x
 template <int NL>
 __device__ __forceinline__ void apply_mode(const TM<NL>& t, double Mj, double Kj,
@@ -285,9 +361,26 @@ __device__ __forceinline__ double group_sum(double v) {
   return v;
 }
 
+// The same with a full-warp mask: only where every lane of the warp calls it.
+template <int DIM>
+__device__ __forceinline__ double group_sum_full(double v) {
+#pragma unroll
+  for (int o = 1; o < (1 << DIM); o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Plain global store (for pointers the compiler cannot prove global).
+__device__ __forceinline__ void st_global(double* p, double v) {
+  asm volatile("st.global.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
+}
+
 // cp.async (LDGSTS) helpers: 8-byte copies, zero fill when !valid.
 __device__ __forceinline__ void cp_async8(double* smem, const double* g, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(g),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async8s(unsigned s, const double* g, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(g),
                "r"(valid ? 8 : 0));
 }
