@@ -63,16 +63,13 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
   const i64 nx = s.nx, slab = NL * nx;
   const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
   const double om1 = 1.0 - omega;
-  const double Mj = me.Mj, Kj = me.Kj;
-  const ModeLU<NL> lu(t, Mj, Kj);
+  const ModeOps<NL> mo(t, me.Mj, me.Kj, omega);
   if (WAIT) pdl_wait();
   const double* fp = f + me.idx;
   const double* up = uin + me.idx;
   double* op = uout + me.idx;
 
-  double uo[NL], un[NL];
-#pragma unroll
-  for (int l = 0; l < NL; ++l) uo[l] = un[l] = 0.0;
+  double so = 0.0, sn = 0.0;  // traces of step n-1: old iterate, smoothed
 
   // (issued before the warm-up, whose loads and solve overlap their latency)
   // ASYNC: the loads of the next kRing-1 step pairs sit in a per-thread
@@ -109,27 +106,20 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
     }
   }
   if (me.ok && has_prev) {  // warm-up: smoothed step n0-1
-    double fv[NL], x[NL];
+    double fv[NL], g[NL], w[NL];
     ld_ro<COH, NL>(fp + (n0 - 1) * slab, nx, fv);
+    mo.solve_w(fv, g);
     if (ZERO) {
-      lu.solve(fv, x);
-#pragma unroll
-      for (int l = 0; l < NL; ++l) un[l] = omega * x[l];
+      sn = trace_sum<NL>(g);
     } else {
-      double u1[NL], u2[NL], nv[NL];
+      double u1[NL], u2[NL];
       ld_ro<COH, NL>(up + (n0 - 1) * slab, nx, u1);
 #pragma unroll
       for (int l = 0; l < NL; ++l) u2[l] = 0.0;
       if (has_prev2) ld_ro<COH, NL>(up + (n0 - 2) * slab, nx, u2);
-      matvec<NL>(t.N, u2, nv);
-#pragma unroll
-      for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
-      lu.solve(fv, x);
-#pragma unroll
-      for (int l = 0; l < NL; ++l) {
-        un[l] = om1 * u1[l] + omega * x[l];
-        uo[l] = u1[l];
-      }
+      mo.sweep(u1, g, trace_sum<NL>(u2), om1, w);
+      sn = trace_sum<NL>(w);
+      so = trace_sum<NL>(u1);
     }
   }
 
@@ -165,33 +155,23 @@ __device__ __forceinline__ void down_body(const i64 tid, const i64 n0, const i64
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const i64 m = n + e;
-      double rhs[NL], x[NL], w[NL];
-      if (!ZERO) {
-        double nv[NL];
-        matvec<NL>(t.N, uo, nv);
+      double g[NL], w[NL];
+      mo.solve_w(f2[e], g);
+      if (ZERO) {
 #pragma unroll
-        for (int l = 0; l < NL; ++l) rhs[l] = f2[e][l] + Mj * nv[l];
+        for (int l = 0; l < NL; ++l) w[l] = g[l];
       } else {
-#pragma unroll
-        for (int l = 0; l < NL; ++l) rhs[l] = f2[e][l];
+        mo.sweep(u2[e], g, so, om1, w);
       }
-      lu.solve(rhs, x);
-#pragma unroll
-      for (int l = 0; l < NL; ++l) w[l] = ZERO ? omega * x[l] : om1 * u2[e][l] + omega * x[l];
       if (me.ok) store_nl<NL>(op + m * slab, nx, w);
-      double aw[NL], np[NL], res[NL], rt[NL];
-      apply_mode<NL>(t, Mj, Kj, w, aw);
-      matvec<NL>(t.N, un, np);
-#pragma unroll
-      for (int l = 0; l < NL; ++l) res[l] = f2[e][l] - aw[l] + Mj * np[l];
+      double res[NL], rt[NL];
+      mo.residual(f2[e], w, sn, res);
       if (e == 0) matvec<NL>(t.R1, res, rt);
       else matvec<NL>(t.R2, res, rt);
 #pragma unroll
-      for (int l = 0; l < NL; ++l) {
-        acc[l] += (CO == 2) ? me.fac * rt[l] : rt[l];
-        if (!ZERO) uo[l] = u2[e][l];
-        un[l] = w[l];
-      }
+      for (int l = 0; l < NL; ++l) acc[l] += (CO == 2) ? me.fac * rt[l] : rt[l];
+      if (!ZERO) so = trace_sum<NL>(u2[e]);
+      sn = trace_sum<NL>(w);
     }
     if (!ASYNC) {
 #pragma unroll
@@ -226,8 +206,7 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
   const i64 nx = s.nx, slab = NL * nx;
   const i64 nxc = (CO == 2) ? ipow(n1c, DIM) : nx, cslab = NL * nxc;
   const double om1 = 1.0 - omega;
-  const double Mj = me.Mj, Kj = me.Kj;
-  const ModeLU<NL> lu(t, Mj, Kj);
+  const ModeOps<NL> mo(t, me.Mj, me.Kj, omega);
   if (WAIT) pdl_wait();
   const double fac = (CO == 2) ? me.fac : 1.0;
   const bool has_c = (CO == 2) ? me.cok : me.ok;
@@ -238,9 +217,10 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
   double sumsq = 0.0;
   if (!me.ok) return 0.0;
 
-  double vo[NL], wp[NL], ev[NL];
+  double so = 0.0, sw = 0.0;  // traces of step n-1: corrected, smoothed
+  double ev[NL];
 #pragma unroll
-  for (int l = 0; l < NL; ++l) vo[l] = wp[l] = ev[l] = 0.0;
+  for (int l = 0; l < NL; ++l) ev[l] = 0.0;
 
   // software pipeline (see down_body; issued before the warm-up); the
   // register prefetch is off for
@@ -280,13 +260,14 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
   }
   if (has_prev) {
     if (has_c) ld_ro<COH, NL>(ep + ((n0 >> 1) - 1) * cslab, nxc, ev);  // coarse step of n0-2, n0-1
-    double u1[NL], c1[NL];
+    double u1[NL], c1[NL], vo[NL];
     ld_ro<COH, NL>(up + (n0 - 1) * slab, nx, u1);
     matvec_t<NL>(t.R2, ev, c1);
 #pragma unroll
     for (int l = 0; l < NL; ++l) vo[l] = u1[l] + fac * c1[l];
+    so = trace_sum<NL>(vo);
     if (RESID) {
-      double v2[NL], fv[NL], nv[NL], x[NL];
+      double v2[NL], fv[NL], g[NL], w[NL];
 #pragma unroll
       for (int l = 0; l < NL; ++l) v2[l] = 0.0;
       if (has_prev2) {
@@ -297,12 +278,9 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
         for (int l = 0; l < NL; ++l) v2[l] = uu2[l] + fac * c2[l];
       }
       ld_ro<COH, NL>(fp + (n0 - 1) * slab, nx, fv);
-      matvec<NL>(t.N, v2, nv);
-#pragma unroll
-      for (int l = 0; l < NL; ++l) fv[l] += Mj * nv[l];
-      lu.solve(fv, x);
-#pragma unroll
-      for (int l = 0; l < NL; ++l) wp[l] = om1 * vo[l] + omega * x[l];
+      mo.solve_w(fv, g);
+      mo.sweep(vo, g, trace_sum<NL>(v2), om1, w);
+      sw = trace_sum<NL>(w);
     }
   }
 
@@ -345,33 +323,22 @@ __device__ __forceinline__ double up_body(const i64 tid, const i64 n0, const i64
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const i64 m = n + e;
-      double c[NL], v[NL], nv[NL], rhs[NL], x[NL], w[NL];
+      double c[NL], v[NL], g[NL], w[NL];
       if (e == 0) matvec_t<NL>(t.R1, ev, c);
       else matvec_t<NL>(t.R2, ev, c);
 #pragma unroll
       for (int l = 0; l < NL; ++l) v[l] = u2[e][l] + fac * c[l];
-      matvec<NL>(t.N, vo, nv);
-#pragma unroll
-      for (int l = 0; l < NL; ++l) rhs[l] = f2[e][l] + Mj * nv[l];
-      lu.solve(rhs, x);
-#pragma unroll
-      for (int l = 0; l < NL; ++l) w[l] = om1 * v[l] + omega * x[l];
+      mo.solve_w(f2[e], g);
+      mo.sweep(v, g, so, om1, w);
       store_nl<NL>(op + m * slab, nx, w);
       if (RESID) {
-        double aw[NL], np[NL];
-        apply_mode<NL>(t, Mj, Kj, w, aw);
-        matvec<NL>(t.N, wp, np);
+        double r[NL];
+        mo.residual(f2[e], w, sw, r);
 #pragma unroll
-        for (int l = 0; l < NL; ++l) {
-          const double r = f2[e][l] - aw[l] + Mj * np[l];
-          sumsq += r * r;
-        }
+        for (int l = 0; l < NL; ++l) sumsq = fma(r[l], r[l], sumsq);
       }
-#pragma unroll
-      for (int l = 0; l < NL; ++l) {
-        vo[l] = v[l];
-        wp[l] = w[l];
-      }
+      so = trace_sum<NL>(v);
+      sw = trace_sum<NL>(w);
     }
     if (PF && n + 2 < nend) {
 #pragma unroll
