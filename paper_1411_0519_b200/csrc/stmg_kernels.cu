@@ -1041,8 +1041,11 @@ __device__ __forceinline__ double updown_body_tma(const i64 tid, const i64 n0, c
   return me.ok ? sumsq : 0.0;
 }
 
+// p_t <= 1: 96 registers, 5 CTAs per SM (C2 1.78 -> 1.73 ms per solve; the
+// 1024-CTA grid of C2 then runs in 1.4 instead of 1.7 waves); p_t = 2 would
+// spill at 96 (C3 106 -> 157 ms), so no bound there
 template <int DIM, int NL>
-__global__ void __launch_bounds__(128) k_updown_tma(const double* __restrict__ ec,
+__global__ void __launch_bounds__(128, (NL <= 2 ? 5 : 1)) k_updown_tma(const double* __restrict__ ec,
                                                     const PingPong pp,
                                                     const double* __restrict__ f,
                                                     double* __restrict__ fc,
