@@ -2123,6 +2123,9 @@ __host__ __device__ constexpr int dst_pad(int i) { return i + (i >> 4); }
 // A team of TS = L / V threads owns one length-L FFT; every thread holds V
 // values per pass (one radix-16 butterfly, or 16/R radix-R ones), so a pass
 // is: load to registers, team barrier, store (in place), team barrier.
+#ifndef STMG_DST_BUFPAD
+#define STMG_DST_BUFPAD 1
+#endif
 template <int LOG2N>
 struct DSTShape {
   static constexpr int N = 1 << LOG2N;
@@ -2134,9 +2137,11 @@ struct DSTShape {
   static constexpr int BLOCK = TS > 128 ? TS : 128;
   static constexpr int F = BLOCK / TS;  // FFTs (= line pairs) per block
   static constexpr int TL = 2 * F;      // lines per block
-  // padded FFT buffer; +4 double2 puts consecutive FFTs 64 B apart in the
-  // bank space, so the line-pair scatter of a warp is conflict-free
-  static constexpr int BUF = L + L / 16 + 4;
+  // padded FFT buffer.  STMG_DST_BUFPAD = 1 makes BUF odd in 16-byte units
+  // (L >= 128): the F line pairs of a strided (y/z) pass, which a warp's
+  // lanes scatter to / gather from at one index, then hit F distinct bank
+  // groups; with +4 (BUF = 4 mod 8) they hit two and conflict 2-4 ways
+  static constexpr int BUF = L + L / 16 + STMG_DST_BUFPAD;
   static constexpr int KB = (L / 2 + TS - 1) / TS;  // recurrence values per thread
   static constexpr size_t smem = size_t(F) * BUF * sizeof(double2) + size_t(BLOCK) * sizeof(double2);
 };
