@@ -1045,7 +1045,10 @@ __device__ __forceinline__ double updown_body_tma(const i64 tid, const i64 n0, c
 // 1024-CTA grid of C2 then runs in 1.4 instead of 1.7 waves); p_t = 2 would
 // spill at 96 (C3 106 -> 157 ms), so no bound there
 template <int DIM, int NL>
-__global__ void __launch_bounds__(128, (NL <= 2 ? 5 : 1)) k_updown_tma(const double* __restrict__ ec,
+#ifndef STMG_UPDOWN_MINB3
+#define STMG_UPDOWN_MINB3 3  // p_t = 2: 168 registers, 3 CTAs/SM (C3 108 -> 104 ms); 4 spills
+#endif
+__global__ void __launch_bounds__(128, (NL <= 2 ? 5 : NL == 3 ? STMG_UPDOWN_MINB3 : 1)) k_updown_tma(const double* __restrict__ ec,
                                                     const PingPong pp,
                                                     const double* __restrict__ f,
                                                     double* __restrict__ fc,
