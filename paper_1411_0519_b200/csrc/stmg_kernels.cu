@@ -1069,6 +1069,336 @@ __global__ void __launch_bounds__(128, (NL <= 2 ? 5 : NL == 3 ? STMG_UPDOWN_MINB
   if (threadIdx.x == 0) partials[i64(by) * gridDim.x + bx] = tot;
 }
 
+// ---- Row-run staging for the per-level kernels (k_down / k_up) -----------
+// The loader of updown_body_tma (STMG_UPDOWN_TMA = 2) as a reusable piece:
+// NA fine arrays (2 steps x NL components x 2^DIM member runs each) plus,
+// with HC, the NL coarse runs of the block's coarse modes, copied with
+// 16-byte cp.async.cg chunks into kTmaStages stages.
+template <int DIM, int NL, int NA, bool HC>
+struct RowRuns {
+  static constexpr int NM = 1 << DIM, GPB = 128 / NM, SEG = GPB + 2;
+  static constexpr int NF = NA * 2 * NL * NM;  // fine slots
+  static constexpr int NC = NF + (HC ? NL : 0);
+  static constexpr int STAGE = NC * SEG;
+  static constexpr int HCH = SEG / 2, NCH = NC * HCH, KPT = (NCH + 127) / 128;
+  static constexpr size_t smem = size_t(kTmaStages) * STAGE * sizeof(double);
+  const double* csrc[KPT];
+  unsigned cdst[KPT];
+  const double* ecb;  // coarse array + the block's coarse run start
+  i64 slab, nxc, cslab;
+  unsigned ring_s, sh;
+  int ob, oc, b;
+  // segb: NM + 1 shared i64 (written here, one __syncthreads inside)
+  __device__ __forceinline__ void init(const double* const (&arr)[NA], const double* ec,
+                                       const Member& me, const i64 nx, const i64 slab_,
+                                       const i64 nxc_, const i64 cslab_, double* ring,
+                                       i64* segb) {
+    b = int(threadIdx.x) & (NM - 1);
+    if (threadIdx.x < NM) {  // group 0 of the block, member b: its run's first mode
+      segb[b] = (b & 1) ? me.idx - (GPB - 1) : me.idx;
+      if (b == 0) segb[NM] = me.cidx;
+    }
+    __syncthreads();
+    slab = slab_;
+    nxc = nxc_;
+    cslab = cslab_;
+    const i64 sb = segb[b], cb = segb[NM];
+    ob = int(me.idx - sb);
+    oc = int(me.cidx - cb);
+    ecb = HC ? ec + cb : nullptr;
+    sh = 0;
+#pragma unroll
+    for (int a = 0; a < NA; ++a)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int l = 0; l < NL; ++l)
+          sh |= unsigned(shift16(arr[a] + e * slab + l * nx + sb)) << ((a * 2 + e) * NL + l);
+    ring_s = static_cast<unsigned>(__cvta_generic_to_shared(ring));
+#pragma unroll
+    for (int i = 0; i < KPT; ++i) {
+      const int k = int(threadIdx.x) + 128 * i;
+      const int c = k / HCH, j = k - c * HCH;
+      cdst[i] = unsigned(c * SEG + 2 * j) * 8u;
+      csrc[i] = nullptr;
+      if (c < NF) {
+        const int a = c / (2 * NL * NM), r = c - a * (2 * NL * NM);
+        const int m = r % NM, el = r / NM, e = el / NL, l = el - e * NL;
+        const double* base = arr[0];
+#pragma unroll
+        for (int q = 1; q < NA; ++q)
+          if (a == q) base = arr[q];
+        csrc[i] = align16(base + e * slab + l * nx + segb[m]) + 2 * j;
+      }
+    }
+  }
+  __device__ __forceinline__ void issue(const i64 n, const int st) const {
+    const unsigned base = ring_s + unsigned(st * STAGE) * 8u;
+#pragma unroll
+    for (int i = 0; i < KPT; ++i) {
+      const int k = int(threadIdx.x) + 128 * i;
+      if (k >= NCH) break;
+      const int c = k / HCH;
+      const double* src;
+      if (!HC || c < NF) {
+        src = csrc[i] + n * slab;
+      } else {
+        const int l = c - NF, j = k - c * HCH;
+        src = align16(ecb + (n >> 1) * cslab + l * nxc) + 2 * j;
+      }
+      cp_async16cg(base + cdst[i], src);
+    }
+  }
+  __device__ __forceinline__ double fine(const double* ring, int st, int a, int e, int l) const {
+    const int q = (a * 2 + e) * NL + l;
+    return ring[st * STAGE + (q * NM + b) * SEG + ob + int((sh >> q) & 1u)];
+  }
+  __device__ __forceinline__ double coarse(const double* ring, int st, int l, i64 n) const {
+    return ring[st * STAGE + (NF + l) * SEG + oc + shift16(ecb + (n >> 1) * cslab + l * nxc)];
+  }
+};
+
+// k_down on row runs: damped Jacobi sweep + residual + full-weighting
+// restriction (down_body, CO = 2) with the loads staged by RowRuns.
+template <int DIM, int NL, bool ZERO>
+__global__ void __launch_bounds__(128) k_down_rr(const double* __restrict__ f,
+                                                 const double* __restrict__ uin,
+                                                 double* __restrict__ uout,
+                                                 double* __restrict__ fc, const TM<NL> t,
+                                                 const SP s, const i64 n_t, const int C,
+                                                 const i64 n1c, const double omega,
+                                                 const bool first_global) {
+  using RR = RowRuns<DIM, NL, ZERO ? 1 : 2, false>;
+  constexpr int NM = RR::NM;
+  extern __shared__ __align__(16) double ring[];
+  __shared__ i64 segb[NM + 1];
+  const i64 tid = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 n0 = i64(blockIdx.y) * C;
+  const i64 nend = min(n0 + i64(C), n_t);
+  const bool has_prev = n0 > 0 || !first_global, has_prev2 = n0 - 1 > 0 || !first_global;
+  const Member me = make_member<DIM>(s, tid, n1c, true);
+  const i64 nx = s.nx, slab = NL * nx;
+  const i64 nxc = ipow(n1c, DIM), cslab = NL * nxc;
+  const double om1 = 1.0 - omega;
+  const ModeOps<NL> mo(t, me.Mj, me.Kj, omega);
+  RR rr;
+  const double* arrs[ZERO ? 1 : 2] = {f};
+  if (!ZERO) arrs[ZERO ? 0 : 1] = uin;
+  rr.init(arrs, nullptr, me, nx, slab, nxc, cslab, ring, segb);
+  pdl_wait();
+#pragma unroll
+  for (int q = 0; q < kTmaStages - 1; ++q) {
+    if (n0 + 2 * q < nend) rr.issue(n0 + 2 * q, q);
+    cp_async_commit();
+  }
+  const double* fp = f + me.idx;
+  const double* up = uin + me.idx;
+  double so = 0.0, sn = 0.0;  // traces of step n-1: old iterate, smoothed
+  if (me.ok && has_prev) {  // warm-up: smoothed step n0-1
+    double fv[NL], g[NL], w[NL];
+    load_nl<NL>(fp + (n0 - 1) * slab, nx, fv);
+    mo.solve_w(fv, g);
+    if (ZERO) {
+      sn = trace_sum<NL>(g);
+    } else {
+      double u1[NL], u2[NL];
+      load_nl<NL>(up + (n0 - 1) * slab, nx, u1);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) u2[l] = 0.0;
+      if (has_prev2) load_nl<NL>(up + (n0 - 2) * slab, nx, u2);
+      mo.sweep(u1, g, trace_sum<NL>(u2), om1, w);
+      sn = trace_sum<NL>(w);
+      so = trace_sum<NL>(u1);
+    }
+  }
+  int st_use = 0, st_iss = kTmaStages - 1;
+  double* opn = uout + me.idx + n0 * slab;
+  double* fcn = fc + (n0 >> 1) * cslab + me.cidx;
+  const bool cst = me.cok && (tid & (NM - 1)) == 0;
+  for (i64 n = n0; n < nend; n += 2) {
+    cp_async_wait<kTmaStages - 2>();
+    __syncthreads();
+    if (n + 2 * (kTmaStages - 1) < nend) rr.issue(n + 2 * (kTmaStages - 1), st_iss);
+    cp_async_commit();
+    double f2[2][NL], u2[2][NL];
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        f2[e][l] = rr.fine(ring, st_use, 0, e, l);
+        u2[e][l] = ZERO ? 0.0 : rr.fine(ring, st_use, ZERO ? 0 : 1, e, l);
+      }
+    st_use = (st_use == kTmaStages - 1) ? 0 : st_use + 1;
+    st_iss = (st_iss == kTmaStages - 1) ? 0 : st_iss + 1;
+    double acc[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) acc[l] = 0.0;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double g[NL], w[NL], res[NL], rt[NL];
+      mo.solve_w(f2[e], g);
+      if (ZERO) {
+#pragma unroll
+        for (int l = 0; l < NL; ++l) w[l] = g[l];
+      } else {
+        mo.sweep(u2[e], g, so, om1, w);
+      }
+      if (me.ok) {
+#pragma unroll
+        for (int l = 0; l < NL; ++l) st_global(opn + e * slab + l * nx, w[l]);
+      }
+      mo.residual(f2[e], w, sn, res);
+      if (e == 0) matvec<NL>(t.R1, res, rt);
+      else matvec<NL>(t.R2, res, rt);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) acc[l] += me.fac * rt[l];
+      if (!ZERO) so = trace_sum<NL>(u2[e]);
+      sn = trace_sum<NL>(w);
+    }
+    opn += 2 * slab;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) acc[l] = group_sum_full<DIM>(me.ok ? acc[l] : 0.0);
+    if (cst) {
+#pragma unroll
+      for (int l = 0; l < NL; ++l) st_global(fcn + l * nxc, acc[l]);
+    }
+    fcn += cslab;
+  }
+  pdl_trigger();
+}
+
+// k_up on row runs: prolongation + correction + damped Jacobi sweep
+// (+ residual sum of squares) (up_body, CO = 2) with RowRuns loads.
+template <int DIM, int NL, bool RESID>
+__global__ void __launch_bounds__(128) k_up_rr(const double* __restrict__ ec,
+                                               const double* __restrict__ uin,
+                                               const double* __restrict__ f,
+                                               double* __restrict__ uout,
+                                               double* __restrict__ partials, const TM<NL> t,
+                                               const SP s, const i64 n_t, const int C,
+                                               const i64 n1c, const double omega,
+                                               const bool first_global) {
+  using RR = RowRuns<DIM, NL, 2, true>;
+  constexpr int NM = RR::NM;
+  extern __shared__ __align__(16) double ring[];
+  __shared__ i64 segb[NM + 1];
+  __shared__ double sh[32];
+  const unsigned bx = blockIdx.x, by = blockIdx.y;
+  const i64 tid = i64(bx) * blockDim.x + threadIdx.x;
+  const i64 n0 = i64(by) * C;
+  const i64 nend = min(n0 + i64(C), n_t);
+  const bool has_prev = n0 > 0 || !first_global, has_prev2 = n0 - 1 > 0 || !first_global;
+  const Member me = make_member<DIM>(s, tid, n1c, true);
+  const i64 nx = s.nx, slab = NL * nx;
+  const i64 nxc = ipow(n1c, DIM), cslab = NL * nxc;
+  const double om1 = 1.0 - omega;
+  const ModeOps<NL> mo(t, me.Mj, me.Kj, omega);
+  const double fac = me.fac;
+  const bool has_c = me.cok;
+  RR rr;
+  const double* arrs[2] = {uin, f};
+  rr.init(arrs, ec, me, nx, slab, nxc, cslab, ring, segb);
+  pdl_wait();
+#pragma unroll
+  for (int q = 0; q < kTmaStages - 1; ++q) {
+    if (n0 + 2 * q < nend) rr.issue(n0 + 2 * q, q);
+    cp_async_commit();
+  }
+  const double* ep = ec + me.cidx;
+  const double* fp = f + me.idx;
+  const double* up = uin + me.idx;
+  double so = 0.0, sw = 0.0;  // traces of step n-1: corrected, smoothed
+  double sumsq = 0.0;
+  if (me.ok && has_prev) {
+    double ev[NL], u1[NL], c1[NL], vo[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) ev[l] = 0.0;
+    if (has_c) load_nl<NL>(ep + ((n0 >> 1) - 1) * cslab, nxc, ev);  // coarse step of n0-2, n0-1
+    load_nl<NL>(up + (n0 - 1) * slab, nx, u1);
+    matvec_t<NL>(t.R2, ev, c1);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) vo[l] = u1[l] + fac * c1[l];
+    so = trace_sum<NL>(vo);
+    if (RESID) {
+      double v2[NL], fv[NL], g[NL], w[NL];
+#pragma unroll
+      for (int l = 0; l < NL; ++l) v2[l] = 0.0;
+      if (has_prev2) {
+        double uu2[NL], c2[NL];
+        load_nl<NL>(up + (n0 - 2) * slab, nx, uu2);
+        matvec_t<NL>(t.R1, ev, c2);
+#pragma unroll
+        for (int l = 0; l < NL; ++l) v2[l] = uu2[l] + fac * c2[l];
+      }
+      load_nl<NL>(fp + (n0 - 1) * slab, nx, fv);
+      mo.solve_w(fv, g);
+      mo.sweep(vo, g, trace_sum<NL>(v2), om1, w);
+      sw = trace_sum<NL>(w);
+    }
+  }
+  int st_use = 0, st_iss = kTmaStages - 1;
+  double* opn = uout + me.idx + n0 * slab;
+  for (i64 n = n0; n < nend; n += 2) {
+    cp_async_wait<kTmaStages - 2>();
+    __syncthreads();
+    if (n + 2 * (kTmaStages - 1) < nend) rr.issue(n + 2 * (kTmaStages - 1), st_iss);
+    cp_async_commit();
+    double u2[2][NL], f2[2][NL], ev[NL];
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
+        u2[e][l] = rr.fine(ring, st_use, 0, e, l);
+        f2[e][l] = rr.fine(ring, st_use, 1, e, l);
+      }
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      const double v = rr.coarse(ring, st_use, l, n);
+      ev[l] = has_c ? v : 0.0;
+    }
+    st_use = (st_use == kTmaStages - 1) ? 0 : st_use + 1;
+    st_iss = (st_iss == kTmaStages - 1) ? 0 : st_iss + 1;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double c[NL], v[NL], g[NL], w[NL];
+      if (e == 0) matvec_t<NL>(t.R1, ev, c);
+      else matvec_t<NL>(t.R2, ev, c);
+#pragma unroll
+      for (int l = 0; l < NL; ++l) v[l] = u2[e][l] + fac * c[l];
+      mo.solve_w(f2[e], g);
+      mo.sweep(v, g, so, om1, w);
+      if (me.ok) {
+#pragma unroll
+        for (int l = 0; l < NL; ++l) st_global(opn + e * slab + l * nx, w[l]);
+      }
+      if (RESID) {
+        double r[NL];
+        mo.residual(f2[e], w, sw, r);
+#pragma unroll
+        for (int l = 0; l < NL; ++l) sumsq = fma(r[l], r[l], sumsq);
+      }
+      so = trace_sum<NL>(v);
+      sw = trace_sum<NL>(w);
+    }
+    opn += 2 * slab;
+  }
+  pdl_trigger();
+  if (RESID) {
+    const double tot = block_sum(me.ok ? sumsq : 0.0, sh);
+    if (threadIdx.x == 0) partials[i64(by) * gridDim.x + bx] = tot;
+  }
+}
+
+#ifndef STMG_LEVEL_RR
+#define STMG_LEVEL_RR 1
+#endif
+// row runs only for large levels: on small, latency-bound ones (C2 level 1,
+// 1M dofs, 4-step chunks) the per-pair CTA barrier costs more than the L1
+// relief gains (C2 1.77 -> 1.84 ms with row runs on every level)
+#ifndef STMG_LEVEL_RR_MIN
+#define STMG_LEVEL_RR_MIN (i64(1) << 22)
+#endif
+
 #ifndef STMG_UPDOWN_OPS
 #define STMG_UPDOWN_OPS 1
 #endif
@@ -3011,7 +3341,15 @@ cudaError_t launch_down(const LevelView& L, ModalArgs& a, bool zero_guess, const
   const dim3 grid(grid1(lanes, 128), unsigned((L.n_t + a.chunk - 1) / a.chunk));
   STMG_DISPATCH(L.sp.dim, L.tc.nl, {
     const TM<NL> t = make_tm<NL>(L.tc);
-    if (a.mode == 2) {
+    if (a.mode == 2 && STMG_LEVEL_RR && L.size() >= STMG_LEVEL_RR_MIN &&
+        s.G % RowRuns<DIM, NL, 1, false>::GPB == 0) {
+      if (zero_guess)
+        PDLK(k_down_rr<DIM, NL, true>, grid, 128, RowRuns<DIM, NL, 1, false>::smem, st, f, u_in,
+             u_out, fc, t, s, L.n_t, a.chunk, a.n1c, a.omega, L.first_global);
+      else
+        PDLK(k_down_rr<DIM, NL, false>, grid, 128, RowRuns<DIM, NL, 2, false>::smem, st, f, u_in,
+             u_out, fc, t, s, L.n_t, a.chunk, a.n1c, a.omega, L.first_global);
+    } else if (a.mode == 2) {
       if (zero_guess)
         PDLK(k_down<DIM, NL, true, 2>, grid, 128, ring_bytes(2 * NL), st, f, u_in, u_out, fc, t, s, L.n_t, a.chunk,
                                                       a.n1c, a.omega, L.first_global);
@@ -3039,7 +3377,15 @@ cudaError_t launch_up(const LevelView& L, ModalArgs& a, const double* ec, const 
   STMG_DISPATCH(L.sp.dim, L.tc.nl, {
     const TM<NL> t = make_tm<NL>(L.tc);
     const i64 n1c = a.mode == 2 ? a.n1c : L.sp.n1;
-    if (a.mode == 2) {
+    if (a.mode == 2 && STMG_LEVEL_RR && L.size() >= STMG_LEVEL_RR_MIN &&
+        s.G % RowRuns<DIM, NL, 2, true>::GPB == 0) {
+      if (partials)
+        PDLK(k_up_rr<DIM, NL, true>, grid, 128, RowRuns<DIM, NL, 2, true>::smem, st, ec, u_in, f,
+             u_out, partials, t, s, L.n_t, a.chunk, n1c, a.omega, L.first_global);
+      else
+        PDLK(k_up_rr<DIM, NL, false>, grid, 128, RowRuns<DIM, NL, 2, true>::smem, st, ec, u_in, f,
+             u_out, partials, t, s, L.n_t, a.chunk, n1c, a.omega, L.first_global);
+    } else if (a.mode == 2) {
       if (partials)
         PDLK(k_up<DIM, NL, 2, true>, grid, 128, ring_bytes(5 * NL), st, ec, u_in, f, u_out, partials, t, s, L.n_t,
                                                     a.chunk, n1c, a.omega, L.first_global);
