@@ -1916,6 +1916,9 @@ __device__ __forceinline__ void stencil_smem(const double* s, int tx, int ty, in
   }
 }
 
+#ifndef STMG_APPLY_FREG
+#define STMG_APPLY_FREG 1
+#endif
 template <int DIM, int NL, bool RES>
 __global__ void __launch_bounds__(ResTile<DIM>::THREADS) k_apply(
     const double* __restrict__ u, const double* __restrict__ f, double* __restrict__ y,
@@ -1953,7 +1956,11 @@ __global__ void __launch_bounds__(ResTile<DIM>::THREADS) k_apply(
   // residual, this tile's f of step m; STAGES - 1 steps are in flight while
   // one is computed (the kernel is latency bound with a single slab ahead)
   constexpr int NS = T::STAGES;
-  constexpr int FS = RES ? NL * T::THREADS : 0;
+  // FREG: f goes straight to registers one step ahead instead of through the
+  // shared-memory ring (the ring's 8-byte LDGSTS + LDS traffic is what bounds
+  // this kernel: L1 throughput 83 % on C2)
+  constexpr bool FREG = RES && STMG_APPLY_FREG;
+  constexpr int FS = (RES && !FREG) ? NL * T::THREADS : 0;
   constexpr int SS = BS + FS;  // doubles per stage
   auto stage = [&](int m) { return dsm + ((m + NS) % NS) * SS; };
   StagePlan<DIM, NL> plan;
@@ -1961,7 +1968,7 @@ __global__ void __launch_bounds__(ResTile<DIM>::THREADS) k_apply(
   auto issue = [&](i64 n) {  // slab n -> stage (n - n0 + 1) mod NS
     double* st = stage(int(n - n0 + 1));
     stage_slab<DIM, NL>(st, u, n, nx, plan);
-    if (RES) {
+    if (RES && !FREG) {
 #pragma unroll
       for (int k = 0; k < NL; ++k)
         cp_async8(st + BS + k * T::THREADS + threadIdx.x,
@@ -1987,8 +1994,19 @@ __global__ void __launch_bounds__(ResTile<DIM>::THREADS) k_apply(
       mw_prev += b[l] * Mv;
     }
   }
+  double fc[NL], fn[NL];
+#pragma unroll
+  for (int k = 0; k < NL; ++k) fc[k] = fn[k] = 0.0;
+  if (FREG && inside && n0 < nend) {
+#pragma unroll
+    for (int k = 0; k < NL; ++k) fc[k] = __ldcs(f + n0 * slab + k * nx + r);
+  }
   for (i64 n = n0; n < nend; ++n) {
     const int j = int(n - n0 + 1);
+    if (FREG && inside && n + 1 < nend) {
+#pragma unroll
+      for (int k = 0; k < NL; ++k) fn[k] = __ldcs(f + (n + 1) * slab + k * nx + r);
+    }
     cp_async_wait<NS - 2>();  // groups up to step n landed
     __syncthreads();          // slab n visible; stage of n - 1 free
     if (n + NS - 1 < nend) issue(n + NS - 1);
@@ -2008,9 +2026,14 @@ __global__ void __launch_bounds__(ResTile<DIM>::THREADS) k_apply(
         for (int l = 0; l < NL; ++l) acc += MU[l] * t.K[k][l] + KU[l] * t.M[k][l];
         acc -= a[k] * mw_prev;
         const i64 o = n * slab + k * nx + r;
-        __stcs(y + o, RES ? st[BS + k * T::THREADS + threadIdx.x] - acc : acc);
+        const double fv = FREG ? fc[k] : (RES ? st[BS + k * T::THREADS + threadIdx.x] : 0.0);
+        __stcs(y + o, RES ? fv - acc : acc);
       }
       mw_prev = mw;
+    }
+    if (FREG) {
+#pragma unroll
+      for (int k = 0; k < NL; ++k) fc[k] = fn[k];
     }
   }
 }
@@ -3023,9 +3046,10 @@ cudaError_t launch_apply(const LevelView& L, const double* u, const double* f, d
     C = std::min<i64>(C, L.n_t);
     const dim3 g(unsigned(tiles), unsigned((L.n_t + C - 1) / C));
     const TM<NL> t = make_tm<NL>(L.tc);
-    const size_t smem = size_t(T::STAGES) *
-                        (size_t(NL) * T::HALO + (residual ? size_t(NL) * T::THREADS : 0)) *
-                        sizeof(double);
+    const size_t smem =
+        size_t(T::STAGES) *
+        (size_t(NL) * T::HALO + (residual && !STMG_APPLY_FREG ? size_t(NL) * T::THREADS : 0)) *
+        sizeof(double);
     static bool attr = false;
     if (!attr) {
       const int most = int(T::STAGES * 2 * size_t(NL) * T::HALO * sizeof(double));  // >= smem
