@@ -201,6 +201,19 @@ int stmg_solve(stmg_ctx* ctx, const double* f, double* u,
 int stmg_solve_host(stmg_ctx* ctx, const double* f_host, double* u_host,
                     const stmg_cycle_config* cfg, double eps, int max_iter,
                     double* history, int history_cap, stmg_solve_report* report);
+/* Extension (no reference counterpart; solve, mg.cpp:134-166, takes one f per
+ * call): a batch of independent solves (many right-hand sides / initial
+ * guesses) streamed through one context.  Problem i solves from u0_host[i]
+ * (u0_host NULL: u_host[i] in place) into u_host[i] while the H2D of problem
+ * i+1 and the D2H of problem i-1 run on the copy engines (two device staging
+ * sets).  Each result is bitwise stmg_solve_host's.  reports (optional) gets
+ * count entries; wall_time_seconds there is per solve, without the overlapped
+ * copies.  Host buffers should be pinned (stmg_host_alloc) for the copies to
+ * overlap. */
+int stmg_solve_host_batch(stmg_ctx* ctx, int count, const double* const* f_host,
+                          const double* const* u0_host, double* const* u_host,
+                          const stmg_cycle_config* cfg, double eps,
+                          int max_iter, stmg_solve_report* reports);
 
 /* ---- multi-GPU: time slabs over ranks (one process per GPU, NCCL) ------- */
 /* 128-byte NCCL unique id, created on rank 0 and broadcast by the caller. */

@@ -98,6 +98,8 @@ SIGNATURES = [
                              C.POINTER(SolveReport)]),
     ("stmg_solve_host", C.c_int, [VP, VP, VP, C.POINTER(CycleConfig), D, C.c_int, PD, C.c_int,
                                   C.POINTER(SolveReport)]),
+    ("stmg_solve_host_batch", C.c_int, [VP, C.c_int, VP, VP, VP, C.POINTER(CycleConfig), D,
+                                        C.c_int, C.POINTER(SolveReport)]),
     ("stmg_nccl_unique_id", C.c_int, [VP, C.c_size_t]),
     ("stmg_create_distributed", C.c_int, [C.POINTER(HierarchyParams), C.c_int, C.c_int, VP,
                                           C.c_size_t, C.POINTER(VP)]),

@@ -141,7 +141,12 @@ struct stmg_ctx {
   double* d_hist = nullptr;
   int hist_cap = 0;
   double* h_norm = nullptr;  // pinned
-  DevBuf user_f, user_u;     // for stmg_solve_host
+  DevBuf user_f, user_u;     // for stmg_solve_host (and set 0 of the batch)
+  // stmg_solve_host_batch: second staging set, copy streams and their events
+  DevBuf user_f2, user_u2;
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  cudaEvent_t ev_done = nullptr;
   // graphs of one spectral V-cycle keyed by (cfg, starting buffer parity)
   struct GraphKey {
     int nu1, nu2, gamma, cur0;
@@ -2106,6 +2111,12 @@ int stmg_destroy(stmg_ctx* c) {
     for (auto& kv : c->cop) cudaFree(kv.second);
     c->user_f.release();
     c->user_u.release();
+    c->user_f2.release();
+    c->user_u2.release();
+    for (cudaEvent_t e : {c->ev_in[0], c->ev_in[1], c->ev_free[0], c->ev_free[1], c->ev_done})
+      if (e) cudaEventDestroy(e);
+    if (c->s_in) cudaStreamDestroy(c->s_in);
+    if (c->s_out) cudaStreamDestroy(c->s_out);
     for (auto& s : c->prof) {
       for (auto& e : s.pool) {
         cudaEventDestroy(e.first);
@@ -2424,6 +2435,77 @@ int stmg_solve_host(stmg_ctx* c, const double* f_host, double* u_host,
     r.wall_time_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (report) *report = r;
+  });
+}
+
+// Streams a batch of independent solves through one context: the H2D of
+// problem i+1 (copy stream s_in) and the D2H of problem i-1 (s_out) run on the
+// two copy engines while problem i solves on the context stream, with two
+// device staging sets {f, u} in ping-pong.  Each solve is exactly
+// stmg_solve_host's (same kernels, same result bits); only the copies overlap.
+int stmg_solve_host_batch(stmg_ctx* c, int count, const double* const* f_host,
+                          const double* const* u0_host, double* const* u_host,
+                          const stmg_cycle_config* cfg, double eps, int max_iter,
+                          stmg_solve_report* reports) {
+  return guard([&] {
+    require(c != nullptr, "null context");
+    check_cfg(cfg);
+    require(count >= 0, "count must be >= 0");
+    if (count == 0) return;
+    require(f_host != nullptr && u_host != nullptr, "null vector array");
+    for (int i = 0; i < count; ++i)
+      require(f_host[i] && u_host[i] && (!u0_host || u0_host[i]), "null vector");
+    require(eps > 0.0, "eps_mg must be positive");
+    require(max_iter >= 0, "max_iter must be >= 0");
+    Level& L0 = c->levels[0];
+    const i64 n = (c->shards && c->shards->nccl) ? L0.view.size() / c->shards->S : L0.view.size();
+    const size_t bytes = size_t(n) * sizeof(double);
+    DevBuf* F[2] = {&c->user_f, &c->user_f2};
+    DevBuf* U[2] = {&c->user_u, &c->user_u2};
+    for (int s = 0; s < 2; ++s) {
+      ensure(*F[s], n);
+      ensure(*U[s], n);
+    }
+    if (!c->s_in) {
+      CK(cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking));
+      for (int s = 0; s < 2; ++s) {
+        CK(cudaEventCreateWithFlags(&c->ev_in[s], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_free[s], cudaEventDisableTiming));
+      }
+      CK(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+    }
+    // set s may be refilled once the D2H of its previous problem has drained
+    // (its f was consumed by that solve's forward transform before that)
+    CK(cudaStreamSynchronize(c->s_out));
+    auto upload = [&](int i) {
+      const int s = i & 1;
+      const double* u0 = u0_host ? u0_host[i] : u_host[i];
+      if (i >= 2) CK(cudaStreamWaitEvent(c->s_in, c->ev_free[s], 0));
+      CK(cudaMemcpyAsync(F[s]->base, f_host[i], bytes, cudaMemcpyHostToDevice, c->s_in));
+      CK(cudaMemcpyAsync(U[s]->base, u0, bytes, cudaMemcpyHostToDevice, c->s_in));
+      CK(cudaEventRecord(c->ev_in[s], c->s_in));
+    };
+    upload(0);
+    for (int i = 0; i < count; ++i) {
+      const int s = i & 1;
+      if (i + 1 < count) upload(i + 1);
+      CK(cudaStreamWaitEvent(c->stream, c->ev_in[s], 0));
+      const auto t0 = std::chrono::steady_clock::now();
+      stmg_solve_report r{};
+      if (c->shards)
+        solve_sharded(c, F[s]->base, U[s]->base, *cfg, eps, max_iter, nullptr, 0, &r);
+      else
+        solve_impl(c, F[s]->base, U[s]->base, *cfg, eps, max_iter, nullptr, 0, &r);
+      CK(cudaEventRecord(c->ev_done, c->stream));
+      CK(cudaStreamWaitEvent(c->s_out, c->ev_done, 0));
+      CK(cudaMemcpyAsync(u_host[i], U[s]->base, bytes, cudaMemcpyDeviceToHost, c->s_out));
+      CK(cudaEventRecord(c->ev_free[s], c->s_out));
+      r.wall_time_seconds =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (reports) reports[i] = r;
+    }
+    CK(cudaStreamSynchronize(c->s_out));
   });
 }
 

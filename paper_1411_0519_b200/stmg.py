@@ -329,6 +329,31 @@ class Hierarchy:
                            hist[: rep.iterations + 1].tolist(), rep.wall_time_seconds,
                            rep.device_time_seconds, rep.seed)
 
+    def solve_host_batch(self, fs, us, cfg: CycleConfig, eps_mg: float, max_iter: int = 250,
+                         u0s=None) -> List[SolveReport]:
+        """Independent solves of HOST arrays streamed through the context
+        (stmg_solve_host_batch): problem i+1's upload and problem i-1's download
+        overlap solve i.  us[i] is updated in place, or written from u0s[i]."""
+        _, n = self.local_steps()
+        local = n * self.levels[0]["n_loc"] * self.levels[0]["n_x"]
+        k = len(fs)
+        if len(us) != k or (u0s is not None and len(u0s) != k):
+            raise ValueError("batch length mismatch")
+        for a in list(fs) + list(us) + list(u0s or []):
+            if a.dtype != np.float64 or a.size != local or not a.flags.c_contiguous:
+                raise ValueError("space-time vector shape mismatch")
+        P = C.c_void_p * max(k, 1)
+        pf = P(*[a.ctypes.data for a in fs])
+        pu = P(*[a.ctypes.data for a in us])
+        p0 = P(*[a.ctypes.data for a in u0s]) if u0s is not None else None
+        reps = (A.SolveReport * max(k, 1))()
+        c = cfg.c()
+        check(A.lib().stmg_solve_host_batch(self._ctx, k, pf, p0, pu, C.byref(c), eps_mg, max_iter,
+                                            reps))
+        return [SolveReport(r.iterations, bool(r.converged), [r.r0, r.r_final][: r.iterations + 1],
+                            r.wall_time_seconds, r.device_time_seconds, r.seed)
+                for r in reps[:k]]
+
     # ---- inputs ----------------------------------------------------------------
     def fill_uniform(self, v: BlockVector, seed: int, stream: int, offset: int = 0) -> BlockVector:
         check(A.lib().stmg_fill_uniform(self._ctx, v.ptr, v.n, seed, stream, offset))

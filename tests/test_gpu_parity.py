@@ -325,3 +325,42 @@ def test_n63_transforms_match_oracle(S, p, dim, tl):
     du = g.upload(u)
     g.mg_cycle(0, du, g.upload(b), S.CycleConfig(nu1=1, nu2=1))
     assert rel(du.numpy(), o.mg_cycle(0, u, b)) < 1e-10
+
+
+def test_host_solves_match_device_solve(S):
+    """stmg_solve_host and the pipelined stmg_solve_host_batch give the device
+    solve's iterate bit for bit, for distinct problems in one batch (in place
+    and from separate initial guesses), and the oracle's within 1e-10."""
+    g, o = pair(S, 1, 2, 4, 5, 1.0)
+    cfg = S.CycleConfig(nu1=1, nu2=1)
+    fs = [O.make_inputs(o, 40 + i, random_u0=True) for i in range(5)]
+    u0s = [O.fill_uniform(o.levels[0].size, 70 + i, 1) for i in range(5)]
+    ref, iters = [], []
+    for f, u0 in zip(fs, u0s):
+        du = g.upload(u0)
+        rep = g.solve(g.upload(f), du, cfg, 1e-8)
+        ref.append(du.numpy())
+        iters.append(rep.iterations)
+    u_o, rep_o = o.solve(fs[0], u=u0s[0], eps=1e-8)
+    assert rep_o["iterations"] == iters[0] and rel(ref[0], u_o) < 1e-10
+    uh = u0s[0].copy()
+    rep = g.solve_host(fs[0], uh, cfg, 1e-8)
+    assert rep.iterations == iters[0] and np.array_equal(uh, ref[0])
+    # in place
+    us = [u.copy() for u in u0s]
+    reps = g.solve_host_batch(fs, us, cfg, 1e-8)
+    assert [r.iterations for r in reps] == iters and all(r.converged for r in reps)
+    for u, r in zip(us, ref):
+        assert np.array_equal(u, r)
+    # separate initial guesses (inputs untouched), outputs reused round-robin
+    outs = [np.empty_like(u0s[0]) for _ in range(5)]
+    keep = [u.copy() for u in u0s]
+    reps = g.solve_host_batch(fs, outs, cfg, 1e-8, u0s=u0s)
+    for u, r in zip(outs, ref):
+        assert np.array_equal(u, r)
+    assert all(np.array_equal(a, b) for a, b in zip(u0s, keep))
+    assert g.solve_host_batch([], [], cfg, 1e-8) == []
+    with pytest.raises(ValueError):
+        g.solve_host_batch(fs, us[:2], cfg, 1e-8)
+    with pytest.raises(Exception):
+        g.solve_host_batch(fs[:1], us[:1], cfg, -1.0)
