@@ -142,10 +142,12 @@ struct stmg_ctx {
   int hist_cap = 0;
   double* h_norm = nullptr;  // pinned
   DevBuf user_f, user_u;     // for stmg_solve_host (and set 0 of the batch)
-  // stmg_solve_host_batch: second staging set, copy streams and their events
-  DevBuf user_f2, user_u2;
+  // stmg_solve_host_batch: staging sets 1..2 (set 0 = user_f/user_u), copy
+  // streams and their events
+  static constexpr int kSets = 3;
+  DevBuf batch_f[kSets - 1], batch_u[kSets - 1];
   cudaStream_t s_in = nullptr, s_out = nullptr;
-  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  cudaEvent_t ev_in[kSets] = {}, ev_free[kSets] = {};
   cudaEvent_t ev_done = nullptr;
   // graphs of one spectral V-cycle keyed by (cfg, starting buffer parity)
   struct GraphKey {
@@ -187,6 +189,11 @@ struct stmg_ctx {
   size_t tail_smem = 0;
   int* d_flag = nullptr;
   int* h_flag = nullptr;  // pinned
+  // mailbox: pinned host words the solve path's tiny kernels write directly
+  // (k_tiny) instead of cudaMemcpyAsync, so the solve never queues behind a
+  // bulk transfer on the copy engines (stmg_solve_host_batch)
+  double* h_hist = nullptr;  // pinned, hist_cap entries
+  int* h_iter = nullptr;     // pinned
   // device-side solve loop (conditional while node): cached per configuration
   std::map<std::string, cudaGraphExec_t> loops;
   std::map<std::string, i64> loop_kernels;  // kernels per body iteration
@@ -350,6 +357,56 @@ void build_level_tables(Level& L) {
     v.tc.psi0[k] = (k % 2 == 0) ? 1.0 : -1.0;
   }
 }
+
+// ------------------------------------------------------- tiny moves (k_tiny)
+// Scalar bookkeeping of the solve path (flags, norms, iteration counts, the
+// history, the ping-pong table) as one 1-CTA kernel: a copy of `bytes` from
+// src, or a 4/8-byte immediate when src is null.  Host-side ends are pinned
+// (mapped) words, written over PCIe by the kernel, so nothing on the solve
+// path goes through the copy engines.
+struct TinyOp {
+  void* dst;
+  const void* src;
+  unsigned long long imm;
+  int bytes;
+};
+struct TinyOps {
+  TinyOp op[8];
+  int n;
+};
+
+__global__ void k_tiny(TinyOps t) {
+  for (int k = 0; k < t.n; ++k) {
+    const TinyOp o = t.op[k];
+    if (o.src) {
+      for (int i = threadIdx.x; i < o.bytes / 4; i += blockDim.x)
+        static_cast<unsigned*>(o.dst)[i] = static_cast<const unsigned*>(o.src)[i];
+    } else if (threadIdx.x == 0) {
+      if (o.bytes == 4) *static_cast<unsigned*>(o.dst) = unsigned(o.imm);
+      else *static_cast<unsigned long long*>(o.dst) = o.imm;
+    }
+    __syncthreads();
+  }
+}
+
+void* mapped(void* h) {
+  void* d = nullptr;
+  CK(cudaHostGetDevicePointer(&d, h, 0));
+  return d;
+}
+
+void tiny(stmg_ctx* c, std::initializer_list<TinyOp> ops) {
+  TinyOps t{};
+  for (const TinyOp& o : ops) t.op[t.n++] = o;
+  k_tiny<<<1, 128, 0, c->stream>>>(t);
+  CK(cudaGetLastError());
+  count(c);
+}
+
+TinyOp to_host(void* h, const void* d, int bytes) { return TinyOp{mapped(h), d, 0ull, bytes}; }
+TinyOp set4(void* d, unsigned v) { return TinyOp{d, nullptr, v, 4}; }
+TinyOp set8(void* d, unsigned long long v) { return TinyOp{d, nullptr, v, 8}; }
+TinyOp copy(void* d, const void* s, int bytes) { return TinyOp{d, s, 0ull, bytes}; }
 
 void ensure(DevBuf& b, i64 n, i64 halo = 0) {
   if (b.count != n) b.alloc(n, halo);
@@ -959,7 +1016,10 @@ void ensure_hist(stmg_ctx* c, int n) {
   for (auto& kv : c->loops) cudaGraphExecDestroy(kv.second);  // they bake d_hist in
   c->loops.clear();
   if (c->d_hist) cudaFree(c->d_hist);
+  if (c->h_hist) cudaFreeHost(c->h_hist);
+  c->h_hist = nullptr;
   CK(cudaMalloc(&c->d_hist, size_t(n) * sizeof(double)));
+  CK(cudaMallocHost(&c->h_hist, size_t(n) * sizeof(double)));
   c->hist_cap = n;
 }
 
@@ -971,7 +1031,7 @@ double spectral_resnorm(stmg_ctx* c, int level) {
                           c->stream));
   CK(stmg::launch_norm_final(c->partials.base, a.n_partials, c->d_norm, nullptr, 0, c->stream));
   count(c, 2);
-  CK(cudaMemcpyAsync(c->h_norm, c->d_norm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  tiny(c, {to_host(c->h_norm, c->d_norm, 8)});
   CK(cudaStreamSynchronize(c->stream));
   return *c->h_norm;
 }
@@ -1082,11 +1142,11 @@ void run_device_loop(stmg_ctx* c, cudaGraphExec_t exec, int max_iter, double* hi
                      int history_cap, int* nh, stmg_solve_report& r, double eps) {
   CK(cudaMemsetAsync(c->d_iter, 0, sizeof(int), c->stream));
   CK(cudaGraphLaunch(exec, c->stream));
-  int it = 0;
-  CK(cudaMemcpyAsync(&it, c->d_iter, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  tiny(c, {to_host(c->h_iter, c->d_iter, 4),
+           to_host(c->h_hist, c->d_hist, (max_iter + 1) * int(sizeof(double)))});
   CK(cudaStreamSynchronize(c->stream));
-  std::vector<double> h(size_t(it) + 1);
-  CK(cudaMemcpy(h.data(), c->d_hist, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  const int it = *c->h_iter;
+  const std::vector<double> h(c->h_hist, c->h_hist + it + 1);
   for (int k = 1; k <= it; ++k) {
     if (history && *nh < history_cap) history[*nh] = h[k];
     ++*nh;
@@ -1150,13 +1210,10 @@ void run_fused(stmg_ctx* c, const stmg_cycle_config& cfg, double eps, int max_it
                          c->stream));
     count(c);
   }
-  double* tbl[2] = {L.U[0].base, L.U[1].base};
-  const int par1 = 1;
-  CK(cudaMemcpyAsync(c->d_pp, tbl, sizeof(tbl), cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemcpyAsync(c->d_par, &par1, sizeof(int), cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemcpyAsync(c->d_r0, c->d_norm, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-  CK(cudaMemcpyAsync(c->d_hist, c->d_norm, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-  CK(cudaMemsetAsync(c->d_iter, 0, sizeof(int), c->stream));
+  tiny(c, {set8(c->d_pp, reinterpret_cast<unsigned long long>(L.U[0].base)),
+           set8(c->d_pp + 1, reinterpret_cast<unsigned long long>(L.U[1].base)),
+           set4(c->d_par, 1u), copy(c->d_r0, c->d_norm, 8), copy(c->d_hist, c->d_norm, 8),
+           set4(c->d_iter, 0u)});
   int iters = 0;
   if (c->use_device_loop && !c->profile) {
     cudaGraphExec_t ex = device_loop(
@@ -1167,8 +1224,10 @@ void run_fused(stmg_ctx* c, const stmg_cycle_config& cfg, double eps, int max_it
         },
         c->d_par);
     CK(cudaGraphLaunch(ex, c->stream));
-    CK(cudaMemcpyAsync(&iters, c->d_iter, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    tiny(c, {to_host(c->h_iter, c->d_iter, 4),
+             to_host(c->h_hist, c->d_hist, (max_iter + 1) * int(sizeof(double)))});
     CK(cudaStreamSynchronize(c->stream));
+    iters = *c->h_iter;
     c->launches += iters * c->loop_kernels[loop_key("fused", cfg, 0, eps, max_iter)];
   } else {  // host-driven cycles (profiling: event records around k_updown)
     const std::string key = loop_key("fusedbody", cfg, 0, eps, max_iter);
@@ -1206,9 +1265,12 @@ void run_fused(stmg_ctx* c, const stmg_cycle_config& cfg, double eps, int max_it
       if (*c->h_norm <= eps * r.r0) break;
     }
   }
-  // history and report
-  std::vector<double> h(size_t(iters) + 1);
-  CK(cudaMemcpy(h.data(), c->d_hist, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  // history and report (the device loop fetched it with the iteration count)
+  if (!(c->use_device_loop && !c->profile)) {
+    tiny(c, {to_host(c->h_hist, c->d_hist, (iters + 1) * int(sizeof(double)))});
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  const std::vector<double> h(c->h_hist, c->h_hist + iters + 1);
   for (int k = 1; k <= iters; ++k) {
     if (history && *nh < history_cap) history[*nh] = h[k];
     ++*nh;
@@ -1266,10 +1328,10 @@ void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config
     ensure_svc(c, cfg);
     c->cur[0] = 0;
     // a zero initial guess (the usual case) needs no transform
-    CK(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+    tiny(c, {set4(c->d_flag, 0u)});
     CK(stmg::launch_nonzero(u, L0.view.size(), c->d_flag, c->stream));
     count(c);
-    CK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    tiny(c, {to_host(c->h_flag, c->d_flag, 4)});
     dst_all(c, L0, f, L0.F.base);
     CK(cudaStreamSynchronize(c->stream));
     if (*c->h_flag) dst_all(c, L0, u, L0.U[0].base);
@@ -2069,6 +2131,7 @@ int stmg_create(const stmg_hierarchy_params* p, stmg_ctx** out) {
     if (const char* e = std::getenv("STMG_FUSED")) c->use_fused = std::atoi(e) != 0;
     if (const char* e = std::getenv("STMG_COARSE_OP")) c->use_cop = std::atoi(e) != 0;
     CK(cudaMallocHost(&c->h_flag, sizeof(int)));
+    CK(cudaMallocHost(&c->h_iter, sizeof(int)));
     CK(cudaEventCreate(&c->ev_solve[0]));
     CK(cudaEventCreate(&c->ev_solve[1]));
     for (auto& s : c->prof) {
@@ -2111,10 +2174,15 @@ int stmg_destroy(stmg_ctx* c) {
     for (auto& kv : c->cop) cudaFree(kv.second);
     c->user_f.release();
     c->user_u.release();
-    c->user_f2.release();
-    c->user_u2.release();
-    for (cudaEvent_t e : {c->ev_in[0], c->ev_in[1], c->ev_free[0], c->ev_free[1], c->ev_done})
-      if (e) cudaEventDestroy(e);
+    for (int s = 0; s < stmg_ctx::kSets; ++s) {
+      if (s > 0) {
+        c->batch_f[s - 1].release();
+        c->batch_u[s - 1].release();
+      }
+      if (c->ev_in[s]) cudaEventDestroy(c->ev_in[s]);
+      if (c->ev_free[s]) cudaEventDestroy(c->ev_free[s]);
+    }
+    if (c->ev_done) cudaEventDestroy(c->ev_done);
     if (c->s_in) cudaStreamDestroy(c->s_in);
     if (c->s_out) cudaStreamDestroy(c->s_out);
     for (auto& s : c->prof) {
@@ -2137,6 +2205,8 @@ int stmg_destroy(stmg_ctx* c) {
     cudaFree(c->d_r0);
     for (auto& kv : c->loops) cudaGraphExecDestroy(kv.second);
     cudaFreeHost(c->h_flag);
+    cudaFreeHost(c->h_iter);
+    if (c->h_hist) cudaFreeHost(c->h_hist);
     if (c->tail_table) cudaFree(c->tail_table);
     std::free(c->tail_host);
     cudaFreeHost(c->h_norm);
@@ -2439,10 +2509,15 @@ int stmg_solve_host(stmg_ctx* c, const double* f_host, double* u_host,
 }
 
 // Streams a batch of independent solves through one context: the H2D of
-// problem i+1 (copy stream s_in) and the D2H of problem i-1 (s_out) run on the
-// two copy engines while problem i solves on the context stream, with two
-// device staging sets {f, u} in ping-pong.  Each solve is exactly
-// stmg_solve_host's (same kernels, same result bits); only the copies overlap.
+// problems i+1, i+2 (copy stream s_in) and the D2H of problem i-1 (s_out) run
+// on the two copy engines while problem i solves on the context stream.  Three
+// device staging sets {f, u} rotate, so an upload never waits for the download
+// of the problem just before it (with two sets it would, and the upload -- the
+// longest of the three phases -- would serialise behind it).  The solve path
+// itself uses no copy engine (k_tiny), so it never queues behind a bulk copy.
+// Each solve is exactly stmg_solve_host's (same kernels, same result bits).
+// STMG_BATCH_TRACE=1 prints per-problem phase times (ms from the batch start,
+// CUDA events) to stderr.
 int stmg_solve_host_batch(stmg_ctx* c, int count, const double* const* f_host,
                           const double* const* u0_host, double* const* u_host,
                           const stmg_cycle_config* cfg, double eps, int max_iter,
@@ -2457,40 +2532,66 @@ int stmg_solve_host_batch(stmg_ctx* c, int count, const double* const* f_host,
       require(f_host[i] && u_host[i] && (!u0_host || u0_host[i]), "null vector");
     require(eps > 0.0, "eps_mg must be positive");
     require(max_iter >= 0, "max_iter must be >= 0");
+    constexpr int NS = stmg_ctx::kSets;
     Level& L0 = c->levels[0];
     const i64 n = (c->shards && c->shards->nccl) ? L0.view.size() / c->shards->S : L0.view.size();
     const size_t bytes = size_t(n) * sizeof(double);
-    DevBuf* F[2] = {&c->user_f, &c->user_f2};
-    DevBuf* U[2] = {&c->user_u, &c->user_u2};
-    for (int s = 0; s < 2; ++s) {
+    DevBuf* F[NS] = {&c->user_f};
+    DevBuf* U[NS] = {&c->user_u};
+    for (int s = 1; s < NS; ++s) {
+      F[s] = &c->batch_f[s - 1];
+      U[s] = &c->batch_u[s - 1];
+    }
+    for (int s = 0; s < NS; ++s) {
       ensure(*F[s], n);
       ensure(*U[s], n);
     }
     if (!c->s_in) {
       CK(cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking));
       CK(cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking));
-      for (int s = 0; s < 2; ++s) {
+      for (int s = 0; s < NS; ++s) {
         CK(cudaEventCreateWithFlags(&c->ev_in[s], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_free[s], cudaEventDisableTiming));
       }
       CK(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
     }
-    // set s may be refilled once the D2H of its previous problem has drained
+    const char* te = std::getenv("STMG_BATCH_TRACE");
+    const bool trace = te && std::atoi(te) != 0;
+    std::vector<cudaEvent_t> tev;  // per problem: h2d start/end, solve start/end, d2h end
+    auto mark = [&](cudaStream_t st) {
+      if (!trace) return;
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      CK(cudaEventRecord(e, st));
+      tev.push_back(e);
+    };
+    std::vector<int> tslot(size_t(count) * 5, -1);
+    auto tmark = [&](int i, int k, cudaStream_t st) {
+      if (!trace) return;
+      tslot[size_t(i) * 5 + k] = int(tev.size());
+      mark(st);
+    };
+    // a set may be refilled once the D2H of its previous problem has drained
     // (its f was consumed by that solve's forward transform before that)
     CK(cudaStreamSynchronize(c->s_out));
     auto upload = [&](int i) {
-      const int s = i & 1;
+      const int s = i % NS;
       const double* u0 = u0_host ? u0_host[i] : u_host[i];
-      if (i >= 2) CK(cudaStreamWaitEvent(c->s_in, c->ev_free[s], 0));
+      if (i >= NS) CK(cudaStreamWaitEvent(c->s_in, c->ev_free[s], 0));
+      tmark(i, 0, c->s_in);
       CK(cudaMemcpyAsync(F[s]->base, f_host[i], bytes, cudaMemcpyHostToDevice, c->s_in));
       CK(cudaMemcpyAsync(U[s]->base, u0, bytes, cudaMemcpyHostToDevice, c->s_in));
       CK(cudaEventRecord(c->ev_in[s], c->s_in));
+      tmark(i, 1, c->s_in);
     };
-    upload(0);
+    // uploads run NS-1 problems ahead: problem j's set was last used by
+    // problem j-NS, whose D2H (and its ev_free record) is already enqueued
+    for (int j = 0; j < std::min(count, NS - 1); ++j) upload(j);
     for (int i = 0; i < count; ++i) {
-      const int s = i & 1;
-      if (i + 1 < count) upload(i + 1);
+      const int s = i % NS;
+      if (i + NS - 1 < count) upload(i + NS - 1);
       CK(cudaStreamWaitEvent(c->stream, c->ev_in[s], 0));
+      tmark(i, 2, c->stream);
       const auto t0 = std::chrono::steady_clock::now();
       stmg_solve_report r{};
       if (c->shards)
@@ -2498,14 +2599,30 @@ int stmg_solve_host_batch(stmg_ctx* c, int count, const double* const* f_host,
       else
         solve_impl(c, F[s]->base, U[s]->base, *cfg, eps, max_iter, nullptr, 0, &r);
       CK(cudaEventRecord(c->ev_done, c->stream));
+      tmark(i, 3, c->stream);
       CK(cudaStreamWaitEvent(c->s_out, c->ev_done, 0));
       CK(cudaMemcpyAsync(u_host[i], U[s]->base, bytes, cudaMemcpyDeviceToHost, c->s_out));
       CK(cudaEventRecord(c->ev_free[s], c->s_out));
+      tmark(i, 4, c->s_out);
       r.wall_time_seconds =
           std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       if (reports) reports[i] = r;
     }
     CK(cudaStreamSynchronize(c->s_out));
+    CK(cudaStreamSynchronize(c->s_in));
+    if (trace) {
+      for (int i = 0; i < count; ++i) {
+        std::fprintf(stderr, "batch %d:", i);
+        static const char* nm[5] = {"h2d0", "h2d1", "solve0", "solve1", "d2h1"};
+        for (int k = 0; k < 5; ++k) {
+          float ms = 0.f;
+          CK(cudaEventElapsedTime(&ms, tev[0], tev[size_t(tslot[size_t(i) * 5 + k])]));
+          std::fprintf(stderr, " %s=%.3f", nm[k], ms);
+        }
+        std::fprintf(stderr, "\n");
+      }
+      for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    }
   });
 }
 
