@@ -205,6 +205,9 @@ struct stmg_ctx {
   double* d_r0 = nullptr;
   bool use_device_loop = true;
   bool use_fused = true;  // fused level-0 schedule for V(1,1) solves
+  // a device-loop body may leave its final norm reduction to device_loop,
+  // which then launches it fused with the stop test (k_norm_decide)
+  i64 pending_norm = -1;  // number of partials, or -1
   // inexact block solver: sine tables per spatial grid level and one
   // workspace (X, B per sub-level) shared by all levels, sized for level 0
   std::map<int, double*> space_tab;
@@ -1101,11 +1104,18 @@ cudaGraphExec_t device_loop(stmg_ctx* c, const std::string& key, double eps, int
   CK(cudaStreamBeginCaptureToGraph(c->stream, bodyg, nullptr, nullptr, 0,
                                    cudaStreamCaptureModeThreadLocal));
   try {
+    c->pending_norm = -1;
     body();
-    CK(stmg::launch_decide(h, c->d_norm, c->d_r0, c->d_hist, c->d_iter, eps, max_iter, parity,
-                           c->stream));
+    if (c->pending_norm >= 0)
+      CK(stmg::launch_norm_decide(c->partials.base, c->pending_norm, c->d_norm, h, c->d_r0,
+                                  c->d_hist, c->d_iter, eps, max_iter, parity, c->stream));
+    else
+      CK(stmg::launch_decide(h, c->d_norm, c->d_r0, c->d_hist, c->d_iter, eps, max_iter, parity,
+                             c->stream));
+    c->pending_norm = -1;
     count(c);
   } catch (...) {
+    c->pending_norm = -1;
     cudaGraph_t dummy;
     cudaStreamEndCapture(c->stream, &dummy);
     c->capturing = false;
@@ -1140,7 +1150,7 @@ std::string loop_key(const char* kind, const stmg_cycle_config& cfg, int cur0, d
 // Run the remaining cycles on the device; fills r and history from the device.
 void run_device_loop(stmg_ctx* c, cudaGraphExec_t exec, int max_iter, double* history,
                      int history_cap, int* nh, stmg_solve_report& r, double eps) {
-  CK(cudaMemsetAsync(c->d_iter, 0, sizeof(int), c->stream));
+  tiny(c, {set4(c->d_iter, 0u)});
   CK(cudaGraphLaunch(exec, c->stream));
   tiny(c, {to_host(c->h_iter, c->d_iter, 4),
            to_host(c->h_hist, c->d_hist, (max_iter + 1) * int(sizeof(double)))});
@@ -1178,7 +1188,7 @@ void coarse_cycle(stmg_ctx* c, const stmg_cycle_config& cfg) {
 }
 
 // One fused cycle body (captured): coarse(k), k_updown, norm.
-void fused_body(stmg_ctx* c, const stmg_cycle_config& cfg, i64* np) {
+void fused_body(stmg_ctx* c, const stmg_cycle_config& cfg, i64* np, bool defer_norm = false) {
   Level& L = c->levels[0];
   Level& C = c->levels[1];
   prof_begin(c, 4);
@@ -1191,6 +1201,10 @@ void fused_body(stmg_ctx* c, const stmg_cycle_config& cfg, i64* np) {
   prof_end(c, 0, 8.0 * double(3 * L.view.size() + 2 * C.view.size()));
   count(c);
   *np = a.n_partials;
+  if (defer_norm) {
+    c->pending_norm = *np;
+    return;
+  }
   CK(stmg::launch_norm_final(c->partials.base, *np, c->d_norm, nullptr, 0, c->stream));
   count(c);
 }
@@ -1220,7 +1234,7 @@ void run_fused(stmg_ctx* c, const stmg_cycle_config& cfg, double eps, int max_it
         c, loop_key("fused", cfg, 0, eps, max_iter), eps, max_iter,
         [&] {
           i64 np = 0;
-          fused_body(c, cfg, &np);
+          fused_body(c, cfg, &np, true);
         },
         c->d_par);
     CK(cudaGraphLaunch(ex, c->stream));
@@ -1353,21 +1367,17 @@ void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config
     }
     if (loop_ok && !r.converged && max_iter > 0) {
       ensure_hist(c, max_iter + 1);
-      CK(cudaMemcpyAsync(c->d_r0, c->d_norm, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-      CK(cudaMemcpyAsync(c->d_hist, c->d_norm, sizeof(double), cudaMemcpyDeviceToDevice,
-                         c->stream));
+      tiny(c, {copy(c->d_r0, c->d_norm, 8), copy(c->d_hist, c->d_norm, 8)});
       const int cur0 = c->cur[0];
       cudaGraphExec_t ex = device_loop(c, loop_key("single", cfg, cur0, eps, max_iter), eps,
                                        max_iter, [&] {
                                          i64 np = 0;
                                          spectral_cycle(c, 0, false, cfg, true, &np);
-                                         CK(stmg::launch_norm_final(c->partials.base, np, c->d_norm,
-                                                                    nullptr, 0, c->stream));
-                                         count(c);
+                                         c->pending_norm = np;  // fused with the stop test
                                        });
       c->cur[0] = cur0;
       run_device_loop(c, ex, max_iter, history, history_cap, &nh, r, eps);
-      c->launches += r.iterations * (probe_kernels + 1);
+      c->launches += r.iterations * probe_kernels;
     }
     for (int k = 0; k < max_iter && !r.converged && !loop_ok && !fused; ++k) {
       stmg_ctx::GraphEntry& g = cycle_graph(c, cfg);

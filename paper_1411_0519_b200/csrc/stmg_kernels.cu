@@ -2900,6 +2900,39 @@ __global__ void k_decide(cudaGraphConditionalHandle h, const double* __restrict_
   if (h) cudaGraphSetConditional(h, more ? 1u : 0u);
 }
 
+// k_norm_final followed by k_decide in one launch (the last two nodes of a
+// device-loop body): same fixed-order reduction, so the norm, the history and
+// the stop decision are bitwise those of the two-kernel sequence.
+__global__ void __launch_bounds__(256) k_norm_decide(const double* __restrict__ partial,
+                                                     const i64 n, double* __restrict__ out,
+                                                     cudaGraphConditionalHandle h,
+                                                     const double* __restrict__ r0,
+                                                     double* __restrict__ hist,
+                                                     int* __restrict__ iter, const double eps,
+                                                     const int max_iter,
+                                                     int* __restrict__ parity) {
+  pdl_wait();
+  __shared__ double sh[256];
+  double s = 0.0;
+  for (i64 i = threadIdx.x; i < n; i += 256) s += partial[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (int(threadIdx.x) < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double rk = sqrt(sh[0]);
+    out[0] = rk;
+    const int k = *iter + 1;
+    *iter = k;
+    hist[k] = rk;
+    const bool more = !(rk <= eps * (*r0)) && k < max_iter;
+    if (parity) *parity = 1 - *parity;
+    if (h) cudaGraphSetConditional(h, more ? 1u : 0u);
+  }
+}
+
 // Coarse operator: y = B x with B (n x n, row-major) the precomputed linear
 // map of the coarse tail's V(1,1) cycle (levels >= tail start, zero initial
 // guess), rhs -> iterate.  One warp per row; the block's rows are staged into
@@ -3223,6 +3256,14 @@ cudaError_t launch_decide(cudaGraphConditionalHandle h, const double* norm, cons
                           double* hist, int* iter, double eps, int max_iter, int* parity,
                           cudaStream_t st) {
   PDLK(k_decide, 1, 1, 0, st, h, norm, r0, hist, iter, eps, max_iter, parity);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_norm_decide(const double* partial, int64_t n, double* out,
+                               cudaGraphConditionalHandle h, const double* r0, double* hist,
+                               int* iter, double eps, int max_iter, int* parity,
+                               cudaStream_t st) {
+  PDLK(k_norm_decide, 1, 256, 0, st, partial, n, out, h, r0, hist, iter, eps, max_iter, parity);
   return cudaGetLastError();
 }
 

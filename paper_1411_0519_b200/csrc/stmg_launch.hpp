@@ -80,6 +80,11 @@ cudaError_t launch_axpy(double* y, const double* x, double a, int64_t n,
 cudaError_t launch_decide(cudaGraphConditionalHandle h, const double* norm, const double* r0,
                           double* hist, int* iter, double eps, int max_iter, int* parity,
                           cudaStream_t st);
+// launch_norm_final(partial, n, out) + launch_decide(h, out, ...) in one kernel.
+cudaError_t launch_norm_decide(const double* partial, int64_t n, double* out,
+                               cudaGraphConditionalHandle h, const double* r0, double* hist,
+                               int* iter, double eps, int max_iter, int* parity,
+                               cudaStream_t st);
 
 // ---- fused spectral V-cycle kernels (sine coefficients) -------------------
 struct ModalArgs {
