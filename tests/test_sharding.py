@@ -220,3 +220,31 @@ def test_schedule_switches_agree(cfg):
     r_op, u_op = _solve_with_env({}, p, dim, sl, tl, f)
     assert r_op.iterations == r_ref.iterations
     assert np.abs(u_op - u_ref).max() <= 1e-12 * np.abs(u_ref).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cyc", [(1, 1), (2, 2)])
+def test_virtual_shards_host_batch(cyc):
+    """stmg_solve_host_batch on a 4-shard context (fused and general cycles):
+    bitwise the one-shard device solve of every problem."""
+    from oracle import oracle as O
+    from paper_1411_0519_b200 import build, stmg
+    build.build()
+    p, dim, sl, tl = 1, 2, 4, 6
+    o = O.Hierarchy(p, dim, sl, tl)
+    n = o.levels[0].size
+    fs = [O.fill_uniform(n, 20 + i, 0) for i in range(4)]
+    u0s = [O.fill_uniform(n, 30 + i, 0) for i in range(4)]
+    cc = stmg.CycleConfig(nu1=cyc[0], nu2=cyc[1])
+    g1 = stmg.Hierarchy(p, dim, sl, tl)
+    ref, iters = [], []
+    for f, u0 in zip(fs, u0s):
+        u = g1.upload(u0)
+        iters.append(g1.solve(g1.upload(f), u, cc, 1e-9).iterations)
+        ref.append(u.numpy())
+    gs = stmg.Hierarchy(p, dim, sl, tl, shards=4)
+    outs = [np.empty(n) for _ in range(4)]
+    reps = gs.solve_host_batch(fs, outs, cc, 1e-9, u0s=u0s)
+    assert [r.iterations for r in reps] == iters
+    for a, b in zip(outs, ref):
+        assert np.array_equal(a, b)
