@@ -3384,12 +3384,14 @@ int64_t partial_count(const LevelView& L, int chunk, bool grouped) {
 }
 
 #ifndef STMG_CHUNK_TARGET
-#define STMG_CHUNK_TARGET (148 * 512)
+#define STMG_CHUNK_TARGET (148 * 256)
 #endif
 int pick_chunk(const LevelView& L, bool grouped) {
   const i64 G = (L.sp.n1 + 1) / 2;
   const i64 units = grouped ? (ipow(G, L.sp.dim) << L.sp.dim) : L.sp.nx;
-  // aim for ~1K resident threads per SM; chunks are even and divide the
+  // aim for ~0.5K threads per SM worth of (lane, chunk) work items (A/B:
+  // 148*256 beats 148*512 by 2 % on C2, neutral on C3-C5; profiles/
+  // r01_v13_chunk_ab.txt, r01_v14_chunk_ab.txt); chunks are even and divide the
   // (power-of-two) n_t; longer chunks amortise the one-step warm-up
   const i64 target = STMG_CHUNK_TARGET;
   i64 c = 2;
