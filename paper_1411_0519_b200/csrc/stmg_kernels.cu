@@ -755,7 +755,7 @@ __device__ __forceinline__ double updown_body_ops(const i64 tid, const i64 n0, c
 #define STMG_UPDOWN_TMA 2
 #endif
 #ifndef STMG_TMA_STAGES
-#define STMG_TMA_STAGES 3
+#define STMG_TMA_STAGES 3  // A/B vs 4 and 6 stages: profiles/r01_v15_tma_stages_ab.txt
 #endif
 constexpr int kTmaStages = STMG_TMA_STAGES;
 
