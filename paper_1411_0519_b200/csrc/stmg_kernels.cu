@@ -1041,14 +1041,19 @@ __device__ __forceinline__ double updown_body_tma(const i64 tid, const i64 n0, c
   return me.ok ? sumsq : 0.0;
 }
 
-// p_t <= 1: 96 registers, 5 CTAs per SM (C2 1.78 -> 1.73 ms per solve; the
-// 1024-CTA grid of C2 then runs in 1.4 instead of 1.7 waves); p_t = 2 would
-// spill at 96 (C3 106 -> 157 ms), so no bound there
-template <int DIM, int NL>
+// Launch bounds.  p_t <= 1: was 5 CTAs per SM (96 registers) while C2 ran
+// 1024 CTAs (1.4 instead of 1.7 waves); with the 512-CTA grid of chunk target
+// 148*256 all CTAs fit at 4 per SM and the 128-register budget is faster.
+// p_t = 2 would spill at 96 (C3 106 -> 157 ms).
 #ifndef STMG_UPDOWN_MINB3
 #define STMG_UPDOWN_MINB3 3  // p_t = 2: 168 registers, 3 CTAs/SM (C3 108 -> 104 ms); 4 spills
 #endif
-__global__ void __launch_bounds__(128, (NL <= 2 ? 5 : NL == 3 ? STMG_UPDOWN_MINB3 : 1)) k_updown_tma(const double* __restrict__ ec,
+#ifndef STMG_UPDOWN_MINB2
+#define STMG_UPDOWN_MINB2 4  // p_t <= 1: 4 CTAs/SM (v16 A/B vs 5 and 3: C2 1.691 -> 1.669 ms,
+                             // C4/C5 -1.5 %; profiles/r01_v16_minb_ab.txt)
+#endif
+template <int DIM, int NL>
+__global__ void __launch_bounds__(128, (NL <= 2 ? STMG_UPDOWN_MINB2 : NL == 3 ? STMG_UPDOWN_MINB3 : 1)) k_updown_tma(const double* __restrict__ ec,
                                                     const PingPong pp,
                                                     const double* __restrict__ f,
                                                     double* __restrict__ fc,
