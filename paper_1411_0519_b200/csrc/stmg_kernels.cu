@@ -2567,8 +2567,11 @@ __device__ __forceinline__ void dst_passes(double2* X, const int tt,
   }
 }
 
+#ifndef STMG_DST_MINB
+#define STMG_DST_MINB 5  // A/B vs 4 and 6: profiles/r01_v17_dst_minb_ab.txt
+#endif
 template <int LOG2N>
-__global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK, (LOG2N >= 4 ? 5 : 1)) k_dst_lines(
+__global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK, (LOG2N >= 4 ? STMG_DST_MINB : 1)) k_dst_lines(
     const double* __restrict__ in, double* __restrict__ out, const i64 n_lines, const i64 stride,
     const double scale, const double alpha, const int accumulate,
     const double2* __restrict__ tw) {
