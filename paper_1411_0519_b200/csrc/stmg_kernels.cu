@@ -3394,6 +3394,15 @@ int64_t partial_count(const LevelView& L, int chunk, bool grouped) {
 #ifndef STMG_CHUNK_TARGET
 #define STMG_CHUNK_TARGET (148 * 256)
 #endif
+// levels below STMG_CHUNK_BIG dofs (latency-bound coarse levels) may use
+// their own target (A/B: 148*64 ... 148*1024 for them are all slower on C2
+// than the common 148*256; profiles/r01_v17_chunk_small_ab.txt)
+#ifndef STMG_CHUNK_TARGET_SMALL
+#define STMG_CHUNK_TARGET_SMALL STMG_CHUNK_TARGET
+#endif
+#ifndef STMG_CHUNK_BIG
+#define STMG_CHUNK_BIG (i64(1) << 23)
+#endif
 int pick_chunk(const LevelView& L, bool grouped) {
   const i64 G = (L.sp.n1 + 1) / 2;
   const i64 units = grouped ? (ipow(G, L.sp.dim) << L.sp.dim) : L.sp.nx;
@@ -3401,7 +3410,7 @@ int pick_chunk(const LevelView& L, bool grouped) {
   // 148*256 beats 148*512 by 2 % on C2, neutral on C3-C5; profiles/
   // r01_v13_chunk_ab.txt, r01_v14_chunk_ab.txt); chunks are even and divide the
   // (power-of-two) n_t; longer chunks amortise the one-step warm-up
-  const i64 target = STMG_CHUNK_TARGET;
+  const i64 target = L.size() >= STMG_CHUNK_BIG ? i64(STMG_CHUNK_TARGET) : i64(STMG_CHUNK_TARGET_SMALL);
   i64 c = 2;
   while (c < 64 && c * 2 <= L.n_t && units * (L.n_t / (c * 2)) >= target) c *= 2;
   if (c > L.n_t) c = L.n_t;
