@@ -2947,7 +2947,14 @@ __global__ void __launch_bounds__(256) k_norm_decide(const double* __restrict__ 
 // shared memory with cp.async BEFORE the PDL wait (B is a constant), so their
 // HBM traffic overlaps the previous kernel; after the wait only x (L2) is
 // read.  Fixed summation order: deterministic.
-constexpr int kCopRows = 8;
+// Rows per CTA (one warp per row).  2 rows: many small CTAs (C2: 784 of
+// 25 KB) keep more bulk copies in flight per SM than 8 rows (C2: 196 of
+// 100 KB; C1's n = 1984 at 8 rows needs 127 KB, i.e. one CTA per SM).  A/B:
+// C1 0.355 -> 0.318 ms per solve, C2/C4 neutral (profiles/r01_v19_cop_rows_ab.txt)
+#ifndef STMG_COP_ROWS
+#define STMG_COP_ROWS 2
+#endif
+constexpr int kCopRows = STMG_COP_ROWS;
 __global__ void __launch_bounds__(kCopRows * 32) k_cop_gemv(const double* __restrict__ B,
                                                             const double* __restrict__ x,
                                                             double* __restrict__ y, const int n) {
@@ -3317,7 +3324,7 @@ cudaError_t launch_cop_gemv(const double* B, const double* x, double* y, int n,
   const size_t smem = size_t(kCopRows) * n * sizeof(double);
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   static bool attr = false;
-  if (!attr) {  // two 100 KB CTAs per SM: all rows of B in flight in one wave
+  if (!attr) {  // maximum shared-memory carveout: all rows of B in flight in one wave
     cudaFuncSetAttribute(k_cop_gemv, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr = true;
   }
