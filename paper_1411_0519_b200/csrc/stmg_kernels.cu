@@ -2947,12 +2947,14 @@ __global__ void __launch_bounds__(256) k_norm_decide(const double* __restrict__ 
 // shared memory with cp.async BEFORE the PDL wait (B is a constant), so their
 // HBM traffic overlaps the previous kernel; after the wait only x (L2) is
 // read.  Fixed summation order: deterministic.
-// Rows per CTA (one warp per row).  2 rows: many small CTAs (C2: 784 of
-// 25 KB) keep more bulk copies in flight per SM than 8 rows (C2: 196 of
-// 100 KB; C1's n = 1984 at 8 rows needs 127 KB, i.e. one CTA per SM).  A/B:
-// C1 0.355 -> 0.318 ms per solve, C2/C4 neutral (profiles/r01_v19_cop_rows_ab.txt)
+// Rows per CTA (one warp per row).  1 row: many small CTAs (C2: 1568 of
+// 12.5 KB, all resident) keep more bulk copies in flight per SM than 8 rows
+// (C2: 196 of 100 KB; C1's n = 1984 at 8 rows needs 127 KB, one CTA per SM).
+// A/B (profiles/r01_v19_cop_rows_ab.txt, r01_v20_ab.txt): 8 -> 2 -> 1 rows
+// C1 0.355 -> 0.318 -> 0.312 ms per solve, C2 1.662 -> 1.662 -> 1.644 ms,
+// C4 neutral
 #ifndef STMG_COP_ROWS
-#define STMG_COP_ROWS 2
+#define STMG_COP_ROWS 1
 #endif
 constexpr int kCopRows = STMG_COP_ROWS;
 __global__ void __launch_bounds__(kCopRows * 32) k_cop_gemv(const double* __restrict__ B,
