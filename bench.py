@@ -12,11 +12,23 @@ coarsening; stop at ||r_k|| <= 1e-8 ||r_0||.
 One step = one full solve to 1e-8 (basis transforms included) on inputs
 resident in HBM.  value = fine DoF x V-cycles / s, summed over ranks.
 e2e = the same K solves through stmg_solve_host_batch with pinned HOST buffers
-(H2D of f and u0, D2H of u inside the timed region for every step; step i+1's
-upload and step i-1's download overlap solve i); e2e.single_call is the
-unpipelined stmg_solve_host per step.  --impl reference times the CPU oracle
-(the reference algorithm restated in C++/OpenMP; the reference itself cannot
-be built here) on all host cores.
+(H2D of f, D2H of u inside the timed region for every step, zero initial
+guess; step i+1's upload and step i-1's download overlap solve i);
+e2e.single_call is the unpipelined reference-shaped stmg_solve_host per step
+(f and the initial guess uploaded, u downloaded).  --impl reference times the
+CPU oracle (the reference algorithm restated in C++/OpenMP; the reference
+itself cannot be built here) on all host cores.
+
+Multi-GPU (--gpus N > 1): bench.py re-launches itself under
+torch.distributed.run with N ranks (one per GPU) unless it already runs under
+torchrun (WORLD_SIZE set, which must equal N); it exits non-zero when fewer
+than N GPUs are visible or any rank fails -- there is no replica fallback.
+The main line is configs[1] scaled weakly in time (N_t = 256 N, tau fixed:
+per-GPU work constant, time slabs over the ranks, NCCL halo exchange inside
+the library).  Every run (N = 1 included) adds "scaling" sub-records:
+configs[2] C3 strong scaling (N_t = 4096 fixed) and configs[4] C5 weak
+scaling (N_t = 2048 N), each with ms per solve and per V-cycle, iterations and
+the per-rank k_updown HBM GB/s, so the driver's per-N runs give both curves.
 """
 from __future__ import annotations
 
@@ -119,17 +131,59 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def dist_setup():
+def dist_setup(expect_world: int):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != expect_world:
+        raise SystemExit(f"[bench] WORLD_SIZE={world} but --gpus {expect_world}: refusing to run")
     dist = None
     if world > 1:
         import torch
         import torch.distributed as dist
+        ndev = torch.cuda.device_count()
+        if local >= ndev:
+            raise SystemExit(f"[bench] rank {rank}: LOCAL_RANK {local} but only {ndev} GPU(s) visible")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        print(f"[bench] rank {rank}/{world} on cuda:{local} "
+              f"({torch.cuda.get_device_name(local)}): NCCL process group up", file=sys.stderr,
+              flush=True)
     return world, rank, local, dist
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_command(argv, n: int, port: int):
+    """torchrun command that re-runs this script with n ranks on one node."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+            os.path.abspath(__file__)] + list(argv)
+
+
+def spawn(args, argv) -> int:
+    """--gpus N > 1 without torchrun: start N ranks, fail loudly on fewer GPUs."""
+    try:
+        import torch
+        ndev = torch.cuda.device_count()
+    except Exception as exc:  # pragma: no cover
+        print(f"[bench] cannot query GPUs: {exc}", file=sys.stderr)
+        return 2
+    if ndev < args.gpus:
+        print(f"[bench] --gpus {args.gpus} needs {args.gpus} GPUs on this node, found {ndev}; "
+              "not running (no replica fallback)", file=sys.stderr, flush=True)
+        return 2
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator lines: one per rank
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = launch_command(argv, args.gpus, free_port())
+    print("[bench] launching: " + " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.run(cmd, env=env).returncode
 
 
 def allreduce_max(dist, local, x: float) -> float:
@@ -173,9 +227,8 @@ def cpu_reference_cycles(cfg, cycles: int, warm: int = 0):
     times = []
     for k in range(warm + cycles):
         t0 = time.perf_counter()
-        u = h.mg_cycle(0, u, f, 1, 1, 1, 0.5)
-        r = h.residual(0, u, f)
-        h.norm(0, r)
+        h.mg_cycle_inplace(0, u, f, 1, 1, 1, 0.5)
+        h.residual_norm(0, u, f)  # stop-test residual + norm (mg.cpp:150-160)
         dt = time.perf_counter() - t0
         if k >= warm:
             times.append(dt)
@@ -183,24 +236,30 @@ def cpu_reference_cycles(cfg, cycles: int, warm: int = 0):
 
 
 def run_reference(args, cfgname):
-    world, rank, local, dist = dist_setup()
-    if rank != 0:
+    # under torchrun rank 0 alone runs the CPU reference; no process group needed
+    if int(os.environ.get("RANK", "0")) != 0:
         return 0
-    cfg = CONFIGS[cfgname]
+    cfg = scaled(cfgname, args.gpus, weak=True)  # the workload of our arm at this N
     cores = os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     times, n0 = cpu_reference_cycles(cfg, args.steps, args.warmup)
     per = sum(times) / len(times)
     value = n0 / per
-    sample = (f"{args.steps} V(1,1) cycles (+ stop-test residual/norm) of {cfgname} from a zero guess, "
-              f"{args.warmup} untimed; one step = one cycle")
+    sample = (f"{args.steps} V(1,1) cycles (+ stop-test residual/norm each) of {cfgname} from a "
+              f"zero guess, {args.warmup} untimed; one step = one cycle; value = dofs / mean "
+              f"cycle time")
+    workload = cfg["desc"] + (f"; weak in time over {args.gpus} GPUs: N_t = "
+                              f"{2 ** cfg['time_level']}, T = {cfg['t_final']:g}"
+                              if args.gpus > 1 else "")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
-        "higher_is_better": True, "scaling": "weak" if cfgname == "C5" else "strong",
+        "higher_is_better": True, "scaling": "weak" if args.gpus > 1 else "strong",
         "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded splitmix64 uniform[-1,1])",
-        "config": {"workload": cfg["desc"], "dofs": n0, "cycle": "V(1,1) omega_t=0.5 exact blocks"},
+        "data": "synthetic (seeded splitmix64 uniform[-1,1], f and u0)",
+        "config": {"workload": workload, "dofs": n0,
+                   "cycle": "V(1,1), omega_t=0.5, exact DG block solves, mu-driven coarsening",
+                   "eps": EPS, "parallelism": f"CPU oracle, {cores} host threads (OpenMP)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -221,49 +280,131 @@ def traffic_from_profiles(kernel_tag: str):
         return None
 
 
-def run_ours(args, cfgname):
-    world, rank, local, dist = dist_setup()
-    from paper_1411_0519_b200 import stmg
-    from paper_1411_0519_b200 import _capi as A
+def make_hierarchy(stmg, cfg, world, rank, local, dist):
+    """One context: plain on one GPU, time slabs over the ranks otherwise.
+    Any failure propagates (no replica fallback)."""
+    if world == 1:
+        return stmg.Hierarchy(cfg["p_t"], cfg["dim"], cfg["space_level"], cfg["time_level"],
+                              cfg["t_final"], device=local)
+    uid = [stmg.Hierarchy.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    h = stmg.Hierarchy(cfg["p_t"], cfg["dim"], cfg["space_level"], cfg["time_level"],
+                       cfg["t_final"], device=local, rank=rank, world=world, nccl_id=uid[0])
+    first, n = h.local_steps()
+    print(f"[bench] rank {rank}/{world}: time-slab context up (steps [{first}, {first + n}) of "
+          f"{h.levels[0]['n_t']}, own NCCL communicator)", file=sys.stderr, flush=True)
+    return h
+
+
+def scaled(cfgname, world, weak):
+    """configs entry for N ranks: weak = N_t x N with tau fixed (T = N)."""
     cfg = dict(CONFIGS[cfgname])
-    scaling = "strong"
-    if cfgname == "C5":  # weak scaling: N_t = 2048 G, T = G (tau fixed)
+    if weak and world > 1:
         cfg["time_level"] += int(round(math.log2(world)))
         cfg["t_final"] = float(world)
-        scaling = "weak"
-    parallelism = "single GPU"
-    h = None
-    if world > 1:
-        # time slabs over the ranks, NCCL halo exchange inside the library
-        try:
-            uid = [stmg.Hierarchy.unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(uid, src=0)
-            h = stmg.Hierarchy(cfg["p_t"], cfg["dim"], cfg["space_level"], cfg["time_level"],
-                               cfg["t_final"], device=local, rank=rank, world=world,
-                               nccl_id=uid[0])
-            parallelism = f"time-slab x{world} (NCCL halo send/recv, coarse levels gathered on rank 0)"
-        except Exception as exc:  # report, then run replicas rather than nothing
-            print(f"[bench] distributed context failed on rank {rank}: {exc}", file=sys.stderr)
-            h = None
-            parallelism = f"replicas (distributed init failed: {type(exc).__name__})"
-            scaling = "weak"
-    if h is None:
-        h = stmg.Hierarchy(cfg["p_t"], cfg["dim"], cfg["space_level"], cfg["time_level"],
-                           cfg["t_final"], device=local)
-    first, nsteps = h.local_steps()
+    return cfg
+
+
+def local_inputs(stmg, h, cfg):
+    """This rank's slabs of the seeded f (u0 folded into f on rank 0)."""
+    first, _ = h.local_steps()
     L0 = h.levels[0]
     slab = L0["n_loc"] * L0["n_x"]
     f = h.local_vector()
-    n0 = f.n
     h.fill_uniform(f, SEED, 0, first * slab)
     if cfg["random_u0"] and first == 0:
         u0 = stmg.BlockVector(h, L0["n_x"], (L0["n_x"],))
         h.fill_uniform(u0, SEED, 1)
         h.fold_u0(f, u0)
         del u0
+    return f
+
+
+def gather_obj(dist, x):
+    if dist is None:
+        return [x]
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, x)
+    return out
+
+
+def updown_profile(h, step):
+    """k_updown (or k_down/k_up) per-launch ms and algorithmic bytes from CUDA
+    events around every level-0 launch during one profiled replay of `step`."""
+    h.profile(True)
+    h.profile_reset()
+    dev = step().device_time_seconds
+    prof = {k: h.profile_read(k) for k in (0, 1, 2)}
+    h.profile(False)
+    return prof, dev
+
+
+def scaling_record(stmg, name, base, weak, world, rank, local, dist, steps, warmup):
+    """Sub-record of one scaling curve at this N (the driver's per-N runs give
+    the curve; efficiencies are computed by the reader, not here)."""
+    import gc
+    cfg = scaled(base, world, weak)
+    h = make_hierarchy(stmg, cfg, world, rank, local, dist)
+    f = local_inputs(stmg, h, cfg)
     u = h.local_vector()
     ccfg = stmg.CycleConfig(nu1=1, nu2=1, gamma=1, omega_t=0.5)
+    n0 = f.n
+
+    def step():
+        from paper_1411_0519_b200 import _capi as A
+        A.check(A.lib().stmg_memset_zero(h._ctx, u.ptr, n0 * 8))
+        return h.solve(f, u, ccfg, EPS)
+
+    for _ in range(warmup):
+        step()
+    barrier(dist, local)
+    dev, its = [], []
+    for _ in range(steps):
+        r = step()
+        if not r.converged:
+            raise RuntimeError(f"{name}: solve did not converge")
+        dev.append(r.device_time_seconds)
+        its.append(r.iterations)
+    barrier(dist, local)
+    prof, _ = updown_profile(h, step)
+    ms, nl, b = prof[0]
+    gbs = (b / ((ms / nl) * 1e-3) / 1e9) if nl else None
+    t = allreduce_max(dist, local, sum(dev))
+    work = allreduce_sum(dist, local, float(n0 * sum(its)))
+    rec = {
+        "workload": CONFIGS[base]["desc"] + (f"; weak in time: N_t = {h.levels[0]['n_t']}, "
+                                             f"T = {cfg['t_final']:g}" if weak else ""),
+        "scaling": "weak" if weak else "strong", "n_gpus": world, "n_t": h.levels[0]["n_t"],
+        "dofs": h.size(0), "dofs_per_gpu": n0, "iterations": its[0],
+        "ms_per_solve": 1e3 * t / steps, "ms_per_vcycle": 1e3 * t / sum(its),
+        "value": work / t, "unit": UNIT, "steps": steps, "warmup": warmup,
+        "updown_gbs_per_rank": gather_obj(dist, gbs),
+        "updown_ms_per_launch_rank0": (ms / nl) if nl else None,
+    }
+    del f, u, h
+    gc.collect()
+    return rec
+
+
+def run_ours(args, cfgname):
+    import gc
+    world, rank, local, dist = dist_setup(args.gpus)
+    from paper_1411_0519_b200 import stmg
+    from paper_1411_0519_b200 import _capi as A
     import ctypes as C
+    # main line: configs[1] at N = 1; weak in time over N ranks (tau fixed)
+    cfg = scaled(cfgname, world, weak=True)
+    scaling = "weak" if world > 1 else "strong"
+    parallelism = ("single GPU" if world == 1 else
+                   f"time slabs x{world} (NCCL halo send/recv, coarse levels gathered on rank 0)")
+    t_setup0 = time.perf_counter()
+    h = make_hierarchy(stmg, cfg, world, rank, local, dist)
+    L0 = h.levels[0]
+    nlev = len(h.levels)
+    f = local_inputs(stmg, h, cfg)
+    n0 = f.n
+    u = h.local_vector()
+    ccfg = stmg.CycleConfig(nu1=1, nu2=1, gamma=1, omega_t=0.5)
     flush = C.c_void_p()
     A.check(A.lib().stmg_device_alloc(h._ctx, L2_FLUSH_BYTES, C.byref(flush)))
 
@@ -273,7 +414,11 @@ def run_ours(args, cfgname):
         h.synchronize()
         return h.solve(f, u, ccfg, EPS)
 
-    for _ in range(args.warmup):
+    first = one_step()  # context setup: coarse operator, graph capture
+    h.synchronize()
+    setup = {"create_and_first_solve_ms": 1e3 * (time.perf_counter() - t_setup0),
+             "first_solve_device_ms": 1e3 * first.device_time_seconds}
+    for _ in range(max(args.warmup - 1, 0)):
         one_step()
     launches0 = h.launch_count()
     clocks = ClockSampler(local)
@@ -311,13 +456,14 @@ def run_ours(args, cfgname):
     ms_per_step = 1e3 * total_dev / args.steps
 
     # end to end through the C ABI with pinned host buffers
-    hf = C.c_void_p()
-    hu = C.c_void_p()
-    A.check(A.lib().stmg_host_alloc(h._ctx, n0 * 8, C.byref(hf)))
-    A.check(A.lib().stmg_host_alloc(h._ctx, n0 * 8, C.byref(hu)))
-    hf_np = np.ctypeslib.as_array((C.c_double * n0).from_address(hf.value))
-    hu_np = np.ctypeslib.as_array((C.c_double * n0).from_address(hu.value))
+    hf, hu, hu2 = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    for p_ in (hf, hu, hu2):
+        A.check(A.lib().stmg_host_alloc(h._ctx, n0 * 8, C.byref(p_)))
+    arr = lambda p_: np.ctypeslib.as_array((C.c_double * n0).from_address(p_.value))  # noqa: E731
+    hf_np, hu_np, hu2_np = arr(hf), arr(hu), arr(hu2)
     A.check(A.lib().stmg_download(h._ctx, hf.value, f.ptr, n0 * 8))
+    # reference-shaped single call: solve(f, u) with u (the zero initial guess)
+    # uploaded and the result downloaded, copies serialised with the solve
     e2e_s, e2e_it = [], []
     for k in range(args.warmup + args.steps):
         hu_np[:] = 0.0
@@ -331,21 +477,13 @@ def run_ours(args, cfgname):
     e2e1_total = allreduce_max(dist, local, sum(e2e_s))
     e2e1_work = allreduce_sum(dist, local, float(n0 * sum(e2e_it)))
     # the same solves streamed through stmg_solve_host_batch: step i+1's H2D
-    # and step i-1's D2H run on the copy engines during solve i (pinned f, u0
-    # and two pinned output buffers; every step still moves 2 vectors in and
-    # 1 out over PCIe)
-    hu2 = C.c_void_p()
-    hz = C.c_void_p()
-    A.check(A.lib().stmg_host_alloc(h._ctx, n0 * 8, C.byref(hu2)))
-    A.check(A.lib().stmg_host_alloc(h._ctx, n0 * 8, C.byref(hz)))
-    hu2_np = np.ctypeslib.as_array((C.c_double * n0).from_address(hu2.value))
-    hz_np = np.ctypeslib.as_array((C.c_double * n0).from_address(hz.value))
-    hz_np[:] = 0.0  # u0 = 0 as in the single-call loop
+    # and step i-1's D2H run on the copy engines during solve i; zero initial
+    # guess (nothing uploaded for it), so every step moves f in and u out
     outs = [hu_np, hu2_np]
 
     def batch(k):
         return h.solve_host_batch([hf_np] * k, [outs[i % 2] for i in range(k)], ccfg, EPS,
-                                  u0s=[hz_np] * k)
+                                  u0s=[None] * k)
 
     batch(args.warmup)
     h.synchronize()
@@ -356,9 +494,11 @@ def run_ours(args, cfgname):
     tb = time.perf_counter() - tb0
     if not all(r.converged for r in breps):
         raise RuntimeError("batched solve did not converge")
+    if [r.iterations for r in breps] != iters:
+        raise RuntimeError("batched solves disagree with the device-resident solves")
     e2e_total = allreduce_max(dist, local, tb)
     e2e_work = allreduce_sum(dist, local, float(n0 * sum(r.iterations for r in breps)))
-    for p_ in (hf, hu, hu2, hz):
+    for p_ in (hf, hu, hu2):
         A.lib().stmg_host_free(h._ctx, p_)
 
     peak, peak_kind = peaks()
@@ -377,18 +517,35 @@ def run_ours(args, cfgname):
             "frac": achieved / peak, "traffic": traffic_from_profiles(tag),
             "kernel": names[dom], "peak_kind": peak_kind,
             "algorithmic_bytes_per_launch": b, "avg_launch_ms": avg_s * 1e3,
-            "step_share": sum(prof[k][0] for k in names) / (1e3 * sum(prof_dev)) if prof_dev else None,
+            "launches_per_step": nl / max(len(prof_dev), 1),
+            # share of the TIMED (unprofiled) device time per step
+            "step_share": (ms / max(len(prof_dev), 1)) / ms_per_step,
             "measured": "CUDA events on the library stream around every launch, in a replay of "
                         "the K timed steps right after the timed region",
             "transform_ms_per_solve": prof[2][0] / max(len(prof_dev), 1)}
+    del f, u
+    A.lib().stmg_device_free(h._ctx, flush)
+    h.close()
+    del h
+    gc.collect()
+
+    subs = {}
+    if not args.no_scaling:
+        subs["C3_strong"] = scaling_record(stmg, "C3_strong", "C3", False, world, rank, local,
+                                           dist, args.scaling_steps, 1)
+        subs["C5_weak"] = scaling_record(stmg, "C5_weak", "C5", True, world, rank, local, dist,
+                                         args.scaling_steps, 1)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded splitmix64 uniform[-1,1], f and u0)",
-        "config": {"workload": cfg["desc"], "dofs": h.size(0), "dofs_per_gpu": n0,
-                   "n_t": L0["n_t"], "levels": len(h.levels),
+        "config": {"workload": cfg["desc"] + (f"; weak in time over {world} GPUs: N_t = "
+                                              f"{L0['n_t']}, T = {cfg['t_final']:g}"
+                                              if world > 1 else ""),
+                   "dofs": sum(gather_obj(dist, n0)), "dofs_per_gpu": n0,
+                   "n_t": L0["n_t"], "levels": nlev,
                    "cycle": "V(1,1), omega_t=0.5, exact DG block solves, mu-driven coarsening",
                    "eps": EPS, "step": "one full solve to 1e-8 incl. sine-basis transforms",
                    "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB memset); vector {n0 * 8 / 1e6:.0f} MB",
@@ -397,48 +554,64 @@ def run_ours(args, cfgname):
                            "while node, device-side stop test)"},
         "iterations": iters[0], "time_to_1e-8_ms": ms_per_step,
         "wall_ms_per_step_incl_flush": 1e3 * t_wall / args.steps,
+        "setup": setup,
         "e2e": {"value": e2e_work / e2e_total, "unit": UNIT,
-                "h2d_bytes_per_step": 2 * n0 * 8, "d2h_bytes_per_step": n0 * 8,
+                "h2d_bytes_per_step": n0 * 8, "d2h_bytes_per_step": n0 * 8,
                 "ms_per_step": 1e3 * e2e_total / args.steps,
-                "api": "stmg_solve_host_batch (pinned host f/u0 in, u out; H2D of step i+1 and "
-                       "D2H of step i-1 overlap solve i; wall clock around the K-step batch)",
-                "single_call": {"value": e2e1_work / e2e1_total, "unit": UNIT,
-                                "ms_per_step": 1e3 * e2e1_total / args.steps,
-                                "api": "stmg_solve_host, one call per step, copies serialised "
-                                       "with the solve"}},
+                "api": "stmg_solve_host_batch (pinned host f in, u out, zero initial guess; H2D "
+                       "of step i+1 and D2H of step i-1 overlap solve i; wall clock around the "
+                       "K-step batch)",
+                "single_call": {"value": e2e1_work / e2e1_total,
+                                "unit": UNIT, "ms_per_step": 1e3 * e2e1_total / args.steps,
+                                "h2d_bytes_per_step": 2 * n0 * 8, "d2h_bytes_per_step": n0 * 8,
+                                "api": "stmg_solve_host (reference-shaped solve(f, u)), one call "
+                                       "per step, f and u uploaded, u downloaded, copies "
+                                       "serialised with the solve"}},
         "gpu_launches": int(launches),
         "roofline": roof,
         "clocks": clk,
+        "scaling_runs": subs,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        times, n0c = cpu_reference_cycles(cfg, args.cpu_cycles)
+        times, n0c = cpu_reference_cycles(CONFIGS[cfgname], args.cpu_cycles, 1)
         per = sum(times) / len(times)
         line["cpu_baseline"] = {
             "value": n0c / per, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{args.cpu_cycles} V(1,1) cycles (+ stop-test residual/norm) of {cfgname} "
-                      f"from a zero guess on the CPU oracle, OpenMP over time steps"}
+            "sample": f"{args.cpu_cycles} V(1,1) cycles (+ stop-test residual/norm each) of "
+                      f"{cfgname} from a zero guess on the CPU oracle, 1 untimed, OpenMP over "
+                      f"time steps; value = dofs / mean cycle time (same definition as "
+                      f"--impl reference)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
+        dist.barrier()
         dist.destroy_process_group()
     return 0
 
 
-def main():
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
-    ap.add_argument("--cpu-cycles", type=int, default=3)
+    ap.add_argument("--cpu-cycles", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args()
+    ap.add_argument("--scaling-steps", type=int, default=3,
+                    help="timed solves per scaling sub-record (C3 strong, C5 weak)")
+    ap.add_argument("--no-scaling", action="store_true")
+    args = ap.parse_args(argv)
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args, args.config)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args, argv)
     return run_ours(args, args.config)
 
 

@@ -205,8 +205,13 @@ int stmg_solve_host(stmg_ctx* ctx, const double* f_host, double* u_host,
  * call): a batch of independent solves (many right-hand sides / initial
  * guesses) streamed through one context.  Problem i solves from u0_host[i]
  * (u0_host NULL: u_host[i] in place) into u_host[i] while the H2D of problem
- * i+1 and the D2H of problem i-1 run on the copy engines (three device
- * staging sets).  Each result is bitwise stmg_solve_host's.  reports (optional) gets
+ * i+1 and i+2 and the D2H of problem i-1 run on the copy engines (three
+ * device staging sets).  Each result is bitwise stmg_solve_host's.  Because
+ * uploads run two problems ahead, the inputs of problem j (f_host[j] and
+ * u0_host[j], or u_host[j] in place) must not overlap u_host[j-1] or
+ * u_host[j-2]; an overlapping batch fails with STMG_EINVAL.  A NULL entry
+ * u0_host[i] (u0_host itself non-NULL) is a zero initial guess: nothing is
+ * uploaded for it (the device buffer is cleared), so only f crosses PCIe.  reports (optional) gets
  * count entries; wall_time_seconds there is per solve, without the overlapped
  * copies.  Host buffers should be pinned (stmg_host_alloc) for the copies to
  * overlap. */

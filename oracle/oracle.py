@@ -100,6 +100,8 @@ def lib():
             getattr(L, name).argtypes = [C.c_void_p, C.c_int, P, P]
         L.or_residual.argtypes = [C.c_void_p, C.c_int, P, P, P]
         L.or_norm.argtypes = [C.c_void_p, C.c_int, P]
+        L.or_residual_norm.restype = C.c_double
+        L.or_residual_norm.argtypes = [C.c_void_p, C.c_int, P, P]
         L.or_smooth.argtypes = [C.c_void_p, C.c_int, P, P, C.c_double, C.c_int]
         L.or_smooth_ex.argtypes = [C.c_void_p, C.c_int, P, P, C.POINTER(_Smoother)]
         L.or_spatial_vcycle.argtypes = [C.c_void_p, C.c_int, P, P, P, C.POINTER(_Smoother)]
@@ -216,6 +218,18 @@ class Hierarchy:
 
     def norm(self, level, v):
         return lib().or_norm(self._h, level, _ptr(v))
+
+    def residual_norm(self, level, u, f):
+        """norm(residual(u, f)) without a residual vector (bitwise the same)."""
+        return lib().or_residual_norm(self._h, level, _ptr(u), _ptr(f))
+
+    def mg_cycle_inplace(self, level, u, f, nu1=1, nu2=1, gamma=1, omega_t=0.5,
+                         block_solver="exact", **sp):
+        """mg_cycle on u in place (no copy; full-size fixture generation)."""
+        assert u.dtype == np.float64 and u.flags.c_contiguous
+        cfg = _cycle(nu1, nu2, gamma, omega_t, block_solver, **sp)
+        _check(lib().or_mg_cycle(self._h, level, _ptr(u), _ptr(f), C.byref(cfg)))
+        return u
 
     def block_solve(self, level, b):
         x = np.zeros_like(b)

@@ -411,6 +411,30 @@ void dst_axis(const Level& L, int axis, const double* in, double* out) {
   const Grid& g = L.grid;
   const i64 s = axis_stride(g, axis), n1 = g.n1, blk = s * n1;
   const double* S = L.S.data();
+  if (s == 1) {
+    // x axis: lines are contiguous.  Transpose kB lines into a tile so the
+    // sum over i (ascending, the same order as below) runs on kB independent
+    // accumulators instead of one dependent FMA chain.
+    constexpr i64 kB = 8;
+    std::vector<double> tile(n1 * kB), acc(kB);
+    const i64 nlines = g.nx / n1;
+    for (i64 l0 = 0; l0 < nlines; l0 += kB) {
+      const i64 nb = std::min(kB, nlines - l0);
+      for (i64 l = 0; l < nb; ++l)
+        for (i64 i = 0; i < n1; ++i) tile[i * kB + l] = in[(l0 + l) * n1 + i];
+      for (i64 k = 0; k < n1; ++k) {
+        for (i64 l = 0; l < kB; ++l) acc[l] = 0.0;
+        const double* Sk = S + k * n1;
+        for (i64 i = 0; i < n1; ++i) {
+          const double c = Sk[i];
+          const double* t = tile.data() + i * kB;
+          for (i64 l = 0; l < kB; ++l) acc[l] += c * t[l];
+        }
+        for (i64 l = 0; l < nb; ++l) out[(l0 + l) * n1 + k] = acc[l];
+      }
+    }
+    return;
+  }
   for (i64 base = 0; base < g.nx; base += blk)
     for (i64 k = 0; k < n1; ++k) {
       double* o = out + base + k * s;
@@ -474,10 +498,10 @@ void block_solve(const Level& L, const double* b, double* x) {
 }
 
 // st_system.cpp:25-33: y_n = (M U_n) K^T + (K U_n) M^T - (M U_{n-1}) N^T.
-void apply_block_row(const Level& L, const double* u, i64 n, double* y) {
+// un = step n's slab, up = step n-1's slab (nullptr for n = 0), y = output slab.
+void apply_slab(const Level& L, const double* un, const double* up, double* y) {
   const i64 nx = L.grid.nx;
   const int nl = L.dg.nl();
-  const double* un = u + n * nl * nx;
   std::vector<double> MU(nl * nx), KU(nl * nx), out(nl * nx, 0.0);
   for (int l = 0; l < nl; ++l) {
     space_apply(L.grid, false, un + l * nx, MU.data() + l * nx);
@@ -493,8 +517,7 @@ void apply_block_row(const Level& L, const double* u, i64 n, double* y) {
       const double a = L.dg.M[k * nl + l];
       for (i64 r = 0; r < nx; ++r) out[k * nx + r] += KU[l * nx + r] * a;
     }
-  if (n > 0) {
-    const double* up = un - nl * nx;
+  if (up) {
     for (int l = 0; l < nl; ++l) space_apply(L.grid, false, up + l * nx, MU.data() + l * nx);
     for (int k = 0; k < nl; ++k)
       for (int l = 0; l < nl; ++l) {
@@ -502,7 +525,12 @@ void apply_block_row(const Level& L, const double* u, i64 n, double* y) {
         for (i64 r = 0; r < nx; ++r) out[k * nx + r] -= MU[l * nx + r] * a;
       }
   }
-  std::copy(out.begin(), out.end(), y + n * nl * nx);
+  std::copy(out.begin(), out.end(), y);
+}
+
+void apply_block_row(const Level& L, const double* u, i64 n, double* y) {
+  const i64 sl = L.slab();
+  apply_slab(L, u + n * sl, n > 0 ? u + (n - 1) * sl : nullptr, y + n * sl);
 }
 
 void apply(const Level& L, const double* u, double* y) {
@@ -535,6 +563,30 @@ double norm(const Level& L, const double* v) {
   return std::sqrt(sum);
 }
 
+// norm(residual(u, f)) without materialising r: the same per-step partials
+// (slab order) summed in step order, so the value is bitwise norm(r).
+double residual_norm(const Level& L, const double* u, const double* f) {
+  const i64 sl = L.slab();
+  std::vector<double> part(L.n_t);
+#pragma omp parallel
+  {
+    std::vector<double> y(sl);
+#pragma omp for schedule(static)
+    for (i64 n = 0; n < L.n_t; ++n) {
+      apply_slab(L, u + n * sl, n > 0 ? u + (n - 1) * sl : nullptr, y.data());
+      double s = 0.0;
+      for (i64 i = 0; i < sl; ++i) {
+        const double r = f[n * sl + i] - y[i];
+        s += r * r;
+      }
+      part[n] = s;
+    }
+  }
+  double sum = 0.0;
+  for (double p : part) sum += p;
+  return std::sqrt(sum);
+}
+
 // st_system.cpp:118-130.
 void forward_substitution(const Level& L, const double* f, double* u) {
   const i64 nx = L.grid.nx, sl = L.slab();
@@ -555,17 +607,36 @@ void forward_substitution(const Level& L, const double* f, double* u) {
   }
 }
 
-// smoother.cpp:96-106 (exact block solves).
+// smoother.cpp:96-106 (exact block solves).  Frozen-residual Jacobi,
+// u_n += omega A^-1 (f_n - A_nn u_n - B u_{n-1}) with the OLD iterate, done in
+// place without a full residual vector: the steps are split into chunks, each
+// chunk's left-neighbour slab is saved first, and a chunk is swept from its
+// last step down so every step still sees the old u_{n-1}.  The arithmetic is
+// exactly residual() + block_solve() per step.
 void smooth(const Level& L, double* u, const double* f, double omega, int nu) {
-  const i64 sl = L.slab();
-  std::vector<double> r(L.size());
+  const i64 sl = L.slab(), nt = L.n_t;
+  const i64 nchunk = std::min<i64>(nt, 256);
+  std::vector<i64> start(nchunk + 1);
+  for (i64 c = 0; c <= nchunk; ++c) start[c] = c * nt / nchunk;
+  std::vector<double> left(nchunk * sl);
   for (int s = 0; s < nu; ++s) {
-    residual(L, u, f, r.data());
 #pragma omp parallel for schedule(static)
-    for (i64 n = 0; n < L.n_t; ++n) {
-      std::vector<double> x(sl);
-      block_solve(L, r.data() + n * sl, x.data());
-      for (i64 i = 0; i < sl; ++i) u[n * sl + i] += omega * x[i];
+    for (i64 c = 1; c < nchunk; ++c)
+      std::copy(u + (start[c] - 1) * sl, u + start[c] * sl, left.data() + c * sl);
+#pragma omp parallel
+    {
+      std::vector<double> r(sl), x(sl);
+#pragma omp for schedule(static)
+      for (i64 c = 0; c < nchunk; ++c)
+        for (i64 n = start[c + 1] - 1; n >= start[c]; --n) {
+          const double* up = n == 0 ? nullptr
+                             : n == start[c] ? left.data() + c * sl
+                                             : u + (n - 1) * sl;
+          apply_slab(L, u + n * sl, up, r.data());
+          for (i64 i = 0; i < sl; ++i) r[i] = f[n * sl + i] - r[i];
+          block_solve(L, r.data(), x.data());
+          for (i64 i = 0; i < sl; ++i) u[n * sl + i] += omega * x[i];
+        }
     }
   }
 }
@@ -860,16 +931,26 @@ void mg_cycle(const Hier& H, size_t lev, double* u, const double* f, const or_cy
     return;
   }
   smooth_cfg(L, u, f, cfg, cfg.nu1);
-  std::vector<double> r(L.size());
-  residual(L, u, f, r.data());
   const Level& C = H.levels[lev + 1];
-  std::vector<double> rc(C.size()), ec(C.size(), 0.0), corr(L.size());
-  restrict_level(H, int(lev), 0, r.data(), rc.data());
-  for (int g = 0; g < cfg.gamma; ++g) mg_cycle(H, lev + 1, ec.data(), rc.data(), cfg);
-  prolong_level(H, int(lev), 0, ec.data(), corr.data());
-  const i64 sz = L.size();
+  // Temporaries are scoped so at most one fine-level vector is alive besides
+  // u and f (full-size fixtures of C3/C5 run on the CPU box).
+  std::vector<double> ec(C.size(), 0.0);
+  {
+    std::vector<double> rc(C.size());
+    {
+      std::vector<double> r(L.size());
+      residual(L, u, f, r.data());
+      restrict_level(H, int(lev), 0, r.data(), rc.data());
+    }
+    for (int g = 0; g < cfg.gamma; ++g) mg_cycle(H, lev + 1, ec.data(), rc.data(), cfg);
+  }
+  {
+    std::vector<double> corr(L.size());
+    prolong_level(H, int(lev), 0, ec.data(), corr.data());
+    const i64 sz = L.size();
 #pragma omp parallel for schedule(static)
-  for (i64 i = 0; i < sz; ++i) u[i] += corr[i];
+    for (i64 i = 0; i < sz; ++i) u[i] += corr[i];
+  }
   smooth_cfg(L, u, f, cfg, cfg.nu2);
 }
 
@@ -979,6 +1060,12 @@ int or_residual(const or_hier* h, int level, const double* u, const double* f, d
   return guard([&] { residual(level_of(h, level), u, f, r); });
 }
 
+double or_residual_norm(const or_hier* h, int level, const double* u, const double* f) {
+  double out = NAN;
+  guard([&] { out = residual_norm(level_of(h, level), u, f); });
+  return out;
+}
+
 double or_norm(const or_hier* h, int level, const double* v) {
   double out = NAN;
   guard([&] { out = norm(level_of(h, level), v); });
@@ -1056,9 +1143,7 @@ int or_solve(const or_hier* h, const double* f, double* u, const or_cycle* cfg, 
     if (!(eps > 0.0)) throw std::invalid_argument("eps_mg must be positive");
     const Level& L = level_of(h, 0);
     const auto t0 = std::chrono::steady_clock::now();
-    std::vector<double> r(L.size());
-    residual(L, u, f, r.data());
-    const double r0 = norm(L, r.data());
+    const double r0 = residual_norm(L, u, f);
     int it = 0, conv = 0, nh = 0;
     if (history && nh < history_cap) history[nh++] = r0;
     if (r0 == 0.0) {
@@ -1066,8 +1151,7 @@ int or_solve(const or_hier* h, const double* f, double* u, const or_cycle* cfg, 
     } else {
       for (int k = 0; k < max_iter; ++k) {
         mg_cycle(h->H, 0, u, f, *cfg);
-        residual(L, u, f, r.data());
-        const double rk = norm(L, r.data());
+        const double rk = residual_norm(L, u, f);
         if (history && nh < history_cap) history[nh++] = rk;
         ++it;
         if (rk <= eps * r0) {

@@ -83,6 +83,9 @@ int or_apply(const or_hier* h, int level, const double* u, double* y);
 int or_residual(const or_hier* h, int level, const double* u, const double* f,
                 double* r);
 double or_norm(const or_hier* h, int level, const double* v);
+/* norm(residual(u, f)) without a residual vector (bitwise the same value). */
+double or_residual_norm(const or_hier* h, int level, const double* u,
+                        const double* f);
 int or_block_solve(const or_hier* h, int level, const double* b, double* x);
 int or_forward_substitution(const or_hier* h, int level, const double* f,
                             double* u);

@@ -201,6 +201,11 @@ struct stmg_ctx {
   double** d_pp = nullptr;
   int* d_par = nullptr;
   std::map<std::string, cudaGraphExec_t> fused_bodies;  // per-cycle graphs (profiling)
+  // buffer indices (c->cur, then every shard's cur) a captured loop / body
+  // leaves behind; restored when the cached graph is replayed instead of
+  // re-captured, so host code after it (the fused suffix) reads the buffers
+  // the graph actually wrote
+  std::map<std::string, std::vector<std::vector<int>>> cur_after;
   int* d_iter = nullptr;
   double* d_r0 = nullptr;
   bool use_device_loop = true;
@@ -220,6 +225,35 @@ struct stmg_ctx {
 namespace {
 
 // ---------------------------------------------------------------- helpers
+// Entry points that take a context run on its device and restore the caller's.
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(const stmg_ctx* c) {
+    if (c) enter(c->device);
+  }
+  explicit DevGuard(int device) { enter(device); }
+  void enter(int device) {
+    int d = 0;
+    if (cudaGetDevice(&d) == cudaSuccess && d != device) {
+      prev = d;
+      cudaSetDevice(device);
+    }
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DevGuard(const DevGuard&) = delete;
+  DevGuard& operator=(const DevGuard&) = delete;
+};
+
+template <class F>
+int cguard(const stmg_ctx* c, F&& fn) {
+  return guard([&] {
+    DevGuard dg(c);
+    fn();
+  });
+}
+
 Level& lev(stmg_ctx* c, int level) {
   require(c != nullptr, "null context");
   require(level >= 0 && level < int(c->levels.size()), "level index out of range");
@@ -400,7 +434,12 @@ void* mapped(void* h) {
 
 void tiny(stmg_ctx* c, std::initializer_list<TinyOp> ops) {
   TinyOps t{};
-  for (const TinyOp& o : ops) t.op[t.n++] = o;
+  require(ops.size() <= sizeof(t.op) / sizeof(t.op[0]), "internal: too many tiny ops");
+  for (const TinyOp& o : ops) {
+    require(o.bytes > 0 && o.bytes % 4 == 0 && (o.src || o.bytes <= 8),
+            "internal: tiny op size must be a positive multiple of 4 bytes");
+    t.op[t.n++] = o;
+  }
   k_tiny<<<1, 128, 0, c->stream>>>(t);
   CK(cudaGetLastError());
   count(c);
@@ -1016,8 +1055,12 @@ void check_cfg(const stmg_cycle_config* cfg) {
 void ensure_hist(stmg_ctx* c, int n) {
   if (c->hist_cap >= n) return;
   n = std::max(n, 1024);
-  for (auto& kv : c->loops) cudaGraphExecDestroy(kv.second);  // they bake d_hist in
+  // every cached loop and fused body bakes d_hist in (k_decide / k_norm_decide)
+  for (auto& kv : c->loops) cudaGraphExecDestroy(kv.second);
   c->loops.clear();
+  for (auto& kv : c->fused_bodies) cudaGraphExecDestroy(kv.second);
+  c->fused_bodies.clear();
+  c->cur_after.clear();
   if (c->d_hist) cudaFree(c->d_hist);
   if (c->h_hist) cudaFreeHost(c->h_hist);
   c->h_hist = nullptr;
@@ -1075,6 +1118,9 @@ stmg_ctx::GraphEntry& cycle_graph(stmg_ctx* c, const stmg_cycle_config& cfg) {
   return c->graphs[key] = e;
 }
 
+std::vector<std::vector<int>> cur_snapshot(const stmg_ctx* c);
+void cur_restore(stmg_ctx* c, const std::vector<std::vector<int>>& s);
+
 // Buffer flips of the finest level per V-cycle (each sweep ping-pongs).
 int nu_flips(const stmg_cycle_config& cfg) { return std::max(cfg.nu1, 1) + std::max(cfg.nu2, 1); }
 
@@ -1086,7 +1132,10 @@ template <class Body>
 cudaGraphExec_t device_loop(stmg_ctx* c, const std::string& key, double eps, int max_iter,
                             Body&& body, int* parity = nullptr) {
   auto it = c->loops.find(key);
-  if (it != c->loops.end()) return it->second;
+  if (it != c->loops.end()) {
+    cur_restore(c, c->cur_after.at(key));
+    return it->second;
+  }
   cudaGraph_t g;
   CK(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle h;
@@ -1130,6 +1179,7 @@ cudaGraphExec_t device_loop(stmg_ctx* c, const std::string& key, double eps, int
   CK(cudaGraphDestroy(g));
   c->loops[key] = exec;
   c->loop_kernels[key] = c->captured_kernels;
+  c->cur_after[key] = cur_snapshot(c);
   return exec;
 }
 
@@ -1270,6 +1320,9 @@ void run_fused(stmg_ctx* c, const stmg_cycle_config& cfg, double eps, int max_it
       CK(cudaGraphInstantiate(&ex, g, 0));
       CK(cudaGraphDestroy(g));
       it = c->fused_bodies.emplace(key, ex).first;
+      c->cur_after[key] = cur_snapshot(c);
+    } else {
+      cur_restore(c, c->cur_after.at(key));
     }
     for (int k = 0; k < max_iter; ++k) {
       CK(cudaGraphLaunch(it->second, c->stream));
@@ -1488,6 +1541,20 @@ struct ShardSet {
 };
 
 bool is_root(const ShardSet& ss, const Shard& sh) { return sh.g == 0; }
+
+std::vector<std::vector<int>> cur_snapshot(const stmg_ctx* c) {
+  std::vector<std::vector<int>> s{c->cur};
+  if (c->shards)
+    for (const Shard& sh : c->shards->local) s.push_back(sh.cur);
+  return s;
+}
+
+void cur_restore(stmg_ctx* c, const std::vector<std::vector<int>>& s) {
+  c->cur = s.at(0);
+  if (c->shards)
+    for (size_t i = 0; i < c->shards->local.size() && i + 1 < s.size(); ++i)
+      c->shards->local[i].cur = s[i + 1];
+}
 
 int gather_level(stmg_ctx* c, int S) {
   std::vector<stmg::LevelSpec> specs;
@@ -1875,6 +1942,9 @@ void run_sharded_fused(stmg_ctx* c, const stmg_cycle_config& cfg, double eps, in
       CK(cudaGraphDestroy(g));
       c->loop_kernels[key] = c->captured_kernels;
       it = c->fused_bodies.emplace(key, ex).first;
+      c->cur_after[key] = cur_snapshot(c);
+    } else {
+      cur_restore(c, c->cur_after.at(key));
     }
     CK(cudaGraphLaunch(it->second, c->stream));
     c->launches += c->loop_kernels[key];
@@ -2114,7 +2184,7 @@ int stmg_create(const stmg_hierarchy_params* p, stmg_ctx** out) {
     require(p->device >= 0 && p->device < ndev, "device ordinal out of range");
     auto c = std::make_unique<stmg_ctx>();
     c->device = p->device;
-    CK(cudaSetDevice(c->device));
+    DevGuard dg(c->device);  // the caller's current device is restored on return
     CK(stmg::init_kernel_tables());
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->p_t = p->p_t;
@@ -2156,7 +2226,7 @@ int stmg_create(const stmg_hierarchy_params* p, stmg_ctx** out) {
 int stmg_destroy(stmg_ctx* c) {
   return guard([&] {
     if (!c) return;
-    cudaSetDevice(c->device);
+    DevGuard dg(c->device);
     cudaStreamSynchronize(c->stream);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
     if (c->shards) {
@@ -2226,14 +2296,14 @@ int stmg_destroy(stmg_ctx* c) {
 }
 
 int stmg_num_levels(const stmg_ctx* c, int* out) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c && out, "null argument");
     *out = int(c->levels.size());
   });
 }
 
 int stmg_get_level_info(const stmg_ctx* cc, int level, stmg_level_info* o) {
-  return guard([&] {
+  return cguard(cc, [&] {
     stmg_ctx* c = const_cast<stmg_ctx*>(cc);
     require(o != nullptr, "null output");
     const Level& L = lev(c, level);
@@ -2251,22 +2321,21 @@ int stmg_get_level_info(const stmg_ctx* cc, int level, stmg_level_info* o) {
 }
 
 int stmg_level_size(const stmg_ctx* cc, int level, int64_t* out) {
-  return guard([&] {
+  return cguard(cc, [&] {
     require(out != nullptr, "null output");
     *out = lev(const_cast<stmg_ctx*>(cc), level).spec.size();
   });
 }
 
 int stmg_device_alloc(stmg_ctx* c, size_t bytes, void** dptr) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c && dptr, "null argument");
-    CK(cudaSetDevice(c->device));
     CK(cudaMalloc(dptr, bytes ? bytes : 8));
   });
 }
 
 int stmg_device_free(stmg_ctx* c, void* dptr) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c != nullptr, "null context");
     CK(cudaStreamSynchronize(c->stream));
     CK(cudaFree(dptr));
@@ -2274,14 +2343,14 @@ int stmg_device_free(stmg_ctx* c, void* dptr) {
 }
 
 int stmg_upload(stmg_ctx* c, void* dst, const void* src, size_t bytes) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c && (bytes == 0 || (dst && src)), "null argument");
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
   });
 }
 
 int stmg_download(stmg_ctx* c, void* dst, const void* src, size_t bytes) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c && (bytes == 0 || (dst && src)), "null argument");
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -2289,22 +2358,21 @@ int stmg_download(stmg_ctx* c, void* dst, const void* src, size_t bytes) {
 }
 
 int stmg_memset_zero(stmg_ctx* c, void* dst, size_t bytes) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c != nullptr, "null context");
     CK(cudaMemsetAsync(dst, 0, bytes, c->stream));
   });
 }
 
 int stmg_host_alloc(stmg_ctx* c, size_t bytes, void** hptr) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c && hptr, "null argument");
-    CK(cudaSetDevice(c->device));
     CK(cudaHostAlloc(hptr, bytes ? bytes : 8, cudaHostAllocDefault));
   });
 }
 
 int stmg_host_free(stmg_ctx* c, void* hptr) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c != nullptr, "null context");
     CK(cudaStreamSynchronize(c->stream));
     CK(cudaFreeHost(hptr));
@@ -2312,7 +2380,7 @@ int stmg_host_free(stmg_ctx* c, void* hptr) {
 }
 
 int stmg_synchronize(stmg_ctx* c) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c != nullptr, "null context");
     CK(cudaStreamSynchronize(c->stream));
     prof_collect(c);
@@ -2321,7 +2389,7 @@ int stmg_synchronize(stmg_ctx* c) {
 
 int stmg_fill_uniform(stmg_ctx* c, double* dst, int64_t n, uint64_t seed, uint64_t stream,
                       int64_t offset) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c && (n == 0 || dst), "null argument");
     CK(stmg::launch_fill_uniform(dst, n, seed, stream, offset, c->stream));
     count(c);
@@ -2329,7 +2397,7 @@ int stmg_fill_uniform(stmg_ctx* c, double* dst, int64_t n, uint64_t seed, uint64
 }
 
 int stmg_fold_u0(stmg_ctx* c, double* f, const double* u0) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(f && u0, "null vector");
     Level& L = lev(c, 0);
     CK(stmg::launch_fold_u0(L.view, f, u0, c->stream));
@@ -2338,7 +2406,7 @@ int stmg_fold_u0(stmg_ctx* c, double* f, const double* u0) {
 }
 
 int stmg_apply(stmg_ctx* c, int level, const double* u, double* y) {
-  return guard([&] {
+  return cguard(c, [&] {
     Level& L = lev(c, level);
     require(u && y, "null vector");
     CK(stmg::launch_apply(L.view, u, nullptr, y, false, L.d_tables + 3 * L.spec.n1(), c->stream));
@@ -2347,7 +2415,7 @@ int stmg_apply(stmg_ctx* c, int level, const double* u, double* y) {
 }
 
 int stmg_residual(stmg_ctx* c, int level, const double* u, const double* f, double* r) {
-  return guard([&] {
+  return cguard(c, [&] {
     Level& L = lev(c, level);
     require(u && f && r, "null vector");
     residual(c, L, u, f, r);
@@ -2355,7 +2423,7 @@ int stmg_residual(stmg_ctx* c, int level, const double* u, const double* f, doub
 }
 
 int stmg_norm(stmg_ctx* c, int level, const double* v, double* out) {
-  return guard([&] {
+  return cguard(c, [&] {
     Level& L = lev(c, level);
     require(v && out, "null argument");
     *out = norm_phys(c, L, v);
@@ -2363,7 +2431,7 @@ int stmg_norm(stmg_ctx* c, int level, const double* v, double* out) {
 }
 
 int stmg_block_solve(stmg_ctx* c, int level, const double* b, double* x) {
-  return guard([&] {
+  return cguard(c, [&] {
     Level& L = lev(c, level);
     require(b && x, "null vector");
     block_solve(c, L, b, x);
@@ -2371,7 +2439,7 @@ int stmg_block_solve(stmg_ctx* c, int level, const double* b, double* x) {
 }
 
 int stmg_smooth(stmg_ctx* c, int level, double* u, const double* f, double omega_t, int nu) {
-  return guard([&] {
+  return cguard(c, [&] {
     lev(c, level);
     require(u && f, "null vector");
     require(nu >= 0, "nu must be >= 0");
@@ -2395,7 +2463,7 @@ int stmg_smoother_config_init(stmg_smoother_config* cfg) {
 
 int stmg_block_jacobi_step(stmg_ctx* c, int level, double* u, const double* f,
                            const stmg_smoother_config* cfg) {
-  return guard([&] {
+  return cguard(c, [&] {
     lev(c, level);
     require(cfg != nullptr, "null smoother config");
     require(u && f, "null vector");
@@ -2414,7 +2482,7 @@ int stmg_block_jacobi_step(stmg_ctx* c, int level, double* u, const double* f,
 
 int stmg_spatial_vcycle(stmg_ctx* c, int level, const double* b, const double* x0, double* x,
                         const stmg_smoother_config* cfg) {
-  return guard([&] {
+  return cguard(c, [&] {
     Level& L = lev(c, level);
     require(cfg != nullptr, "null smoother config");
     require(b && x, "null vector");
@@ -2429,7 +2497,7 @@ int stmg_spatial_vcycle(stmg_ctx* c, int level, const double* b, const double* x
 }
 
 int stmg_restrict(stmg_ctx* c, int level, int mode, const double* fine, double* coarse) {
-  return guard([&] {
+  return cguard(c, [&] {
     Level& L = lev(c, level);
     require(fine && coarse, "null vector");
     mode = resolve_mode(L, mode);
@@ -2439,7 +2507,7 @@ int stmg_restrict(stmg_ctx* c, int level, int mode, const double* fine, double* 
 }
 
 int stmg_prolong(stmg_ctx* c, int level, int mode, const double* coarse, double* fine) {
-  return guard([&] {
+  return cguard(c, [&] {
     Level& L = lev(c, level);
     require(fine && coarse, "null vector");
     mode = resolve_mode(L, mode);
@@ -2449,7 +2517,7 @@ int stmg_prolong(stmg_ctx* c, int level, int mode, const double* coarse, double*
 }
 
 int stmg_forward_substitution(stmg_ctx* c, int level, const double* f, double* u) {
-  return guard([&] {
+  return cguard(c, [&] {
     Level& L = lev(c, level);
     require(f && u, "null vector");
     fwdsub_phys(c, L, f, u);
@@ -2458,7 +2526,7 @@ int stmg_forward_substitution(stmg_ctx* c, int level, const double* f, double* u
 
 int stmg_mg_cycle(stmg_ctx* c, int level, double* u, const double* f,
                   const stmg_cycle_config* cfg) {
-  return guard([&] {
+  return cguard(c, [&] {
     Level& L = lev(c, level);
     check_cfg(cfg);
     require(u && f, "null vector");
@@ -2479,7 +2547,7 @@ int stmg_mg_cycle(stmg_ctx* c, int level, double* u, const double* f,
 
 int stmg_solve(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config* cfg, double eps,
                int max_iter, double* history, int history_cap, stmg_solve_report* report) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c != nullptr, "null context");
     check_cfg(cfg);
     if (c->shards) solve_sharded(c, f, u, *cfg, eps, max_iter, history, history_cap, report);
@@ -2490,7 +2558,7 @@ int stmg_solve(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config*
 int stmg_solve_host(stmg_ctx* c, const double* f_host, double* u_host,
                     const stmg_cycle_config* cfg, double eps, int max_iter, double* history,
                     int history_cap, stmg_solve_report* report) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c != nullptr, "null context");
     check_cfg(cfg);
     require(f_host && u_host, "null vector");
@@ -2532,20 +2600,35 @@ int stmg_solve_host_batch(stmg_ctx* c, int count, const double* const* f_host,
                           const double* const* u0_host, double* const* u_host,
                           const stmg_cycle_config* cfg, double eps, int max_iter,
                           stmg_solve_report* reports) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c != nullptr, "null context");
     check_cfg(cfg);
     require(count >= 0, "count must be >= 0");
     if (count == 0) return;
     require(f_host != nullptr && u_host != nullptr, "null vector array");
-    for (int i = 0; i < count; ++i)
-      require(f_host[i] && u_host[i] && (!u0_host || u0_host[i]), "null vector");
+    for (int i = 0; i < count; ++i) require(f_host[i] && u_host[i], "null vector");
     require(eps > 0.0, "eps_mg must be positive");
     require(max_iter >= 0, "max_iter must be >= 0");
     constexpr int NS = stmg_ctx::kSets;
     Level& L0 = c->levels[0];
     const i64 n = (c->shards && c->shards->nccl) ? L0.view.size() / c->shards->S : L0.view.size();
     const size_t bytes = size_t(n) * sizeof(double);
+    {  // uploads run NS-1 problems ahead of the downloads: the buffers read by
+       // problem j's upload must not overlap u_host[i] of the NS-1 problems
+       // before it, whose results may still be in flight
+      auto overlap = [&](const void* a, const void* b) {
+        const char* x = static_cast<const char*>(a);
+        const char* y = static_cast<const char*>(b);
+        return x < y + bytes && y < x + bytes;
+      };
+      for (int j = 1; j < count; ++j)
+        for (int i = std::max(0, j - (NS - 1)); i < j; ++i) {
+          const void* src_u = u0_host ? static_cast<const void*>(u0_host[j]) : u_host[j];
+          require(!overlap(f_host[j], u_host[i]) && !(src_u && overlap(src_u, u_host[i])),
+                  "stmg_solve_host_batch: an input of problem j overlaps the output of one of "
+                  "the 2 problems before it (results are downloaded while later inputs upload)");
+        }
+    }
     DevBuf* F[NS] = {&c->user_f};
     DevBuf* U[NS] = {&c->user_u};
     for (int s = 1; s < NS; ++s) {
@@ -2590,11 +2673,12 @@ int stmg_solve_host_batch(stmg_ctx* c, int count, const double* const* f_host,
       if (i >= NS) CK(cudaStreamWaitEvent(c->s_in, c->ev_free[s], 0));
       tmark(i, 0, c->s_in);
       CK(cudaMemcpyAsync(F[s]->base, f_host[i], bytes, cudaMemcpyHostToDevice, c->s_in));
-      CK(cudaMemcpyAsync(U[s]->base, u0, bytes, cudaMemcpyHostToDevice, c->s_in));
+      if (u0) CK(cudaMemcpyAsync(U[s]->base, u0, bytes, cudaMemcpyHostToDevice, c->s_in));
+      else CK(cudaMemsetAsync(U[s]->base, 0, bytes, c->s_in));  // zero initial guess
       CK(cudaEventRecord(c->ev_in[s], c->s_in));
       tmark(i, 1, c->s_in);
     };
-    // uploads run NS-1 problems ahead: problem j's set was last used by
+    // uploads run NS-1 (= 2) problems ahead: problem j's set was last used by
     // problem j-NS, whose D2H (and its ev_free record) is already enqueued
     for (int j = 0; j < std::min(count, NS - 1); ++j) upload(j);
     for (int i = 0; i < count; ++i) {
@@ -2668,7 +2752,7 @@ int stmg_create_distributed(const stmg_hierarchy_params* p, int rank, int world,
       c->shards->local[0].g = rank;
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, sizeof(id));
-      CK(cudaSetDevice(c->device));
+      DevGuard dg(c->device);
       nccl_check(nccl().CommInitRank(&c->shards->comm, world, id, rank), "comm init");
       build_shards(c);
     }
@@ -2691,7 +2775,7 @@ int stmg_shard_plan(const stmg_hierarchy_params* p, int shards, int* gather_leve
 }
 
 int stmg_local_steps(const stmg_ctx* c, int64_t* first_step, int64_t* n_steps) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c && first_step && n_steps, "null argument");
     const i64 nt = c->levels[0].spec.n_t;
     if (c->shards && c->shards->nccl) {
@@ -2706,7 +2790,7 @@ int stmg_local_steps(const stmg_ctx* c, int64_t* first_step, int64_t* n_steps) {
 }
 
 int stmg_profile_enable(stmg_ctx* c, int on) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c != nullptr, "null context");
     if (bool(on) != c->profile) {  // re-capture with / without event nodes
       CK(cudaStreamSynchronize(c->stream));
@@ -2721,7 +2805,7 @@ int stmg_profile_enable(stmg_ctx* c, int on) {
 
 int stmg_profile_read(stmg_ctx* c, int id, double* total_ms, int64_t* launches,
                       double* bytes_per_launch) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c != nullptr, "null context");
     require(id >= 0 && id < 5, "kernel id out of range");
     CK(cudaStreamSynchronize(c->stream));
@@ -2733,7 +2817,7 @@ int stmg_profile_read(stmg_ctx* c, int id, double* total_ms, int64_t* launches,
 }
 
 int stmg_profile_reset(stmg_ctx* c) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c != nullptr, "null context");
     CK(cudaStreamSynchronize(c->stream));
     prof_collect(c);
@@ -2746,7 +2830,7 @@ int stmg_profile_reset(stmg_ctx* c) {
 }
 
 int stmg_launch_count(const stmg_ctx* c, int64_t* out) {
-  return guard([&] {
+  return cguard(c, [&] {
     require(c && out, "null argument");
     *out = c->launches;
   });

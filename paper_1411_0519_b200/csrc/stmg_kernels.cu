@@ -21,12 +21,25 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <vector>
 
 #include "stmg_modal.cuh"
 
 namespace stmg {
 namespace {
+
+// cudaFuncSetAttribute is per device: a launcher sets a kernel's attributes on
+// the first launch on each device (bit d of the mask = done on device d).
+struct PerDevice {
+  std::atomic<unsigned long long> mask{0};
+  bool first_use() {
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned long long b = 1ull << (d & 63);
+    return (mask.fetch_or(b) & b) == 0;
+  }
+};
 
 // ==================================================== fused spectral kernels
 // Loads: the standalone kernels read through the read-only / streaming paths;
@@ -3043,15 +3056,14 @@ cudaError_t launch_apply_rb(const LevelView& L, const double* u, const double* f
   const size_t smem = size_t(T::STAGES) *
                       (size_t(NL) * T::HALO + (residual ? size_t(NL) * T::OUT : 0)) *
                       sizeof(double);
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  if (attr.first_use()) {
     const int most = int(size_t(T::STAGES) * (size_t(NL) * T::HALO + size_t(NL) * T::OUT) *
                          sizeof(double));
     cudaFuncSetAttribute(k_apply_rb<DIM, NL, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, most);
     cudaFuncSetAttribute(k_apply_rb<DIM, NL, false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, most);
-    attr = true;
   }
   const TM<NL> t = make_tm<NL>(L.tc);
   if (residual)
@@ -3100,14 +3112,13 @@ cudaError_t launch_apply(const LevelView& L, const double* u, const double* f, d
         size_t(T::STAGES) *
         (size_t(NL) * T::HALO + (residual && !STMG_APPLY_FREG ? size_t(NL) * T::THREADS : 0)) *
         sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    if (attr.first_use()) {
       const int most = int(T::STAGES * 2 * size_t(NL) * T::HALO * sizeof(double));  // >= smem
       cudaFuncSetAttribute(k_apply<DIM, NL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            most);
       cudaFuncSetAttribute(k_apply<DIM, NL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            most);
-      attr = true;
     }
     if (residual)
       k_apply<DIM, NL, true><<<g, T::THREADS, smem, st>>>(u, f, y, t, n1, L.sp.nx, L.sp.h, L.n_t,
@@ -3189,11 +3200,10 @@ cudaError_t launch_dst_axis(const LevelView& L, int axis, const double* in, doub
   case K: {                                                                                \
     using SH = DSTShape<K>;                                                                \
     const unsigned grid = unsigned((n_lines + SH::TL - 1) / SH::TL);                       \
-    static bool attr_set = false;                                                          \
-    if (!attr_set) {                                                                       \
+    static PerDevice attr_set;                                                             \
+    if (attr_set.first_use()) {                                                            \
       cudaFuncSetAttribute(k_dst_lines<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                            int(SH::smem));                                                 \
-      attr_set = true;                                                                     \
     }                                                                                      \
     k_dst_lines<K><<<grid, SH::BLOCK, SH::smem, st>>>(in, out, n_lines, stride, scale, alpha, \
                                                  accumulate ? 1 : 0, tw);                  \
@@ -3325,10 +3335,9 @@ cudaError_t launch_cop_gemv(const double* B, const double* x, double* y, int n,
   if (n <= 0) return cudaSuccess;
   const size_t smem = size_t(kCopRows) * n * sizeof(double);
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {  // maximum shared-memory carveout: all rows of B in flight in one wave
+  static PerDevice attr;
+  if (attr.first_use()) {  // maximum shared-memory carveout: all rows of B in flight in one wave
     cudaFuncSetAttribute(k_cop_gemv, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    attr = true;
   }
   PDLK(k_cop_gemv, grid1(n, kCopRows), kCopRows * 32, smem, st, B, x, y, n);
   return cudaGetLastError();

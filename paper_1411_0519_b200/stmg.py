@@ -333,19 +333,21 @@ class Hierarchy:
                          u0s=None) -> List[SolveReport]:
         """Independent solves of HOST arrays streamed through the context
         (stmg_solve_host_batch): problem i+1's upload and problem i-1's download
-        overlap solve i.  us[i] is updated in place, or written from u0s[i]."""
+        overlap solve i.  us[i] is updated in place, or written from u0s[i]
+        (None: zero initial guess, no upload)."""
         _, n = self.local_steps()
         local = n * self.levels[0]["n_loc"] * self.levels[0]["n_x"]
         k = len(fs)
         if len(us) != k or (u0s is not None and len(u0s) != k):
             raise ValueError("batch length mismatch")
-        for a in list(fs) + list(us) + list(u0s or []):
+        for a in list(fs) + list(us) + [a for a in (u0s or []) if a is not None]:
             if a.dtype != np.float64 or a.size != local or not a.flags.c_contiguous:
                 raise ValueError("space-time vector shape mismatch")
         P = C.c_void_p * max(k, 1)
         pf = P(*[a.ctypes.data for a in fs])
         pu = P(*[a.ctypes.data for a in us])
-        p0 = P(*[a.ctypes.data for a in u0s]) if u0s is not None else None
+        # a None entry of u0s: zero initial guess (nothing uploaded)
+        p0 = P(*[a.ctypes.data if a is not None else None for a in u0s]) if u0s is not None else None
         reps = (A.SolveReport * max(k, 1))()
         c = cfg.c()
         check(A.lib().stmg_solve_host_batch(self._ctx, k, pf, p0, pu, C.byref(c), eps_mg, max_iter,

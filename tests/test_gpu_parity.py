@@ -364,3 +364,56 @@ def test_host_solves_match_device_solve(S):
         g.solve_host_batch(fs, us[:2], cfg, 1e-8)
     with pytest.raises(Exception):
         g.solve_host_batch(fs[:1], us[:1], cfg, -1.0)
+    # zero initial guesses (None: nothing uploaded) = solves from a zero vector
+    zref = []
+    for f in fs[:3]:
+        du = g.vector(0)
+        g.solve(g.upload(f), du, cfg, 1e-8)
+        zref.append(du.numpy())
+    outs = [np.full_like(u0s[0], 7.0) for _ in range(3)]
+    g.solve_host_batch(fs[:3], outs, cfg, 1e-8, u0s=[None] * 3)
+    for u, r in zip(outs, zref):
+        assert np.array_equal(u, r)
+    # inputs of problem j may not alias the outputs of the two problems before it
+    g.solve_host_batch(fs[:3], [outs[0], outs[1], outs[0]], cfg, 1e-8, u0s=[None] * 3)
+    assert np.array_equal(outs[0], zref[2])  # outputs may repeat: D2Hs are ordered
+    with pytest.raises(ValueError):  # in place: problem 2 uploads the buffer problem 0 downloads into
+        g.solve_host_batch(fs[:3], [outs[0], outs[1], outs[0]], cfg, 1e-8)
+    with pytest.raises(ValueError):
+        g.solve_host_batch(fs[:2], [outs[0], outs[1]], cfg, 1e-8, u0s=[None, outs[0]])
+
+
+def test_cached_fused_loop_after_other_cycle_shapes(S):
+    """A cached fused V(1,1) device loop replayed after cycles that move the
+    coarse buffer indices (mg_cycle, a V(2,1) solve) still returns the right
+    iterate: the suffix reads the coarse correction the graph wrote."""
+    g, o = pair(S, 1, 2, 4, 5, 1.0)
+    f = O.make_inputs(o, 42, random_u0=True)
+    u_o, rep_o = o.solve(f, eps=1e-8)
+    df = g.upload(f)
+    v11 = S.CycleConfig(nu1=1, nu2=1)
+    for _ in range(2):
+        du = g.vector(0)
+        rep = g.solve(df, du, v11, 1e-8)
+        assert rep.iterations == rep_o["iterations"] and rel(du.numpy(), u_o) < 1e-10
+        g.mg_cycle(0, g.vector(0), df, S.CycleConfig(nu1=2, nu2=1))
+        g.solve(df, g.vector(0), S.CycleConfig(nu1=2, nu2=1), 1e-8)
+
+
+@pytest.mark.parametrize("shards", [0, 2])
+def test_history_buffer_regrowth(S, shards):
+    """A solve with max_iter >= 1024 regrows the device history; later solves
+    with a smaller max_iter must not replay graphs that captured the old
+    buffer (fused bodies and device loops)."""
+    g = S.Hierarchy(1, 2, 4, 5, shards=shards)
+    o = O.Hierarchy(1, 2, 4, 5)
+    f = O.make_inputs(o, 42)
+    u_o, rep_o = o.solve(f, eps=1e-8)
+    df = g.upload(f)
+    cfg = S.CycleConfig(nu1=1, nu2=1)
+    for mi in (50, 1500, 50):
+        du = g.vector(0)
+        rep = g.solve(df, du, cfg, 1e-8, max_iter=mi)
+        assert rep.converged and rep.iterations == rep_o["iterations"]
+        assert rel(np.array(rep.residual_history), np.array(rep_o["residual_history"])) < 1e-10
+        assert rel(du.numpy(), u_o) < 1e-10

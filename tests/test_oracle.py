@@ -259,3 +259,21 @@ def test_generator_is_counter_based(oracle):
     assert a.min() >= -1.0 and a.max() < 1.0
     c = oracle.fill_uniform(1000, 42, 1)
     assert not np.array_equal(a, c)
+
+
+def test_full_c2_fixture_reproduces(oracle):
+    """tests/golden/full_C2.npz (tools/make_golden.py) is what the oracle
+    computes: its first two cycles and residual history entries."""
+    import json
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "full_C2.npz"))
+    m = json.loads(str(z["meta"]))
+    assert m["iterations"] == len(z["history"]) - 1 and m["converged"]
+    h = oracle.Hierarchy(m["p_t"], m["dim"], m["space_level"], m["time_level"], m["t_final"])
+    f = oracle.make_inputs(h, m["seed"], random_u0=m["random_u0"])
+    u = np.zeros_like(f)
+    assert h.residual_norm(0, u, f) == z["history"][0]
+    for k in (1, 2):
+        h.mg_cycle_inplace(0, u, f, 1, 1, 1, 0.5)
+        assert np.array_equal(u[z["idx"]], z[f"u{k}"])
+        assert h.residual_norm(0, u, f) == z["history"][k]
