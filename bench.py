@@ -399,6 +399,7 @@ def run_ours(args, cfgname):
                    f"time slabs x{world} (NCCL halo send/recv, coarse levels gathered on rank 0)")
     t_setup0 = time.perf_counter()
     h = make_hierarchy(stmg, cfg, world, rank, local, dist)
+    t_created = time.perf_counter()
     L0 = h.levels[0]
     nlev = len(h.levels)
     f = local_inputs(stmg, h, cfg)
@@ -414,10 +415,15 @@ def run_ours(args, cfgname):
         h.synchronize()
         return h.solve(f, u, ccfg, EPS)
 
+    t_first0 = time.perf_counter()
     first = one_step()  # context setup: coarse operator, graph capture
     h.synchronize()
-    setup = {"create_and_first_solve_ms": 1e3 * (time.perf_counter() - t_setup0),
-             "first_solve_device_ms": 1e3 * first.device_time_seconds}
+    setup = {"create_context_ms": 1e3 * (t_created - t_setup0),
+             "first_solve_wall_ms": 1e3 * (time.perf_counter() - t_first0),
+             "first_solve_device_ms": 1e3 * first.device_time_seconds,
+             "note": "context creation includes the process's first CUDA module load; the "
+                     "first solve builds the coarse operator (one launch) and captures the "
+                     "solve graph"}
     for _ in range(max(args.warmup - 1, 0)):
         one_step()
     launches0 = h.launch_count()

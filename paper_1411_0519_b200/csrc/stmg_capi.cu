@@ -220,6 +220,13 @@ struct stmg_ctx {
   // coarse operator: the tail's V(1,1) map F -> U as a dense matrix per omega_t
   std::map<double, double*> cop;
   bool use_cop = true;
+  // fused coarse levels csub_a..csub_b (alias-group trees, stmg_kernels.cu)
+  stmg::CsubPlan csub;
+  int csub_a = -1, csub_b = -1;
+  bool csub_decided = false;
+  // off by default: slower than the per-level kernels on C2-C5
+  // (profiles/r02_csub_ab.txt); STMG_CSUB=1 enables
+  bool use_csub = false;
 };
 
 namespace {
@@ -461,6 +468,16 @@ void dst_all(stmg_ctx* c, Level& L, const double* in, double* out, bool accumula
              double alpha = 1.0) {
   const int dim = L.spec.dim;
   prof_begin(c, 2);
+  if (dim == 2) {
+    const cudaError_t e =
+        stmg::launch_dst2d(L.view, in, out, accumulate, alpha, L.d_twiddle, c->stream);
+    if (e != cudaErrorNotSupported) {
+      CK(e);
+      count(c);
+      prof_end(c, 2, 16.0 * double(L.view.size()));  // algorithmic: read + write once
+      return;
+    }
+  }
   double* mid = accumulate ? const_cast<double*>(in) : out;
   for (int a = 0; a < dim; ++a) {
     const bool last = a + 1 == dim;
@@ -468,7 +485,7 @@ void dst_all(stmg_ctx* c, Level& L, const double* in, double* out, bool accumula
                              alpha, L.d_twiddle, c->stream));
     count(c);
   }
-  prof_end(c, 2, 16.0 * double(L.view.size()) * dim);
+  prof_end(c, 2, 16.0 * double(L.view.size()));  // algorithmic: read + write once
 }
 
 // Exact block solve on every step: x = A^-1 b (x may equal b).  When
@@ -679,6 +696,55 @@ void ensure_tail(stmg_ctx* c) {
   c->tail_smem = size_t(bytes + tab);
 }
 
+// ---- fused coarse levels ---------------------------------------------------
+// Levels a..b of a V(1,1) cycle (zero initial guess) run as two launches
+// (k_csub_down / k_csub_up) when they are small enough to be latency bound:
+// a = the first coarse level (>= 1) with at most kCsubMaxDofs unknowns,
+// b = the last level before the tail (or before the first level that is not
+// fully coarsened), at most kCsubMaxDepth levels.  Env: STMG_CSUB=0 disables,
+// STMG_CSUB_DEPTH / STMG_CSUB_LANES / STMG_CSUB_THREADS tune.
+constexpr i64 kCsubMaxDofs = i64(4) << 20;
+
+void ensure_csub(stmg_ctx* c) {
+  if (c->csub_decided) return;
+  c->csub_decided = true;
+  if (!c->use_csub) return;
+  const int nl = int(c->levels.size());
+  int a = -1;
+  i64 maxdofs = kCsubMaxDofs;
+  if (const char* e = std::getenv("STMG_CSUB_MAXDOFS")) maxdofs = std::atoll(e);
+  for (int l = 1; l < nl; ++l)
+    if (c->levels[l].view.size() <= maxdofs) {
+      a = l;
+      break;
+    }
+  if (a < 0) return;
+  int depth = 3;
+  if (const char* e = std::getenv("STMG_CSUB_DEPTH")) depth = std::atoi(e);
+  int b = a - 1;
+  const int stop = (c->tail_table && c->tail_start > 0) ? c->tail_start : nl - 1;
+  while (b + 1 < stop && b + 1 - a < depth && c->levels[b + 1].spec.coarsen == 2 &&
+         c->levels[b + 1].F.base && c->levels[b + 2].F.base)
+    ++b;
+  if (b < a || b + 1 >= nl) return;
+  std::vector<stmg::CsubSpec> spec(b + 2 - a);
+  for (int l = a; l <= b + 1; ++l) {
+    Level& L = c->levels[l];
+    stmg::CsubSpec& q = spec[l - a];
+    q.view = L.view;
+    q.n1c = (l + 1 < nl) ? c->levels[l + 1].spec.n1() : L.spec.n1();
+    q.F = L.F.base;
+    q.U0 = L.U[0].base;
+    q.U1 = L.U[1].base;
+  }
+  int lanes = 64;
+  if (const char* e = std::getenv("STMG_CSUB_LANES")) lanes = std::atoi(e);
+  CK(stmg::build_csub(spec.data(), int(spec.size()), lanes, &c->csub));
+  if (const char* e = std::getenv("STMG_CSUB_THREADS")) c->csub.threads = std::atoi(e);
+  c->csub_a = a;
+  c->csub_b = b;
+}
+
 // ---- coarse operator ------------------------------------------------------
 // The tail (levels >= tail_start, V(1,1), zero initial guess) is a fixed
 // linear map F -> U of the tail's first level.  When that level has at most
@@ -709,17 +775,13 @@ void ensure_cop(stmg_ctx* c, double omega) {
   if (!c->use_cop || !c->tail_table || c->cop.count(omega)) return;
   const i64 n = cop_size(c);
   if (n <= 0 || n > kCopMax) return;
-  Level& T = c->levels[c->tail_start];
   double* B = nullptr;
   CK(cudaMalloc(&B, size_t(n * n) * sizeof(double)));
-  const double one = 1.0;
-  for (i64 i = 0; i < n; ++i) {
-    CK(cudaMemsetAsync(T.F.base, 0, size_t(n) * sizeof(double), c->stream));
-    CK(cudaMemcpyAsync(T.F.base + i, &one, sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    launch_tail_kernel(c, omega);
-    CK(cudaMemcpy2DAsync(B + i, size_t(n) * sizeof(double), T.U[0].base, sizeof(double),
-                         sizeof(double), size_t(n), cudaMemcpyDeviceToDevice, c->stream));
-  }
+  // one launch: CTA i runs the tail kernel on e_i and writes column i
+  CK(stmg::launch_tail(c->dim, c->p_t + 1, c->tail_table, c->tail_host,
+                       int(c->levels.size()) - c->tail_start, omega, c->tail_smem, c->stream, B,
+                       n));
+  count(c);
   CK(cudaStreamSynchronize(c->stream));
   c->cop[omega] = B;
 }
@@ -756,6 +818,18 @@ void spectral_cycle(stmg_ctx* c, int level, bool zero_guess, const stmg_cycle_co
                     bool want_resid, i64* np) {
   if (cfg.block_solver == STMG_BLOCK_VCYCLE) {
     inexact_cycle(c, level, zero_guess, cfg, want_resid, np);
+    return;
+  }
+  if (zero_guess && !want_resid && level == c->csub_a && v11_exact(cfg)) {
+    // levels a..b fused: down pass, the levels below b, up pass
+    CK(stmg::launch_csub(c->csub, false, cfg.omega_t, c->stream));
+    count(c);
+    const int nb = c->csub_b + 1;
+    if (c->tail_table && nb == c->tail_start) run_tail(c, cfg.omega_t);
+    else spectral_cycle(c, nb, true, cfg, false, nullptr);
+    CK(stmg::launch_csub(c->csub, true, cfg.omega_t, c->stream));
+    count(c);
+    for (int l = c->csub_a; l <= c->csub_b; ++l) c->cur[l] = 0;
     return;
   }
   Level& L = c->levels[level];
@@ -1391,6 +1465,7 @@ void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config
   } else {
     ensure_spectral(c, 0);
     ensure_tail(c);
+    ensure_csub(c);
     if (v11_exact(cfg)) ensure_cop(c, cfg.omega_t);
     ensure_svc(c, cfg);
     c->cur[0] = 0;
@@ -1975,6 +2050,24 @@ void run_sharded_fused(stmg_ctx* c, const stmg_cycle_config& cfg, double eps, in
   }
 }
 
+// Full sine transform of one shard's finest slabs (the kernels dst_all uses,
+// so sharded iterates stay bitwise those of one shard).
+void shard_dst(stmg_ctx* c, const stmg::LevelView& v, const double* in, double* out) {
+  const void* tw = c->levels[0].d_twiddle;
+  if (c->dim == 2) {
+    const cudaError_t e = stmg::launch_dst2d(v, in, out, false, 1.0, tw, c->stream);
+    if (e != cudaErrorNotSupported) {
+      CK(e);
+      count(c);
+      return;
+    }
+  }
+  for (int a = 0; a < c->dim; ++a) {
+    CK(stmg::launch_dst_axis(v, a, a == 0 ? in : out, out, false, 1.0, tw, c->stream));
+    count(c);
+  }
+}
+
 // Sharded solve: f, u are this process's time slabs (virtual shards: the whole
 // vectors, split here).
 void solve_sharded(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config& cfg,
@@ -2014,11 +2107,7 @@ void solve_sharded(stmg_ctx* c, const double* f, double* u, const stmg_cycle_con
   CK(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   for (Shard& sh : ss.local) {
     ShardLevel& L = sh.lv[0];
-    for (int a = 0; a < c->dim; ++a) {
-      CK(stmg::launch_dst_axis(L.view, a, a == 0 ? f + part(sh) : L.F.base, L.F.base, false, 1.0,
-                               c->levels[0].d_twiddle, c->stream));
-      count(c);
-    }
+    shard_dst(c, L.view, f + part(sh), L.F.base);
     sh.cur[0] = 0;
   }
   CK(cudaStreamSynchronize(c->stream));
@@ -2026,11 +2115,7 @@ void solve_sharded(stmg_ctx* c, const double* f, double* u, const stmg_cycle_con
   for (Shard& sh : ss.local) {
     ShardLevel& L = sh.lv[0];
     if (u_nonzero) {
-      for (int a = 0; a < c->dim; ++a) {
-        CK(stmg::launch_dst_axis(L.view, a, a == 0 ? u + part(sh) : L.U[0].base, L.U[0].base,
-                                 false, 1.0, c->levels[0].d_twiddle, c->stream));
-        count(c);
-      }
+      shard_dst(c, L.view, u + part(sh), L.U[0].base);
     } else {
       CK(cudaMemsetAsync(L.U[0].base, 0, size_t(nloc0) * sizeof(double), c->stream));
     }
@@ -2116,11 +2201,7 @@ void solve_sharded(stmg_ctx* c, const double* f, double* u, const stmg_cycle_con
   }
   for (Shard& sh : ss.local) {
     ShardLevel& L = sh.lv[0];
-    for (int a = 0; a < c->dim; ++a) {
-      CK(stmg::launch_dst_axis(L.view, a, a == 0 ? L.U[sh.cur[0]].base : u + part(sh),
-                               u + part(sh), false, 1.0, c->levels[0].d_twiddle, c->stream));
-      count(c);
-    }
+    shard_dst(c, L.view, L.U[sh.cur[0]].base, u + part(sh));
   }
   CK(cudaEventRecord(c->ev_solve[1], c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -2210,6 +2291,7 @@ int stmg_create(const stmg_hierarchy_params* p, stmg_ctx** out) {
     if (const char* e = std::getenv("STMG_DEVICE_LOOP")) c->use_device_loop = std::atoi(e) != 0;
     if (const char* e = std::getenv("STMG_FUSED")) c->use_fused = std::atoi(e) != 0;
     if (const char* e = std::getenv("STMG_COARSE_OP")) c->use_cop = std::atoi(e) != 0;
+    if (const char* e = std::getenv("STMG_CSUB")) c->use_csub = std::atoi(e) != 0;
     CK(cudaMallocHost(&c->h_flag, sizeof(int)));
     CK(cudaMallocHost(&c->h_iter, sizeof(int)));
     CK(cudaEventCreate(&c->ev_solve[0]));
@@ -2252,6 +2334,7 @@ int stmg_destroy(stmg_ctx* c) {
     c->svc_pool.release();
     for (auto& kv : c->space_tab) cudaFree(kv.second);
     for (auto& kv : c->cop) cudaFree(kv.second);
+    stmg::free_csub(&c->csub);
     c->user_f.release();
     c->user_u.release();
     for (int s = 0; s < stmg_ctx::kSets; ++s) {
@@ -2536,6 +2619,7 @@ int stmg_mg_cycle(stmg_ctx* c, int level, double* u, const double* f,
     }
     ensure_spectral(c, 0);
     ensure_tail(c);
+    ensure_csub(c);
     if (v11_exact(*cfg)) ensure_cop(c, cfg->omega_t);
     c->cur[level] = 0;
     dst_all(c, L, f, L.F.base);

@@ -24,6 +24,8 @@
 #include <atomic>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "stmg_modal.cuh"
 
 namespace stmg {
@@ -1544,10 +1546,14 @@ struct TailParams {
 
 constexpr int kTailThreads = 512;  // 128 registers per thread: no spills
 
+// cop != nullptr: coarse-operator build, one CTA per column i = blockIdx.x:
+// the tail runs on the unit vector e_i (instead of the first level's F) and
+// its result is column i of the n x n row-major matrix cop.
 template <int DIM, int NL>
 __global__ void __launch_bounds__(kTailThreads) k_tail(const TailLevel<NL>* __restrict__ lv,
                                                const int nlev, const double omega,
-                                               const __grid_constant__ TailParams<NL> P) {
+                                               const __grid_constant__ TailParams<NL> P,
+                                               double* __restrict__ cop) {
 #ifdef STMG_TAIL_STAMPS
   unsigned long long ts[32];
   int nts = 0;
@@ -1603,7 +1609,9 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(const TailLevel<NL>* __re
   TAIL_STAMP();
   pdl_wait();  // the tables above are constants; the rhs is the previous kernel's output
   TAIL_STAMP();
-  {  // stage the first level's rhs
+  if (cop) {  // unit rhs e_i
+    for (int i = threadIdx.x; i < sz0; i += T) smem[i] = (i == int(blockIdx.x)) ? 1.0 : 0.0;
+  } else {  // stage the first level's rhs
     const double* g = lv[0].F;
     for (int i = threadIdx.x; i < sz0; i += T) smem[i] = g[i];
   }
@@ -1660,7 +1668,9 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(const TailLevel<NL>* __re
     __syncthreads();
     TAIL_STAMP();
   }
-  {  // hand the first level's iterate back
+  if (cop) {  // column blockIdx.x of the coarse operator
+    for (int i = threadIdx.x; i < sz0; i += T) cop[i64(i) * sz0 + blockIdx.x] = smem[sz0 + i];
+  } else {  // hand the first level's iterate back
     double* g = lv[0].U0;
     for (int i = threadIdx.x; i < sz0; i += T) g[i] = smem[sz0 + i];
   }
@@ -1673,6 +1683,155 @@ __global__ void __launch_bounds__(kTailThreads) k_tail(const TailLevel<NL>* __re
     printf("\n");
   }
 #endif
+}
+
+// Fused coarse levels: the V(1,1) down pass of levels a..b (zero initial
+// guess, mg.cpp:106-119) and, after the tail / coarser levels, the up pass
+// b..a (mg.cpp:121-131), each in ONE launch.  In the sine basis full
+// coarsening only couples the 2^DIM modes of an alias group, so the modes of
+// levels a..b split into independent trees: a tree is rooted at an alias
+// group of level r (r = b, or a "middle" group of a level r < b, whose modes
+// restrict to zero) and holds, one level finer, the groups whose coarse modes
+// are the root's member modes, and so on down to level a.  Every step of the
+// cycle on these levels -- smoothing, residual, restriction, prolongation --
+// stays inside one tree, so a CTA runs whole trees level after level with
+// __syncthreads between the levels instead of a kernel boundary per level.
+// The per-mode work is down_body / up_body of the per-level kernels on the
+// same global buffers (the same arithmetic and alias-group shuffle order, so
+// the results are bitwise those of the per-level path).  Trees of one root
+// level are packed `count` per CTA.
+constexpr int kCsubMaxLevels = 8;  // levels a..b+1
+
+template <int NL>
+struct CsubLevel {
+  TM<NL> t;
+  SP s;
+  i64 n_t;
+  i64 n1c;
+  double* F;
+  double* U0;
+  double* U1;
+};
+
+template <int NL>
+struct CsubParams {
+  CsubLevel<NL> lv[kCsubMaxLevels];  // index 0 = level a
+  int nb;                            // index of level b (b - a)
+  double omega;
+};
+
+// Global lane (alias group << DIM | member) at table level l of local lane
+// `lane` of the tree rooted at group `root` of table level r.  Lane bits
+// [DIM (m - l), DIM (m - l + 1)) select the member at level m; a member that
+// does not exist (the mirror of a middle index) kills its subtree, whose
+// lanes get an out-of-range group (make_member: ok = false, nothing stored).
+template <int DIM, int NL>
+__device__ __forceinline__ i64 csub_lane(const CsubParams<NL>& P, int r, unsigned root, int l,
+                                         int lane) {
+  int ia[DIM];
+  {
+    const unsigned G = unsigned(P.lv[r].s.G);
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      ia[a] = int(root % G);
+      root /= G;
+    }
+  }
+  bool dead = false;
+  for (int m = r; m > l; --m) {
+    const int beta = (lane >> (DIM * (m - l))) & ((1 << DIM) - 1);
+    const int Gm = P.lv[m].s.G;
+    const int n1m = int(P.lv[m].s.n1);
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      const bool mid = ia[a] >= Gm - 1;
+      const int bit = (beta >> a) & 1;
+      if (bit && mid) dead = true;
+      ia[a] = (bit && !mid) ? n1m - 1 - ia[a] : ia[a];
+    }
+  }
+  const i64 Gl = P.lv[l].s.G;
+  i64 gg = 0, mul = 1;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    gg += ia[a] * mul;
+    mul *= Gl;
+  }
+  if (dead) gg = ipow(Gl, DIM);
+  return (gg << DIM) | (lane & ((1 << DIM) - 1));
+}
+
+// Chunk of time steps per work item so that `lanes` lanes fill the block.
+__device__ __forceinline__ int csub_chunk(int lanes, int nt, int T) {
+  int C = 2;
+  while (C < nt && lanes * ((nt + C - 1) / C) > T) C *= 2;
+  return C;
+}
+
+struct CsubCta {
+  int root;    // table level of the trees' roots
+  int first;   // first tree (index into the root-group array)
+  int count;   // trees in this CTA
+};
+
+template <int DIM, int NL>
+__global__ void __launch_bounds__(256) k_csub_down(const CsubCta* __restrict__ ctas,
+                                                   const unsigned* __restrict__ roots,
+                                                   const __grid_constant__ CsubParams<NL> P) {
+  const CsubCta cta = ctas[blockIdx.x];
+  const int T = blockDim.x;
+  pdl_wait();  // level a's rhs is the previous kernel's output
+  for (int l = 0; l <= cta.root; ++l) {
+    const CsubLevel<NL>& A = P.lv[l];
+    const CsubLevel<NL>& B = P.lv[l + 1];
+    const int per = 1 << (DIM * (cta.root - l + 1));
+    const int lanes = per * cta.count;
+    const int nt = int(A.n_t);
+    const int C = csub_chunk(lanes, nt, T);
+    const int items = lanes * ((nt + C - 1) / C);
+    const int rounded = (items + T - 1) / T * T;
+    for (int it = threadIdx.x; it < rounded; it += T) {
+      const int lane = it % lanes, n0 = (it / lanes) * C;
+      if (n0 >= nt) continue;  // whole alias groups skip together
+      const i64 tid = csub_lane<DIM, NL>(P, cta.root, roots[cta.first + lane / per], l, lane % per);
+      const int nend = min(n0 + C, nt);
+      if (l == 0)
+        down_body<DIM, NL, true, 2, false>(tid, n0, nend, A.F, A.U1, A.U1, B.F, A.t, A.s, A.n1c,
+                                           P.omega, n0 > 0, n0 - 1 > 0);
+      else
+        down_body<DIM, NL, true, 2, true>(tid, n0, nend, A.F, A.U1, A.U1, B.F, A.t, A.s, A.n1c,
+                                          P.omega, n0 > 0, n0 - 1 > 0);
+    }
+    __syncthreads();
+  }
+  pdl_trigger();
+}
+
+template <int DIM, int NL>
+__global__ void __launch_bounds__(256) k_csub_up(const CsubCta* __restrict__ ctas,
+                                                 const unsigned* __restrict__ roots,
+                                                 const __grid_constant__ CsubParams<NL> P) {
+  const CsubCta cta = ctas[blockIdx.x];
+  const int T = blockDim.x;
+  pdl_wait();  // the correction of level b + 1 is the previous kernel's output
+  for (int l = cta.root; l >= 0; --l) {
+    const CsubLevel<NL>& A = P.lv[l];
+    const CsubLevel<NL>& B = P.lv[l + 1];
+    const int per = 1 << (DIM * (cta.root - l + 1));
+    const int lanes = per * cta.count;
+    const int nt = int(A.n_t);
+    const int C = csub_chunk(lanes, nt, T);
+    const int items = lanes * ((nt + C - 1) / C);
+    for (int it = threadIdx.x; it < items; it += T) {
+      const int lane = it % lanes, n0 = (it / lanes) * C;
+      const i64 tid = csub_lane<DIM, NL>(P, cta.root, roots[cta.first + lane / per], l, lane % per);
+      const int nend = min(n0 + C, nt);
+      up_body<DIM, NL, 2, false, true>(tid, n0, nend, B.U0, A.U1, A.F, A.U0, A.t, A.s, A.n1c,
+                                       P.omega, n0 > 0, n0 - 1 > 0);
+    }
+    __syncthreads();
+  }
+  pdl_trigger();
 }
 
 // Plain damped block-Jacobi sweep per mode (ping-pong: u_out != u_in).
@@ -2747,6 +2906,254 @@ __global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK, (LOG2N >= 4 ? STMG_DST
   }
 }
 
+// ---- one-pass 2D DST-I of whole slabs (thread-block cluster + DSMEM) -------
+// One cluster of CL CTAs transforms one n1 x n1 slab (one time step and DG
+// component) along both axes with one HBM read and one HBM write (16 B per
+// dof instead of 32 for the per-axis passes):
+//   1. CTA q loads rows [q R, q R + R) (contiguous: one TMA bulk copy);
+//   2. x pass: R/2 row pairs -> R/2 half-length FFTs (the k_dst_lines
+//      algorithm); output column j goes straight into the shared memory of
+//      the CTA that owns column block j / R (DSMEM stores: the transpose of
+//      the slab happens on the cluster, not through HBM);
+//   3. y pass: R/2 column pairs of the CTA's own block; output rows go to
+//      global memory (R contiguous doubles per row).
+// One shared region per CTA holds, in turn, the rows, the FFT buffers and the
+// column block: every phase first gathers what it needs into registers, so
+// the region is reused (35 KB per CTA instead of 68: twice the resident CTAs),
+// and radix-8 passes with 2x the threads per FFT double the warps per CTA.
+// radix-16 passes, 8 threads per FFT, >= 4 CTAs per SM: the fastest of
+// {radix 8, 16} x {3, 4 CTAs/SM} on C2 (84 vs 106 us per 2D transform for the
+// per-axis passes; profiles/r02_dst2d_ab.txt).  For 255-node axes the
+// 16-CTA clusters lose to the per-axis passes (10.6 vs 9.5 ms on C3), so the
+// one-pass kernel is used for 127-node slabs unless STMG_DST2D=2.
+#ifndef STMG_DST2D_LOG2V
+#define STMG_DST2D_LOG2V 4
+#endif
+template <int LOG2N, int R>
+struct DST2Shape {
+  static constexpr int N = 1 << LOG2N;
+  static constexpr int n1 = N - 1;
+  static constexpr int CL = N / R;            // CTAs per slab (cluster size)
+  static constexpr int LOG2V = STMG_DST2D_LOG2V;  // values per thread and pass
+  static constexpr int TS = N >> LOG2V;       // threads per FFT
+  static constexpr int F = R / 2;             // FFTs (line pairs) per pass
+  static constexpr int BLOCK = TS * F;
+  static constexpr int BUF = N + N / 16 + 1;  // padded FFT buffer (double2)
+  static constexpr int KB = (N / 2 + TS - 1) / TS;
+  static constexpr int H = N / 2;
+  static constexpr int PRE = (F * H + BLOCK - 1) / BLOCK;   // pre-processing items per thread
+  static constexpr int OUT = (F * n1 + BLOCK - 1) / BLOCK;  // x-pass outputs per thread
+  static constexpr int ROWS = R * n1 + 2;                    // rows (+ alignment shift)
+  static constexpr int FFTB = 2 * F * BUF;                   // FFT buffers, in doubles
+  static constexpr int REGION = ROWS > FFTB ? ROWS : FFTB;
+  static constexpr size_t smem = size_t(REGION) * sizeof(double);
+  static_assert(TS <= 32 && 32 % TS == 0, "FFT teams stay inside a warp");
+  static_assert(R % 2 == 0 && N % R == 0, "row blocks tile the slab");
+};
+
+__host__ __device__ constexpr int dst2_radix(int m, int lv, int p) {
+  return (m - lv * p) >= lv ? (1 << lv) : (1 << (m - lv * p));
+}
+
+template <int LOG2N, int LOG2V, int P, int NS>
+__device__ __forceinline__ void dst2_passes(double2* X, const int tt,
+                                            const double2* __restrict__ tw) {
+  constexpr int NP = (LOG2N + LOG2V - 1) / LOG2V;
+  if constexpr (P < NP) {
+    constexpr int Rx = dst2_radix(LOG2N, LOG2V, P);
+    stockham_pass<(1 << LOG2N), (1 << (LOG2N - LOG2V)), Rx, NS>(X, tt, tw);
+    dst2_passes<LOG2N, LOG2V, P + 1, NS * Rx>(X, tt, tw);
+  }
+}
+
+// Pre-processing of one pair of lines into its FFT buffer X (k_dst_lines):
+// X_j = sin(j pi/N)(z_j + z_{N-j}) + (z_j - z_{N-j})/2 with z_j = (a, b)_{j-1}.
+template <int N>
+__device__ __forceinline__ void dst2_pre(double2* X, int jj, double2 lo, double2 hi,
+                                         const double2* __restrict__ tw) {
+  constexpr int H = N / 2;
+  const int j = jj + 1;
+  const double sj = -__ldg(tw + j).y;  // sin(j pi / N)
+  const double2 sum = make_double2(lo.x + hi.x, lo.y + hi.y);
+  const double2 dif = make_double2(0.5 * (lo.x - hi.x), 0.5 * (lo.y - hi.y));
+  X[dst_pad(j)] = make_double2(sj * sum.x + dif.x, sj * sum.y + dif.y);
+  if (j != H) X[dst_pad(N - j)] = make_double2(sj * sum.x - dif.x, sj * sum.y - dif.y);
+}
+
+// FFT + post-processing of the team's buffer: afterwards X[dst_pad(j + 1)]
+// holds output j (j < n1) of both lines of the pair.
+template <int LOG2N, int LOG2V, int TS, int KB>
+__device__ __forceinline__ void dst2_fft_post(double2* X, int tt, const double2* __restrict__ tw) {
+  constexpr int N = 1 << LOG2N;
+  dst2_passes<LOG2N, LOG2V, 0, 1>(X, tt, tw);
+  double2 Rv[KB], Iv[KB];
+  double2 run = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int q = 0; q < KB; ++q) {
+    const int k = tt * KB + q;
+    double2 Rk = make_double2(0.0, 0.0), I = make_double2(0.0, 0.0);
+    if (k < N / 2) {
+      const double2 Y1 = X[dst_pad(k)], Y2 = X[dst_pad((N - k) & (N - 1))];
+      Rk = make_double2(0.5 * (Y1.x + Y2.x), 0.5 * (Y1.y + Y2.y));
+      I = make_double2(0.5 * (Y2.y - Y1.y), 0.5 * (Y1.x - Y2.x));
+      if (k == 0) Rk = make_double2(0.5 * Rk.x, 0.5 * Rk.y);
+    }
+    run = make_double2(run.x + Rk.x, run.y + Rk.y);
+    Rv[q] = run;
+    Iv[q] = I;
+  }
+  double2 inc = run;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < TS; d <<= 1) {
+    const double ux = __shfl_up_sync(0xffffffffu, inc.x, d, TS);
+    const double uy = __shfl_up_sync(0xffffffffu, inc.y, d, TS);
+    if ((lane % TS) >= d) {
+      inc.x += ux;
+      inc.y += uy;
+    }
+  }
+  const double2 off = make_double2(inc.x - run.x, inc.y - run.y);
+  __syncwarp();  // every Y read of the team is done
+#pragma unroll
+  for (int q = 0; q < KB; ++q) {
+    const int k = tt * KB + q;
+    if (k >= N / 2) continue;
+    if (k >= 1) X[dst_pad(2 * k)] = Iv[q];
+    X[dst_pad(2 * k + 1)] = make_double2(off.x + Rv[q].x, off.y + Rv[q].y);
+  }
+}
+
+#ifndef STMG_DST2D_MINB
+#define STMG_DST2D_MINB 4
+#endif
+template <int LOG2N, int R>
+__global__ void __launch_bounds__(DST2Shape<LOG2N, R>::BLOCK, STMG_DST2D_MINB) k_dst2d(
+    const double* __restrict__ in, double* __restrict__ out, const i64 total, const double scale,
+    const double alpha, const int accumulate, const double2* __restrict__ tw) {
+  using S = DST2Shape<LOG2N, R>;
+  constexpr int N = S::N, n1 = S::n1, F = S::F, TS = S::TS, BUF = S::BUF, H = S::H;
+  constexpr int BLK = S::BLOCK;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ double dsm[];  // the region: rows / FFT buffers / column block
+  __shared__ alignas(8) unsigned long long bar;
+  double2* Xb = reinterpret_cast<double2*>(dsm);
+  double* B = dsm;  // column block [n1 rows][R columns]
+  const int q = int(cluster.block_rank());
+  const i64 slab = i64(blockIdx.x / S::CL) * n1 * n1;
+  const int r0 = q * R;            // first row (x pass) / column (y pass)
+  const int nr = min(R, n1 - r0);  // rows / columns of this CTA
+  const int team = threadIdx.x / TS, tt = threadIdx.x % TS;
+  double2* X = Xb + team * BUF;
+
+  // 1. rows [r0, r0 + nr), one TMA bulk copy from the 16-byte aligned-down
+  // start (n1^2 is odd: every other slab starts at 8 mod 16); plain loads
+  // where the rounded copy would read past the vector's end
+  const double* src = in + slab + i64(r0) * n1;
+  const int cnt = nr * n1;
+  const int mis = int((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+  double* A = dsm + mis;
+  const unsigned bytes = unsigned(((cnt + mis) * 8 + 15) & ~15);
+  const bool bulk = (src - mis) + bytes / 8 <= in + total;
+  const unsigned bar_s = static_cast<unsigned>(__cvta_generic_to_shared(&bar));
+  if (bulk && threadIdx.x == 0) {
+    mbar_init(bar_s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    mbar_expect(bar_s, bytes);
+    bulk_g2s(static_cast<unsigned>(__cvta_generic_to_shared(dsm)), src - mis, bytes, bar_s);
+  }
+  if (!bulk) {
+#pragma unroll 8
+    for (int i = threadIdx.x; i < cnt; i += BLK) A[i] = __ldcs(src + i);
+  }
+  __syncthreads();
+  if (bulk) mbar_wait(bar_s, 0);
+  if (nr < R) {
+    for (int i = cnt + threadIdx.x; i < R * n1; i += BLK) A[i] = 0.0;
+    __syncthreads();
+  }
+  // 2. x pass: pair f = local rows 2f, 2f+1; inputs to registers, then the
+  // region becomes the FFT buffers
+  double2 lo[S::PRE], hi[S::PRE];
+#pragma unroll
+  for (int i = 0; i < S::PRE; ++i) {
+    const int e = threadIdx.x + i * BLK;
+    const int f = e / H, jj = e - f * H;
+    if (e < F * H) {
+      const double* a = A + (2 * f) * n1;
+      lo[i] = make_double2(a[jj], a[n1 + jj]);
+      hi[i] = make_double2(a[N - 2 - jj], a[n1 + N - 2 - jj]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < F) Xb[threadIdx.x * BUF + dst_pad(0)] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < S::PRE; ++i) {
+    const int e = threadIdx.x + i * BLK;
+    const int f = e / H, jj = e - f * H;
+    if (e < F * H) dst2_pre<N>(Xb + f * BUF, jj, lo[i], hi[i], tw);
+  }
+  __syncthreads();
+  dst2_fft_post<LOG2N, S::LOG2V, TS, S::KB>(X, tt, tw);
+  __syncthreads();
+  double2 res[S::OUT];
+#pragma unroll
+  for (int i = 0; i < S::OUT; ++i) {
+    const int e = threadIdx.x + i * BLK;
+    const int f = e / n1, j = e - f * n1;
+    if (e < F * n1) res[i] = Xb[f * BUF + dst_pad(j + 1)];
+  }
+  cluster.sync();  // every CTA has read its FFT buffers: regions take columns
+  // column j of rows (r0 + 2f, r0 + 2f + 1) -> CTA j / R, block [row][j % R]
+#pragma unroll
+  for (int i = 0; i < S::OUT; ++i) {
+    const int e = threadIdx.x + i * BLK;
+    const int f = e / n1, j = e - f * n1;
+    const int row = r0 + 2 * f;
+    if (e >= F * n1 || row >= n1) continue;
+    double* dst = cluster.map_shared_rank(B, j / R);
+    const int c = j % R;
+    dst[row * R + c] = res[i].x * scale;
+    if (row + 1 < n1) dst[(row + 1) * R + c] = res[i].y * scale;
+  }
+  if (nr < R)  // columns past n1 of the last block: zero (line b of its last pair)
+    for (int i = threadIdx.x; i < n1 * (R - nr); i += BLK)
+      B[(i / (R - nr)) * R + nr + i % (R - nr)] = 0.0;
+  cluster.sync();  // the column block is complete
+  // 3. y pass: pair f = local columns 2f, 2f+1 (row N-1 never read: index <= N-2)
+#pragma unroll
+  for (int i = 0; i < S::PRE; ++i) {
+    const int e = threadIdx.x + i * BLK;
+    const int jj = e / F, f = e - jj * F;
+    if (e < F * H) {
+      lo[i] = *reinterpret_cast<const double2*>(B + jj * R + 2 * f);
+      hi[i] = *reinterpret_cast<const double2*>(B + (N - 2 - jj) * R + 2 * f);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < F) Xb[threadIdx.x * BUF + dst_pad(0)] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < S::PRE; ++i) {
+    const int e = threadIdx.x + i * BLK;
+    const int jj = e / F, f = e - jj * F;
+    if (e < F * H) dst2_pre<N>(Xb + f * BUF, jj, lo[i], hi[i], tw);
+  }
+  __syncthreads();
+  dst2_fft_post<LOG2N, S::LOG2V, TS, S::KB>(X, tt, tw);
+  __syncthreads();
+  // output rows j, columns r0 + t (t = 2f + parity): R contiguous doubles per row
+  for (int e = threadIdx.x; e < n1 * R; e += BLK) {
+    const int j = e / R, t = e - j * R;
+    if (t >= nr) continue;
+    const double2 Z = Xb[(t >> 1) * BUF + dst_pad(j + 1)];
+    const double v = ((t & 1) ? Z.y : Z.x) * scale;
+    double* o = out + slab + i64(j) * n1 + r0 + t;
+    if (accumulate) *o += alpha * v;
+    else __stcs(o, v);
+  }
+}
+
 // ================================================================ misc
 // ---- dense DST-I for n1 = 63 (3D C4 and every 63-node axis) --------------
 // For N = 64 the transform as a dense contraction on the FP64 tensor cores
@@ -3225,6 +3632,64 @@ cudaError_t launch_dst_axis(const LevelView& L, int axis, const double* in, doub
   return cudaGetLastError();
 }
 
+// One-pass 2D transform of every n1 x n1 slab (n1 = 127 or 255); returns
+// cudaErrorNotSupported for other shapes (the caller runs per-axis passes).
+cudaError_t launch_dst2d(const LevelView& L, const double* in, double* out, bool accumulate,
+                         double alpha, const void* twiddles, cudaStream_t st) {
+  if (L.sp.dim != 2) return cudaErrorNotSupported;
+  static const int mode = [] {  // 0 off, 1 127-node slabs, 2 also 255
+    const char* e = std::getenv("STMG_DST2D");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (mode == 0 || (mode == 1 && L.sp.n1 != 127)) return cudaErrorNotSupported;
+  const i64 n1 = L.sp.n1;
+  const i64 slabs = L.n_t * L.tc.nl;
+  if (slabs == 0) return cudaSuccess;
+  const double scale = std::sqrt(2.0 / double(n1 + 1));
+  const double2* tw = static_cast<const double2*>(twiddles);
+  static PerDevice attr127, attr255;
+  auto go = [&](auto kern, PerDevice& attr, int cl, int block, size_t smem, bool nonportable) {
+    if (attr.first_use()) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (nonportable) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(slabs * cl));
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(cl);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t le =
+        cudaLaunchKernelEx(&cfg, kern, in, out, slabs * n1 * n1, scale, alpha, accumulate ? 1 : 0, tw);
+    if (le != cudaSuccess && std::getenv("STMG_DEBUG_DST2D")) {
+      int ncl = -1;
+      cudaError_t oe = cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
+      std::fprintf(stderr, "dst2d launch: %s; cluster %d block %d smem %zu grid %u; max active "
+                   "clusters %d (%s)\n", cudaGetErrorString(le), cl, block, smem, cfg.gridDim.x,
+                   ncl, cudaGetErrorString(oe));
+    }
+    return le;
+  };
+  cudaError_t e;
+  if (n1 == 127) {
+    using SH = DST2Shape<7, 32>;
+    e = go(k_dst2d<7, 32>, attr127, SH::CL, SH::BLOCK, SH::smem, false);
+  } else if (n1 == 255) {
+    using SH = DST2Shape<8, 16>;
+    e = go(k_dst2d<8, 16>, attr255, SH::CL, SH::BLOCK, SH::smem, true);
+  } else {
+    return cudaErrorNotSupported;
+  }
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 cudaError_t init_kernel_tables() {
   // Sodd[j'][c] = S(2c+1, j'+1) (j' < 31), S(2c+1, 32) (j' = 31);
   // Seven[j'][c] = S(2c+2, j'+1) (j' < 31, c < 31), else 0; S(k, j) = sqrt(2/64) sin(pi k j / 64)
@@ -3389,7 +3854,8 @@ cudaError_t build_tail_table(const TailSpec* levels, int nlev, void** dev_table,
 }
 
 cudaError_t launch_tail(int dim, int nl, const void* dev_table, const void* host_table, int nlev,
-                        double omega, size_t smem_bytes, cudaStream_t st) {
+                        double omega, size_t smem_bytes, cudaStream_t st, double* cop,
+                        int64_t cop_n) {
   if (nlev > kTailMaxLevels) return cudaErrorInvalidValue;
   STMG_DISPATCH(dim, nl, {
     TailParams<NL> P;
@@ -3397,10 +3863,95 @@ cudaError_t launch_tail(int dim, int nl, const void* dev_table, const void* host
     for (int k = 0; k < nlev; ++k) P.t[k] = h[k].t;
     cudaFuncSetAttribute(k_tail<DIM, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(smem_bytes));
-    PDLK(k_tail<DIM, NL>, 1, kTailThreads, smem_bytes, st, 
-        static_cast<const TailLevel<NL>*>(dev_table), nlev, omega, P);
+    const unsigned grid = cop ? unsigned(cop_n) : 1u;
+    PDLK(k_tail<DIM, NL>, grid, kTailThreads, smem_bytes, st,
+         static_cast<const TailLevel<NL>*>(dev_table), nlev, omega, P, cop);
   });
   return cudaGetLastError();
+}
+
+template <int NL>
+cudaError_t build_csub_t(const CsubSpec* lv, int nlev, int lanes_target, CsubPlan* plan) {
+  if (nlev < 2 || nlev > kCsubMaxLevels) return cudaErrorInvalidValue;
+  CsubParams<NL> P{};
+  const int dim = lv[0].view.sp.dim;
+  for (int k = 0; k < nlev; ++k) {
+    P.lv[k].t = make_tm<NL>(lv[k].view.tc);
+    P.lv[k].s = make_sp(lv[k].view.sp);
+    P.lv[k].n_t = lv[k].view.n_t;
+    P.lv[k].n1c = lv[k].n1c;
+    P.lv[k].F = lv[k].F;
+    P.lv[k].U0 = lv[k].U0;
+    P.lv[k].U1 = lv[k].U1;
+  }
+  P.nb = nlev - 2;
+  // trees: every group of level b, and the middle groups of levels a..b-1
+  std::vector<CsubCta> ctas;
+  std::vector<unsigned> roots;
+  for (int r = P.nb; r >= 0; --r) {
+    const i64 G = P.lv[r].s.G;
+    const i64 ng = ipow(G, dim);
+    const int first = int(roots.size());
+    for (i64 g = 0; g < ng; ++g) {
+      bool mid = false;
+      i64 q = g;
+      for (int a = 0; a < dim; ++a, q /= G) mid |= (q % G) == G - 1;
+      if (r == P.nb || mid) roots.push_back(unsigned(g));
+    }
+    const int n = int(roots.size()) - first;
+    const int per = 1 << (dim * (r + 1));  // level-a lanes of one tree
+    const int k = std::max(1, lanes_target / per);
+    for (int i = 0; i < n; i += k) ctas.push_back(CsubCta{r, first + i, std::min(k, n - i)});
+  }
+  free_csub(plan);
+  plan->dim = dim;
+  plan->nl = NL;
+  plan->n_ctas = int(ctas.size());
+  plan->trees = int(roots.size());
+  cudaError_t e = cudaMalloc(&plan->ctas, ctas.size() * sizeof(CsubCta));
+  if (e == cudaSuccess) e = cudaMalloc(&plan->roots, roots.size() * sizeof(unsigned));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(plan->ctas, ctas.data(), ctas.size() * sizeof(CsubCta), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(plan->roots, roots.data(), roots.size() * sizeof(unsigned),
+                   cudaMemcpyHostToDevice);
+  plan->params = std::malloc(sizeof(P));
+  std::memcpy(plan->params, &P, sizeof(P));
+  return e;
+}
+
+cudaError_t build_csub(const CsubSpec* levels, int nlev, int lanes_target, CsubPlan* plan) {
+  switch (levels[0].view.tc.nl) {
+    case 1: return build_csub_t<1>(levels, nlev, lanes_target, plan);
+    case 2: return build_csub_t<2>(levels, nlev, lanes_target, plan);
+    case 3: return build_csub_t<3>(levels, nlev, lanes_target, plan);
+    case 4: return build_csub_t<4>(levels, nlev, lanes_target, plan);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_csub(const CsubPlan& plan, bool up, double omega, cudaStream_t st) {
+  if (!plan.params || plan.n_ctas <= 0) return cudaErrorInvalidValue;
+  STMG_DISPATCH(plan.dim, plan.nl, {
+    CsubParams<NL> P;
+    std::memcpy(&P, plan.params, sizeof(P));
+    P.omega = omega;
+    const CsubCta* c = static_cast<const CsubCta*>(plan.ctas);
+    const unsigned* r = static_cast<const unsigned*>(plan.roots);
+    if (up)
+      PDLK(k_csub_up<DIM, NL>, plan.n_ctas, plan.threads, 0, st, c, r, P);
+    else
+      PDLK(k_csub_down<DIM, NL>, plan.n_ctas, plan.threads, 0, st, c, r, P);
+  });
+  return cudaGetLastError();
+}
+
+void free_csub(CsubPlan* plan) {
+  if (plan->ctas) cudaFree(plan->ctas);
+  if (plan->roots) cudaFree(plan->roots);
+  std::free(plan->params);
+  plan->ctas = plan->roots = plan->params = nullptr;
+  plan->n_ctas = plan->trees = 0;
 }
 
 int64_t partial_count(const LevelView& L, int chunk, bool grouped) {

@@ -58,6 +58,11 @@ cudaError_t launch_fold_u0(const LevelView& L, double* f, const double* u0,
 cudaError_t launch_dst_axis(const LevelView& L, int axis, const double* in,
                             double* out, bool accumulate, double alpha,
                             const void* twiddles, cudaStream_t st);
+// Both axes of every slab of a 2D level in one pass (thread-block cluster per
+// slab); cudaErrorNotSupported when the shape has no one-pass kernel.
+cudaError_t launch_dst2d(const LevelView& L, const double* in, double* out,
+                         bool accumulate, double alpha, const void* twiddles,
+                         cudaStream_t st);
 // Constant tables of the kernels (dense DST-I matrix); once per process/device.
 cudaError_t init_kernel_tables();
 // Per-mode exact block solve in the sine basis, in place.
@@ -135,8 +140,33 @@ struct TailSpec {
 // host_table: malloc'd host copy (free with std::free).
 cudaError_t build_tail_table(const TailSpec* levels, int nlev, void** dev_table,
                              void** host_table);
+// cop != nullptr: build the coarse operator instead, cop_n CTAs, CTA i runs
+// the tail on e_i and writes column i of cop (row-major cop_n x cop_n).
 cudaError_t launch_tail(int dim, int nl, const void* dev_table, const void* host_table, int nlev,
-                        double omega, size_t smem_bytes, cudaStream_t st);
+                        double omega, size_t smem_bytes, cudaStream_t st,
+                        double* cop = nullptr, int64_t cop_n = 0);
+// ---- fused coarse levels (alias-group trees, one launch per pass) ----------
+// levels[0..nlev) = coarse levels a..b+1 of a V(1,1) cycle with zero initial
+// guess, all coarsened fully down to b + 1.  down: levels a..b (writes U1 and
+// the rhs F of a+1..b+1); up: levels b..a (reads U0 of b + 1, writes U0).
+struct CsubSpec {
+  LevelView view;
+  int64_t n1c = 0;
+  double* F = nullptr;
+  double* U0 = nullptr;
+  double* U1 = nullptr;
+};
+struct CsubPlan {
+  void* ctas = nullptr;    // device CsubCta[n_ctas]
+  void* roots = nullptr;   // device root group per tree
+  void* params = nullptr;  // host copy of the level table (malloc'd)
+  int n_ctas = 0, trees = 0, dim = 1, nl = 1, threads = 256;
+};
+// lanes_target: level-a lanes per CTA when packing small trees.
+cudaError_t build_csub(const CsubSpec* levels, int nlev, int lanes_target, CsubPlan* plan);
+cudaError_t launch_csub(const CsubPlan& plan, bool up, double omega, cudaStream_t st);
+void free_csub(CsubPlan* plan);
+
 // ---- inexact block solver: spatial V-cycle in the sine basis --------------
 // (SpatialVCycleSolver, smoother.cpp:8-78; kernels in stmg_spatial.cu.)  The
 // LevelView supplies n_t and the DG blocks of the space-time level; SvcArgs

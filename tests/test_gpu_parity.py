@@ -417,3 +417,19 @@ def test_history_buffer_regrowth(S, shards):
         assert rep.converged and rep.iterations == rep_o["iterations"]
         assert rel(np.array(rep.residual_history), np.array(rep_o["residual_history"])) < 1e-10
         assert rel(du.numpy(), u_o) < 1e-10
+
+
+@pytest.mark.parametrize("sl", [6, 7])
+def test_one_pass_2d_transform_matches_oracle(S, sl):
+    """127^2 and 255^2 slabs use the one-pass cluster DST (k_dst2d): the exact
+    block solve (forward + inverse 2D transforms) and the physical smoother
+    against the oracle, the accumulate mode, and in-place use."""
+    g, o = pair(S, 1, 2, sl, 2, 0.1, 1, 1)
+    n = o.levels[0].size
+    b = O.fill_uniform(n, 41, 0)
+    u = O.fill_uniform(n, 42, 0)
+    assert rel(g.block_solve(0, g.upload(b)).numpy(), o.block_solve(0, b)) < 1e-12
+    us = g.block_jacobi_step(0, g.upload(u), g.upload(b), 0.5, 2).numpy()
+    assert rel(us, o.smooth(0, u, b, 0.5, 2)) < 1e-11
+    fs = g.forward_substitution_solve(0, g.upload(b)).numpy()
+    assert rel(fs, o.forward_substitution(0, b)) < 1e-11

@@ -223,6 +223,26 @@ def test_schedule_switches_agree(cfg):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("cfg", [(1, 2, 6, 8), (2, 2, 6, 7), (1, 3, 4, 6), (1, 2, 7, 6)])
+@pytest.mark.parametrize("depth", ["1", "3"])
+def test_fused_coarse_trees_bitwise(cfg, depth):
+    """The alias-group-tree kernels for the coarse levels (STMG_CSUB=1,
+    k_csub_down/up) run the per-level kernels' arithmetic: bitwise equal
+    iterates and histories."""
+    from oracle import oracle as O
+    from paper_1411_0519_b200 import build
+    build.build()
+    p, dim, sl, tl = cfg
+    o = O.Hierarchy(p, dim, sl, tl)
+    f = O.make_inputs(o, 42, random_u0=(dim == 2))
+    r_ref, u_ref = _solve_with_env({"STMG_CSUB": "0"}, p, dim, sl, tl, f)
+    r_cs, u_cs = _solve_with_env({"STMG_CSUB": "1", "STMG_CSUB_DEPTH": depth}, p, dim, sl, tl, f)
+    assert r_cs.iterations == r_ref.iterations
+    assert r_cs.residual_history == r_ref.residual_history
+    assert np.array_equal(u_cs, u_ref)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("cyc", [(1, 1), (2, 2)])
 def test_virtual_shards_host_batch(cyc):
     """stmg_solve_host_batch on a 4-shard context (fused and general cycles):
