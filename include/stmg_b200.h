@@ -53,7 +53,7 @@ typedef struct stmg_ctx stmg_ctx;
 
 /* HierarchyParams (mg.hpp:49-58) + build_two_grid's mode (mg.hpp:81). */
 typedef struct {
-  int p_t;          /* DG degree in time, 0..3 on the GPU path */
+  int p_t;          /* DG degree in time, 0..10 (4..10: physical-path kernels) */
   int dim;          /* 1, 2 or 3 */
   int space_level;  /* finest space level L: n1 = 2^(L+1)-1 nodes per axis */
   int time_level;   /* finest n_t = 2^time_level */
@@ -148,6 +148,9 @@ int stmg_fill_uniform(stmg_ctx* ctx, double* dst_dev, int64_t n, uint64_t seed,
                       uint64_t stream, int64_t offset);
 /* f(0,k,:) += psi_k(0) * M_h u0 on the finest level (u0: n_x nodal values). */
 int stmg_fold_u0(stmg_ctx* ctx, double* f_dev, const double* u0_dev);
+/* fill_random (mg.cpp:168-173), reference-exact, on the HOST (no GPU needed):
+ * std::mt19937_64 gen(seed); dst[i] = (gen() >> 11) * 2^-53, i = 0..n-1. */
+int stmg_fill_random_host(double* dst_host, int64_t n, uint64_t seed);
 
 /* Reference defaults: CycleConfig (mg.hpp:66-71: nu1 = nu2 = 2, gamma = 1)
  * with SmootherConfig (smoother.hpp:15-24: omega_t = 1/2, exact blocks,

@@ -390,9 +390,145 @@ inline SolveReport solve(const STHierarchy& h, const BlockVector& f, BlockVector
   return out;
 }
 
-// mg.hpp:98 (counter-based generator of SURVEY.md 8(d), uniform [-1, 1))
-inline void fill_random(BlockVector& v, std::uint64_t seed, std::uint64_t stream = 0) {
+// mg.hpp:98 / mg.cpp:168-173, reference-exact: std::mt19937_64(seed),
+// v[i] = (gen() >> 11) * 2^-53 in [0, 1) over the flat BlockVector order
+// (generated on the host -- the stream is sequential -- then uploaded).
+inline void fill_random(BlockVector& v, std::uint64_t seed) {
+  std::vector<double> h(static_cast<size_t>(v.size()));
+  check(stmg_fill_random_host(h.data(), v.size(), seed));
+  v.from_host(h);
+}
+
+// The benchmarks' counter-based generator: uniform [-1, 1),
+// splitmix64 of (seed, stream, index), generated on the device.
+inline void fill_uniform(BlockVector& v, std::uint64_t seed, std::uint64_t stream = 0) {
   check(stmg_fill_uniform(v.ctx(), v.data(), v.size(), seed, stream, 0));
+}
+
+// ---- reference-signature overloads ---------------------------------------
+// fem_space.hpp:11-17 / fem_space.cpp (host only)
+struct SpaceGrid {
+  int dim = 1;
+  int level = 0;
+  double h = 0.5;
+  std::int64_t n_per_dim = 1;
+  std::int64_t n_nodes = 1;
+};
+inline SpaceGrid build_space_grid(int dim, int level) {
+  if (dim < 1 || dim > 3) throw std::invalid_argument("dim must be 1, 2 or 3");
+  if (level < 0) throw std::invalid_argument("level must be >= 0");
+  SpaceGrid g;
+  g.dim = dim;
+  g.level = level;
+  g.n_per_dim = (std::int64_t(1) << (level + 1)) - 1;
+  g.h = 1.0 / double(g.n_per_dim + 1);
+  g.n_nodes = 1;
+  for (int a = 0; a < dim; ++a) g.n_nodes *= g.n_per_dim;
+  return g;
+}
+
+// st_system.hpp:50-63: the exact block solver of a level (sine-basis direct
+// solve on the B200 path; there is no factorisation to cache).
+class BlockSolver {
+ public:
+  explicit BlockSolver(const STOperator& op) : op_(op) {}
+  // A x = b on every time step of a level vector (the reference solves one slice)
+  BlockVector solve(const BlockVector& b) const {
+    BlockVector x = BlockVector::for_level(op_);
+    check(stmg_block_solve(op_.ctx, op_.level, b.data(), x.data()));
+    return x;
+  }
+  const STOperator& op() const { return op_; }
+
+ private:
+  STOperator op_;
+};
+
+// smoother.hpp:60-63
+struct BlockSolveContext {
+  const BlockSolver* exact = nullptr;
+  const SpatialVCycleSolver* vcycle = nullptr;
+};
+
+// smoother.hpp:68-70: cfg.block_solver picks the solver (smoother.cpp:82-92);
+// the context must carry it.
+inline void block_jacobi_step(const STOperator& op, const BlockSolveContext& ctx, BlockVector& u,
+                              const BlockVector& f, const SmootherConfig& cfg) {
+  if (cfg.block_solver == BlockSolverKind::exact ? ctx.exact == nullptr : ctx.vcycle == nullptr)
+    throw std::invalid_argument("block_jacobi_step: the context lacks the configured block solver");
+  block_jacobi_step(op, u, f, cfg);
+}
+
+// st_system.hpp:70-72
+inline BlockVector forward_substitution_solve(const STOperator& op, const BlockSolver& block_lu,
+                                              const BlockVector& f) {
+  (void)block_lu;  // the level's direct solve is part of the context
+  return forward_substitution_solve(op, f);
+}
+
+namespace detail {
+// The hierarchy level a vector belongs to, from its shape (n_t halves every
+// level, so (n_t, n_x) is unique); grid_level >= 0 also checks the space level.
+inline STOperator level_of(const BlockVector& v, int grid_level = -1) {
+  int n = 0;
+  check(stmg_num_levels(v.ctx(), &n));
+  for (int l = 0; l < n; ++l) {
+    stmg_level_info li{};
+    check(stmg_get_level_info(v.ctx(), l, &li));
+    if (li.n_t == v.n_t() && li.n_x == v.n_x() && li.n_loc == v.n_loc() &&
+        (grid_level < 0 || li.space_level == grid_level))
+      return STOperator{v.ctx(), l};
+  }
+  throw std::invalid_argument("vector does not match a level of its hierarchy");
+}
+inline void check_transfer(const TimeTransfer& t, const BlockVector& v) {
+  if (std::int64_t(t.R1.size()) != v.n_loc() * v.n_loc() || t.R1.size() != t.R2.size())
+    throw std::invalid_argument("time transfer does not match the vector's DG degree");
+}
+}  // namespace detail
+
+// transfer.hpp:27-28
+inline BlockVector restrict_semi(const TimeTransfer& t, const BlockVector& fine) {
+  detail::check_transfer(t, fine);
+  if (fine.n_t() % 2 != 0) throw std::invalid_argument("restrict_semi requires an even step count");
+  return restrict_semi(detail::level_of(fine), fine);
+}
+inline BlockVector prolong_semi(const TimeTransfer& t, const BlockVector& coarse) {
+  detail::check_transfer(t, coarse);
+  // the fine level: twice the steps, same nodes
+  int n = 0;
+  check(stmg_num_levels(coarse.ctx(), &n));
+  for (int l = 0; l < n; ++l) {
+    stmg_level_info li{};
+    check(stmg_get_level_info(coarse.ctx(), l, &li));
+    if (li.n_t == 2 * coarse.n_t() && li.n_x == coarse.n_x() && li.n_loc == coarse.n_loc())
+      return prolong_semi(STOperator{coarse.ctx(), l}, coarse);
+  }
+  throw std::invalid_argument("vector does not match a level of its hierarchy");
+}
+// transfer.hpp:41-44
+inline BlockVector restrict_full(const TimeTransfer& t, const SpaceGrid& fine_grid,
+                                 const SpaceGrid& coarse_grid, const BlockVector& fine) {
+  detail::check_transfer(t, fine);
+  if (coarse_grid.level + 1 != fine_grid.level || fine.n_x() != fine_grid.n_nodes)
+    throw std::invalid_argument("restrict_full: grids do not match the vector");
+  return restrict_full(detail::level_of(fine, fine_grid.level), fine);
+}
+inline BlockVector prolong_full(const TimeTransfer& t, const SpaceGrid& coarse_grid,
+                                const SpaceGrid& fine_grid, const BlockVector& coarse) {
+  detail::check_transfer(t, coarse);
+  if (coarse_grid.level + 1 != fine_grid.level || coarse.n_x() != coarse_grid.n_nodes)
+    throw std::invalid_argument("prolong_full: grids do not match the vector");
+  int n = 0;
+  check(stmg_num_levels(coarse.ctx(), &n));
+  for (int l = 0; l < n; ++l) {
+    stmg_level_info li{};
+    check(stmg_get_level_info(coarse.ctx(), l, &li));
+    if (li.n_t == 2 * coarse.n_t() && li.space_level == fine_grid.level &&
+        li.n_loc == coarse.n_loc())
+      return prolong_full(STOperator{coarse.ctx(), l}, coarse);
+  }
+  throw std::invalid_argument("vector does not match a level of its hierarchy");
 }
 
 }  // namespace stmg

@@ -80,6 +80,7 @@ SIGNATURES = [
     ("stmg_host_free", C.c_int, [VP, VP]),
     ("stmg_synchronize", C.c_int, [VP]),
     ("stmg_fill_uniform", C.c_int, [VP, VP, C.c_int64, C.c_uint64, C.c_uint64, C.c_int64]),
+    ("stmg_fill_random_host", C.c_int, [VP, C.c_int64, C.c_uint64]),
     ("stmg_fold_u0", C.c_int, [VP, VP, VP]),
     ("stmg_apply", C.c_int, [VP, C.c_int, VP, VP]),
     ("stmg_residual", C.c_int, [VP, C.c_int, VP, VP, VP]),

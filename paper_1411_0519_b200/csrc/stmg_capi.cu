@@ -24,6 +24,7 @@
 #include <functional>
 #include <map>
 #include <memory>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -134,6 +135,9 @@ struct stmg_ctx {
   cudaStream_t stream = nullptr;
   std::vector<Level> levels;
   int p_t = 0, dim = 1;
+  // p_t > 3: the physical-path operators with a runtime DG size (the fused
+  // spectral kernels are compiled for p_t <= 3); every cycle runs there
+  bool hi_degree = false;
   // scratch
   DevBuf partials;       // norm partial sums of the spectral cycle (graph-resident)
   DevBuf partials_phys;  // per-step partials of stmg_norm
@@ -1124,6 +1128,18 @@ void check_cfg(const stmg_cycle_config* cfg) {
           "block_solver must be 'exact' or 'vcycle'");
   if (cfg->block_solver == STMG_BLOCK_VCYCLE)
     check_spatial(cfg->omega_x, cfg->nu1_x, cfg->nu2_x, cfg->gamma_x);
+}
+
+// The cycle configuration a context actually runs: p_t > 3 takes the
+// physical path (same iteration, reference call structure).
+stmg_cycle_config effective_cfg(const stmg_ctx* c, const stmg_cycle_config& cfg) {
+  stmg_cycle_config e = cfg;
+  if (c->hi_degree) {
+    require(cfg.block_solver == STMG_BLOCK_EXACT,
+            "spatial V-cycle block solves support p_t <= 3 on the B200 path");
+    e.path = STMG_PATH_PHYSICAL;
+  }
+  return e;
 }
 
 void ensure_hist(stmg_ctx* c, int n) {
@@ -2256,8 +2272,10 @@ int stmg_create(const stmg_hierarchy_params* p, stmg_ctx** out) {
     *out = nullptr;
     auto specs = stmg::build_ladder(p->p_t, p->dim, p->space_level, p->time_level, p->t_final,
                                     p->mu_star, p->policy, p->two_grid);
-    if (p->p_t + 1 > stmg::kMaxNL)
-      throw std::invalid_argument("p_t > 3 is not supported on the B200 path");
+    // (build_ladder already rejected p_t outside 0..kMaxTimeDegree = 10)
+    require(p->p_t + 1 <= stmg::kMaxNL, "p_t out of range");
+    require(p->p_t + 1 <= stmg::kFastNL || p->shards <= 1,
+            "time-slab sharding runs the spectral kernels: p_t <= 3");
     int ndev = 0;
     const cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess || ndev == 0)
@@ -2270,6 +2288,7 @@ int stmg_create(const stmg_hierarchy_params* p, stmg_ctx** out) {
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->p_t = p->p_t;
     c->dim = p->dim;
+    c->hi_degree = p->p_t + 1 > stmg::kFastNL;
     c->levels.resize(specs.size());
     for (size_t i = 0; i < specs.size(); ++i) {
       c->levels[i].spec = specs[i];
@@ -2479,6 +2498,14 @@ int stmg_fill_uniform(stmg_ctx* c, double* dst, int64_t n, uint64_t seed, uint64
   });
 }
 
+int stmg_fill_random_host(double* dst, int64_t n, uint64_t seed) {
+  return guard([&] {
+    require(n >= 0 && (n == 0 || dst), "null argument");
+    std::mt19937_64 gen(seed);  // mg.cpp:168-173
+    for (int64_t i = 0; i < n; ++i) dst[i] = double(gen() >> 11) * 0x1.0p-53;
+  });
+}
+
 int stmg_fold_u0(stmg_ctx* c, double* f, const double* u0) {
   return cguard(c, [&] {
     require(f && u0, "null vector");
@@ -2555,6 +2582,7 @@ int stmg_block_jacobi_step(stmg_ctx* c, int level, double* u, const double* f,
             "block_solver must be 'exact' or 'vcycle'");
     if (cfg->block_solver == STMG_BLOCK_VCYCLE) {
       check_spatial(cfg->omega_x, cfg->nu1_x, cfg->nu2_x, cfg->gamma_x);
+      require(!c->hi_degree, "spatial V-cycle block solves support p_t <= 3 on the B200 path");
       const Spatial sp = spatial_of(*cfg);
       smooth_phys(c, level, u, f, cfg->omega_t, cfg->nu, &sp);
     } else {
@@ -2570,6 +2598,7 @@ int stmg_spatial_vcycle(stmg_ctx* c, int level, const double* b, const double* x
     require(cfg != nullptr, "null smoother config");
     require(b && x, "null vector");
     check_spatial(cfg->omega_x, cfg->nu1_x, cfg->nu2_x, cfg->gamma_x);
+    require(!c->hi_degree, "spatial V-cycle block solves support p_t <= 3 on the B200 path");
     const Spatial sp = spatial_of(*cfg);
     const SvcBufs w = svc_bufs(c, L);
     dst_all(c, L, b, w.B[0]);
@@ -2613,6 +2642,8 @@ int stmg_mg_cycle(stmg_ctx* c, int level, double* u, const double* f,
     Level& L = lev(c, level);
     check_cfg(cfg);
     require(u && f, "null vector");
+    const stmg_cycle_config ecfg = effective_cfg(c, *cfg);
+    cfg = &ecfg;
     if (cfg->path == STMG_PATH_PHYSICAL) {
       phys_cycle(c, level, u, f, *cfg);
       return;
@@ -2634,8 +2665,9 @@ int stmg_solve(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config*
   return cguard(c, [&] {
     require(c != nullptr, "null context");
     check_cfg(cfg);
-    if (c->shards) solve_sharded(c, f, u, *cfg, eps, max_iter, history, history_cap, report);
-    else solve_impl(c, f, u, *cfg, eps, max_iter, history, history_cap, report);
+    const stmg_cycle_config ec = effective_cfg(c, *cfg);
+    if (c->shards) solve_sharded(c, f, u, ec, eps, max_iter, history, history_cap, report);
+    else solve_impl(c, f, u, ec, eps, max_iter, history, history_cap, report);
   });
 }
 
@@ -2646,6 +2678,8 @@ int stmg_solve_host(stmg_ctx* c, const double* f_host, double* u_host,
     require(c != nullptr, "null context");
     check_cfg(cfg);
     require(f_host && u_host, "null vector");
+    const stmg_cycle_config ecfg = effective_cfg(c, *cfg);
+    cfg = &ecfg;
     Level& L0 = c->levels[0];
     const i64 n = (c->shards && c->shards->nccl) ? L0.view.size() / c->shards->S : L0.view.size();
     ensure(c->user_f, n);
@@ -2687,6 +2721,8 @@ int stmg_solve_host_batch(stmg_ctx* c, int count, const double* const* f_host,
   return cguard(c, [&] {
     require(c != nullptr, "null context");
     check_cfg(cfg);
+    const stmg_cycle_config ecfg = effective_cfg(c, *cfg);
+    cfg = &ecfg;
     require(count >= 0, "count must be >= 0");
     if (count == 0) return;
     require(f_host != nullptr && u_host != nullptr, "null vector array");
@@ -2829,6 +2865,7 @@ int stmg_create_distributed(const stmg_hierarchy_params* p, int rank, int world,
     }
     std::unique_ptr<stmg_ctx, int (*)(stmg_ctx*)> hold(c, stmg_destroy);
     if (world > 1) {
+      require(!c->hi_degree, "time-slab sharding runs the spectral kernels: p_t <= 3");
       c->shards = std::make_unique<ShardSet>();
       c->shards->S = world;
       c->shards->nccl = true;

@@ -2584,6 +2584,272 @@ __global__ void k_fold_u0(double* __restrict__ f, const double* __restrict__ u0,
   for (int k = 0; k < NL; ++k) f[k * nx + r] += tc.psi0[k] * Mv;
 }
 
+// ================================================ high DG degree (p_t 4..10)
+// The reference accepts p_t <= kMaxTimeDegree = 10 (dg_time.hpp:10).  Degrees
+// above kFastNL - 1 run the physical-path operators below, with the number of
+// DG components a runtime value (per-thread NL x NL algebra in local memory):
+// correct, not tuned -- the fused spectral kernels are compiled for NL <= 4.
+constexpr int kHiNL = kMaxNL;
+
+// Dense NL x NL Gaussian elimination with partial pivoting, in place: A is
+// destroyed, b becomes the solution.
+__device__ __forceinline__ void hi_solve(int nl, double (&A)[kHiNL][kHiNL], double (&b)[kHiNL]) {
+  for (int c = 0; c < nl; ++c) {
+    int p = c;
+    for (int r = c + 1; r < nl; ++r)
+      if (fabs(A[r][c]) > fabs(A[p][c])) p = r;
+    if (p != c) {
+      for (int k = 0; k < nl; ++k) {
+        const double t = A[c][k];
+        A[c][k] = A[p][k];
+        A[p][k] = t;
+      }
+      const double t = b[c];
+      b[c] = b[p];
+      b[p] = t;
+    }
+    const double inv = 1.0 / A[c][c];
+    for (int r = c + 1; r < nl; ++r) {
+      const double f = A[r][c] * inv;
+      for (int k = c + 1; k < nl; ++k) A[r][k] -= f * A[c][k];
+      b[r] -= f * b[c];
+    }
+  }
+  for (int c = nl - 1; c >= 0; --c) {
+    double s = b[c];
+    for (int k = c + 1; k < nl; ++k) s -= A[c][k] * b[k];
+    b[c] = s / A[c][c];
+  }
+}
+
+template <int DIM>
+__device__ __forceinline__ void hi_block(const TimeConsts& tc, double Mj, double Kj,
+                                         double (&A)[kHiNL][kHiNL]) {
+  for (int i = 0; i < tc.nl; ++i)
+    for (int j = 0; j < tc.nl; ++j)
+      A[i][j] = Mj * tc.K[i * kMaxNL + j] + Kj * tc.M[i * kMaxNL + j];
+}
+
+// y = L u (or r = f - L u) at (node r, step n): st_system.cpp:25-33.
+template <int DIM>
+__global__ void __launch_bounds__(128) k_apply_hi(const double* __restrict__ u,
+                                                  const double* __restrict__ f,
+                                                  double* __restrict__ y, const TimeConsts tc,
+                                                  const i64 n1, const i64 nx, const double h,
+                                                  const i64 n_t, const int residual) {
+  const unsigned r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nx) return;
+  const int nl = tc.nl;
+  int c[3];
+  coords<DIM>(r, unsigned(n1), c);
+  for (i64 n = blockIdx.y; n < n_t; n += gridDim.y) {
+    double Mv[kHiNL], Kv[kHiNL], Mp[kHiNL];
+    const double* un = u + n * nl * nx;
+    for (int l = 0; l < nl; ++l) {
+      stencil_MK<DIM>(un + l * nx, n1, h, c, Mv[l], Kv[l], true);
+      double kd;
+      Mp[l] = 0.0;
+      if (n > 0) stencil_MK<DIM>(un - nl * nx + l * nx, n1, h, c, Mp[l], kd, false);
+    }
+    for (int k = 0; k < nl; ++k) {
+      double s = 0.0;
+      for (int l = 0; l < nl; ++l) s += Mv[l] * tc.K[k * kMaxNL + l];
+      for (int l = 0; l < nl; ++l) s += Kv[l] * tc.M[k * kMaxNL + l];
+      for (int l = 0; l < nl; ++l) s -= Mp[l] * tc.N[k * kMaxNL + l];
+      const i64 o = (n * nl + k) * nx + r;
+      y[o] = residual ? __ldg(f + o) - s : s;
+    }
+  }
+}
+
+// Per-mode exact block solve in place (sine basis).
+template <int DIM>
+__global__ void __launch_bounds__(128) k_modal_solve_hi(double* __restrict__ x,
+                                                        const TimeConsts tc, const SP s,
+                                                        const i64 n_t) {
+  const unsigned r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= s.nx) return;
+  const int nl = tc.nl;
+  double Mj, Kj;
+  mode_eig<DIM>(s, r, Mj, Kj);
+  for (i64 n = blockIdx.y; n < n_t; n += gridDim.y) {
+    double A[kHiNL][kHiNL], b[kHiNL];
+    hi_block<DIM>(tc, Mj, Kj, A);
+    double* p = x + n * nl * s.nx + r;
+    for (int l = 0; l < nl; ++l) b[l] = p[l * s.nx];
+    hi_solve(nl, A, b);
+    for (int l = 0; l < nl; ++l) p[l * s.nx] = b[l];
+  }
+}
+
+// Per-mode forward substitution u_n = A^-1 (f_n + M_j N u_{n-1}).
+template <int DIM>
+__global__ void __launch_bounds__(128) k_fwdsub_hi(const double* __restrict__ f,
+                                                   double* __restrict__ u, const TimeConsts tc,
+                                                   const SP s, const i64 n_t) {
+  const unsigned r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= s.nx) return;
+  const int nl = tc.nl;
+  double Mj, Kj;
+  mode_eig<DIM>(s, r, Mj, Kj);
+  double prev[kHiNL];
+  for (int l = 0; l < nl; ++l) prev[l] = 0.0;
+  for (i64 m = 0; m < n_t; ++m) {
+    double A[kHiNL][kHiNL], b[kHiNL];
+    hi_block<DIM>(tc, Mj, Kj, A);
+    for (int k = 0; k < nl; ++k) {
+      double s2 = 0.0;
+      for (int l = 0; l < nl; ++l) s2 += tc.N[k * kMaxNL + l] * prev[l];
+      b[k] = __ldg(f + (m * nl + k) * s.nx + r) + Mj * s2;
+    }
+    hi_solve(nl, A, b);
+    for (int l = 0; l < nl; ++l) {
+      u[(m * nl + l) * s.nx + r] = b[l];
+      prev[l] = b[l];
+    }
+  }
+}
+
+// restrict_semi / restrict_full (transfer.cpp:75-85, 138-149).
+template <int DIM, int CO>
+__global__ void __launch_bounds__(128) k_restrict_hi(const double* __restrict__ fine,
+                                                     double* __restrict__ coarse,
+                                                     const TimeConsts tc, const i64 n1,
+                                                     const i64 n1c, const i64 ntc) {
+  const i64 nx = ipow(n1, DIM), nxc = ipow(n1c, DIM);
+  const unsigned rc = blockIdx.x * blockDim.x + threadIdx.x;
+  if (rc >= nxc) return;
+  const int nl = tc.nl;
+  int c[3];
+  coords<DIM>(rc, unsigned(n1c), c);
+  for (i64 nc = blockIdx.y; nc < ntc; nc += gridDim.y) {
+    double v0[kHiNL], v1[kHiNL];
+    for (int l = 0; l < nl; ++l) v0[l] = v1[l] = 0.0;
+    const double* a0 = fine + (2 * nc) * nl * nx;
+    const double* a1 = a0 + nl * nx;
+    const int dzn = (CO == 2 && DIM > 2) ? 3 : 1, dyn = (CO == 2 && DIM > 1) ? 3 : 1;
+    const int dxn = CO == 2 ? 3 : 1;
+    for (int dz = 0; dz < dzn; ++dz)
+      for (int dy = 0; dy < dyn; ++dy)
+        for (int dx = 0; dx < dxn; ++dx) {
+          i64 rf = rc;
+          double w = 1.0;
+          if (CO == 2) {
+            const i64 fx = 2 * c[0] + dx;
+            const i64 fy = DIM > 1 ? 2 * c[1] + dy : 0;
+            const i64 fz = DIM > 2 ? 2 * c[2] + dz : 0;
+            w = (dx == 1 ? 1.0 : 0.5) * (DIM > 1 ? (dy == 1 ? 1.0 : 0.5) : 1.0) *
+                (DIM > 2 ? (dz == 1 ? 1.0 : 0.5) : 1.0);
+            rf = (fz * n1 + fy) * n1 + fx;
+          }
+          for (int l = 0; l < nl; ++l) {
+            v0[l] += w * __ldg(a0 + l * nx + rf);
+            v1[l] += w * __ldg(a1 + l * nx + rf);
+          }
+        }
+    double* o = coarse + nc * nl * nxc + rc;
+    for (int k = 0; k < nl; ++k) {
+      double s0 = 0.0, s1 = 0.0;
+      for (int l = 0; l < nl; ++l) {
+        s0 += v0[l] * tc.R1[k * kMaxNL + l];
+        s1 += v1[l] * tc.R2[k * kMaxNL + l];
+      }
+      o[k * nxc] = s0 + s1;
+    }
+  }
+}
+
+// prolong_semi / prolong_full (transfer.cpp:87-96, 151-158).
+template <int DIM, int CO>
+__global__ void __launch_bounds__(128) k_prolong_hi(const double* __restrict__ coarse,
+                                                    double* __restrict__ fine,
+                                                    const TimeConsts tc, const i64 n1,
+                                                    const i64 n1c, const i64 n_t) {
+  const i64 nx = ipow(n1, DIM), nxc = ipow(n1c, DIM);
+  const unsigned r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nx) return;
+  const int nl = tc.nl;
+  int c[3];
+  coords<DIM>(r, unsigned(n1), c);
+  for (i64 n = blockIdx.y; n < n_t; n += gridDim.y) {
+    const i64 nc = n >> 1;
+    double cv[kHiNL];
+    for (int l = 0; l < nl; ++l) cv[l] = 0.0;
+    const double* src = coarse + nc * nl * nxc;
+    if (CO == 1) {
+      for (int k = 0; k < nl; ++k) cv[k] = __ldg(src + k * nxc + r);
+    } else {
+      int j[3][2], cnt[3];
+      double w[3][2];
+      for (int a = 0; a < 3; ++a) {
+        cnt[a] = 1;
+        j[a][0] = j[a][1] = 0;
+        w[a][0] = 1.0;
+        w[a][1] = 0.0;
+        if (a >= DIM) continue;
+        const int i = c[a];
+        if (i % 2 == 1) {
+          j[a][0] = i / 2;
+        } else {
+          const int jj = i / 2;
+          cnt[a] = 0;
+          if (jj > 0) {
+            j[a][cnt[a]] = jj - 1;
+            w[a][cnt[a]++] = 0.5;
+          }
+          if (jj < n1c) {
+            j[a][cnt[a]] = jj;
+            w[a][cnt[a]++] = 0.5;
+          }
+        }
+      }
+      for (int iz = 0; iz < cnt[2]; ++iz)
+        for (int iy = 0; iy < cnt[1]; ++iy)
+          for (int ix = 0; ix < cnt[0]; ++ix) {
+            const double ww = w[0][ix] * w[1][iy] * w[2][iz];
+            const i64 rc = (i64(j[2][iz]) * n1c + j[1][iy]) * n1c + j[0][ix];
+            for (int k = 0; k < nl; ++k) cv[k] += ww * __ldg(src + k * nxc + rc);
+          }
+    }
+    const double* Rm = (n & 1) ? tc.R2 : tc.R1;
+    for (int l = 0; l < nl; ++l) {
+      double s = 0.0;
+      for (int k = 0; k < nl; ++k) s += cv[k] * Rm[k * kMaxNL + l];
+      fine[(n * nl + l) * nx + r] = s;
+    }
+  }
+}
+
+template <int DIM>
+__global__ void k_fold_u0_hi(double* __restrict__ f, const double* __restrict__ u0, const i64 n1,
+                             const i64 nx, const double h, const TimeConsts tc) {
+  const unsigned r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nx) return;
+  int c[3];
+  coords<DIM>(r, unsigned(n1), c);
+  double Mv, Kv;
+  stencil_MK<DIM>(u0, n1, h, c, Mv, Kv, false);
+  for (int k = 0; k < tc.nl; ++k) f[k * nx + r] += tc.psi0[k] * Mv;
+}
+
+#define STMG_DIM_DISPATCH(dim, ...)        \
+  switch (dim) {                            \
+    case 1: {                               \
+      constexpr int DIM = 1;                \
+      __VA_ARGS__;                          \
+    } break;                                \
+    case 2: {                               \
+      constexpr int DIM = 2;                \
+      __VA_ARGS__;                          \
+    } break;                                \
+    case 3: {                               \
+      constexpr int DIM = 3;                \
+      __VA_ARGS__;                          \
+    } break;                                \
+    default:                                \
+      return cudaErrorInvalidValue;         \
+  }
+
 // ================================================================ DST-I
 // Orthonormal DST-I of length n1 = N-1 (N = 2^LOG2N) along one axis, with a
 // complex FFT of length N per PAIR of real lines (a + i b):
@@ -3485,6 +3751,13 @@ cudaError_t launch_apply_rb(const LevelView& L, const double* u, const double* f
 cudaError_t launch_apply(const LevelView& L, const double* u, const double* f, double* y,
                          bool residual, const double* ab, cudaStream_t st) {
   if (L.n_t * L.sp.nx == 0) return cudaSuccess;
+  if (L.tc.nl > kFastNL) {
+    STMG_DIM_DISPATCH(L.sp.dim, {
+      k_apply_hi<DIM><<<grid2(L.sp.nx, L.n_t, 128), 128, 0, st>>>(
+          u, f, y, L.tc, L.sp.n1, L.sp.nx, L.sp.h, L.n_t, residual ? 1 : 0);
+    });
+    return cudaGetLastError();
+  }
   // register-blocked kernel: measured faster in 3D (27-point stencil), slower
   // in 2D (profiles/r01_v8_residual_ab.txt); STMG_APPLY_RB=0/1 forces either
   static const int rb = [] {
@@ -3543,6 +3816,18 @@ cudaError_t launch_restrict(const LevelView& F, int mode, int64_t n1c, const dou
   const i64 n1o = mode == 2 ? n1c : F.sp.n1;
   const i64 nxo = n1o * (F.sp.dim > 1 ? n1o : 1) * (F.sp.dim > 2 ? n1o : 1);
   if (ntc * nxo == 0) return cudaSuccess;
+  if (F.tc.nl > kFastNL) {
+    const i64 nc1 = mode == 2 ? n1c : F.sp.n1;
+    STMG_DIM_DISPATCH(F.sp.dim, {
+      if (mode == 2)
+        k_restrict_hi<DIM, 2><<<grid2(nxo, ntc, 128), 128, 0, st>>>(fine, coarse, F.tc, F.sp.n1,
+                                                                   nc1, ntc);
+      else
+        k_restrict_hi<DIM, 1><<<grid2(nxo, ntc, 128), 128, 0, st>>>(fine, coarse, F.tc, F.sp.n1,
+                                                                   nc1, ntc);
+    });
+    return cudaGetLastError();
+  }
   const dim3 g = grid2(nxo, ntc, 256);
   STMG_DISPATCH(F.sp.dim, F.tc.nl, {
     const TM<NL> t = make_tm<NL>(F.tc);
@@ -3558,6 +3843,18 @@ cudaError_t launch_prolong(const LevelView& F, int mode, int64_t n1c, const doub
                            double* fine, cudaStream_t st) {
   const i64 total = F.n_t * F.sp.nx;
   if (total == 0) return cudaSuccess;
+  if (F.tc.nl > kFastNL) {
+    const i64 nc1 = mode == 2 ? n1c : F.sp.n1;
+    STMG_DIM_DISPATCH(F.sp.dim, {
+      if (mode == 2)
+        k_prolong_hi<DIM, 2><<<grid2(F.sp.nx, F.n_t, 128), 128, 0, st>>>(coarse, fine, F.tc,
+                                                                        F.sp.n1, nc1, F.n_t);
+      else
+        k_prolong_hi<DIM, 1><<<grid2(F.sp.nx, F.n_t, 128), 128, 0, st>>>(coarse, fine, F.tc,
+                                                                        F.sp.n1, nc1, F.n_t);
+    });
+    return cudaGetLastError();
+  }
   const dim3 g = grid2(F.sp.nx, F.n_t, 256);
   STMG_DISPATCH(F.sp.dim, F.tc.nl, {
     const TM<NL> t = make_tm<NL>(F.tc);
@@ -3570,6 +3867,13 @@ cudaError_t launch_prolong(const LevelView& F, int mode, int64_t n1c, const doub
 }
 
 cudaError_t launch_fold_u0(const LevelView& L, double* f, const double* u0, cudaStream_t st) {
+  if (L.tc.nl > kFastNL) {
+    STMG_DIM_DISPATCH(L.sp.dim, {
+      k_fold_u0_hi<DIM><<<grid1(L.sp.nx, 256), 256, 0, st>>>(f, u0, L.sp.n1, L.sp.nx, L.sp.h,
+                                                             L.tc);
+    });
+    return cudaGetLastError();
+  }
   STMG_DISPATCH(L.sp.dim, L.tc.nl, {
     k_fold_u0<DIM, NL><<<grid1(L.sp.nx, 256), 256, 0, st>>>(f, u0, L.sp.n1, L.sp.nx, L.sp.h, L.tc);
   });
@@ -3709,6 +4013,12 @@ cudaError_t launch_modal_solve(const LevelView& L, double* x, cudaStream_t st) {
   const i64 total = L.n_t * L.sp.nx;
   if (total == 0) return cudaSuccess;
   const SP s = make_sp(L.sp);
+  if (L.tc.nl > kFastNL) {
+    STMG_DIM_DISPATCH(L.sp.dim, {
+      k_modal_solve_hi<DIM><<<grid2(L.sp.nx, L.n_t, 128), 128, 0, st>>>(x, L.tc, s, L.n_t);
+    });
+    return cudaGetLastError();
+  }
   STMG_DISPATCH(L.sp.dim, L.tc.nl, {
     k_modal_solve<DIM, NL><<<grid2(L.sp.nx, L.n_t, 256), 256, 0, st>>>(x, make_tm<NL>(L.tc), s,
                                                                         L.n_t);
@@ -3718,6 +4028,12 @@ cudaError_t launch_modal_solve(const LevelView& L, double* x, cudaStream_t st) {
 
 cudaError_t launch_modal_fwdsub(const LevelView& L, const double* f, double* u, cudaStream_t st) {
   const SP s = make_sp(L.sp);
+  if (L.tc.nl > kFastNL) {
+    STMG_DIM_DISPATCH(L.sp.dim, {
+      k_fwdsub_hi<DIM><<<grid1(L.sp.nx, 128), 128, 0, st>>>(f, u, L.tc, s, L.n_t);
+    });
+    return cudaGetLastError();
+  }
   STMG_DISPATCH(L.sp.dim, L.tc.nl, {
     PDLK(k_fwdsub<DIM, NL>, grid1(L.sp.nx, 128), 128, 0, st, f, u, make_tm<NL>(L.tc), s, L.n_t);
   });

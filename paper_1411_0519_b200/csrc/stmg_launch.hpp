@@ -7,7 +7,8 @@
 
 namespace stmg {
 
-constexpr int kMaxNL = 4;  // p_t <= 3 on the GPU path
+constexpr int kMaxNL = 11;  // p_t <= kMaxTimeDegree = 10 (dg_time.hpp:10)
+constexpr int kFastNL = 4;  // the fused spectral kernels: p_t <= 3
 
 // DG time-step blocks and transfer blocks, row-major with row stride kMaxNL.
 struct TimeConsts {

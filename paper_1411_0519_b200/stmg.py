@@ -34,6 +34,14 @@ def critical_mu(p_t: int) -> float:
     return v
 
 
+def fill_random_host(n: int, seed: int) -> np.ndarray:
+    """fill_random (mg.cpp:168-173), reference-exact: std::mt19937_64(seed),
+    v[i] = (gen() >> 11) * 2^-53 in [0, 1); host only."""
+    v = np.empty(int(n))
+    check(A.lib().stmg_fill_random_host(v.ctypes.data, int(n), int(seed)))
+    return v
+
+
 def assemble_dg_block(p_t: int, tau: float):
     """assemble_dg_block (dg_time.cpp:125-166) -> (K, M, N)."""
     n = max(p_t + 1, 1)
@@ -357,6 +365,10 @@ class Hierarchy:
                 for r in reps[:k]]
 
     # ---- inputs ----------------------------------------------------------------
+    def fill_random(self, v: BlockVector, seed: int) -> BlockVector:
+        """fill_random(v, seed) of the reference (mg.cpp:168-173), bit-exact."""
+        return v.copy_from(fill_random_host(v.n, seed))
+
     def fill_uniform(self, v: BlockVector, seed: int, stream: int, offset: int = 0) -> BlockVector:
         check(A.lib().stmg_fill_uniform(self._ctx, v.ptr, v.n, seed, stream, offset))
         return v

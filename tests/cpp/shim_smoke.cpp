@@ -18,7 +18,7 @@ int main() {
   const STHierarchy h = build_hierarchy(p);
   const STOperator op = h.finest().op();
   BlockVector f = make_vector(op), u = make_vector(op), r = make_vector(op);
-  fill_random(f, 42, 0);
+  fill_uniform(f, 42, 0);
   CycleConfig cfg;
   cfg.nu1 = cfg.nu2 = 1;
   const SolveReport rep = solve(h, f, u, cfg, 1e-8);
@@ -31,6 +31,22 @@ int main() {
   const SolveReport irep = solve(h, f, ui, icfg, 1e-8);
   const SpatialVCycleSolver vc(op);
   const BlockVector x = vc.cycle(f, nullptr, icfg.smoother);
+  // reference-signature overloads (smoother.hpp:68-70, st_system.hpp:70-72, transfer.hpp:27-44)
+  const BlockSolver lu(op);
+  const SpatialVCycleSolver svc(op);
+  BlockSolveContext bctx;
+  bctx.exact = &lu;
+  bctx.vcycle = &svc;
+  BlockVector us = make_vector(op);
+  fill_random(us, 7);  // mt19937_64, [0, 1) (mg.cpp:168-173)
+  block_jacobi_step(op, bctx, us, f, cfg.smoother);
+  const BlockVector fs = forward_substitution_solve(op, lu, f);
+  const TimeTransfer tt = build_time_transfer(p.p_t, 1.0);
+  const SpaceGrid g0 = build_space_grid(1, p.space_level), g1 = build_space_grid(1, p.space_level - 1);
+  const BlockVector rf = restrict_full(tt, g0, g1, us);
+  const BlockVector pf = prolong_full(tt, g1, g0, rf);
+  const bool overloads_ok = rf.n_t() == us.n_t() / 2 && rf.n_x() == g1.n_nodes &&
+                            pf.size() == us.size() && fs.size() == f.size();
   bool threw = false;
   try {
     BlockVector odd(op.ctx, 3, 63, 2);
@@ -38,8 +54,8 @@ int main() {
   } catch (const std::invalid_argument&) {
     threw = true;
   }
-  std::printf("{\"iterations\": %d, \"converged\": %d, \"rel_residual\": %.17g, \"levels\": %zu, \"threw\": %d, \"inexact_iterations\": %d, \"inexact_converged\": %d, \"vcycle_size\": %lld}\n",
+  std::printf("{\"iterations\": %d, \"converged\": %d, \"rel_residual\": %.17g, \"levels\": %zu, \"threw\": %d, \"inexact_iterations\": %d, \"inexact_converged\": %d, \"vcycle_size\": %lld, \"overloads_ok\": %d}\n",
               rep.iterations, int(rep.converged), rel, h.levels.size(), int(threw),
-              irep.iterations, int(irep.converged), (long long)x.size());
-  return rep.converged && rel <= 1e-8 && threw && irep.converged ? 0 : 1;
+              irep.iterations, int(irep.converged), (long long)x.size(), int(overloads_ok));
+  return rep.converged && rel <= 1e-8 && threw && irep.converged && overloads_ok ? 0 : 1;
 }

@@ -96,3 +96,15 @@ def test_no_cpu_fallback(capi):
     from paper_1411_0519_b200 import stmg
     with pytest.raises(RuntimeError, match="no CUDA device"):
         stmg.Hierarchy(1, 1, 5, 6)
+
+
+def test_fill_random_is_reference_mt19937_64(capi):
+    """fill_random (mg.cpp:168-173) is std::mt19937_64 with (x >> 11) * 2^-53.
+    Known answer: the C++ standard fixes the 10000th output of a default-seeded
+    (5489) mt19937_64 at 9981545732273789042 ([rand.predef])."""
+    from paper_1411_0519_b200 import stmg
+    v = stmg.fill_random_host(10000, 5489)
+    assert v[-1] == float(9981545732273789042 >> 11) * 2.0 ** -53
+    assert v.min() >= 0.0 and v.max() < 1.0
+    assert np.array_equal(stmg.fill_random_host(100, 42), stmg.fill_random_host(100, 42))
+    assert not np.array_equal(stmg.fill_random_host(100, 42), stmg.fill_random_host(100, 43))

@@ -433,3 +433,40 @@ def test_one_pass_2d_transform_matches_oracle(S, sl):
     assert rel(us, o.smooth(0, u, b, 0.5, 2)) < 1e-11
     fs = g.forward_substitution_solve(0, g.upload(b)).numpy()
     assert rel(fs, o.forward_substitution(0, b)) < 1e-11
+
+
+@pytest.mark.parametrize("case", [
+    (4, 1, 4, 3, 1.0, 0), (5, 2, 3, 3, 0.5, 0), (7, 1, 3, 2, 1.0, 2), (10, 1, 3, 2, 1.0, 0),
+    (4, 3, 2, 2, 1.0, 0),
+])
+def test_high_degree_matches_oracle(S, case):
+    """p_t 4..10 (dg_time.hpp:10; SPEC acceptance p_t 0..5): every operator
+    and a full solve against the oracle (runtime-NL physical kernels)."""
+    p, dim, sl, tl, T, pol = case
+    g, o = pair(S, p, dim, sl, tl, T, pol)
+    for lev in range(len(o.levels)):
+        n = o.levels[lev].size
+        u = O.fill_uniform(n, 100 + lev, 0)
+        f = O.fill_uniform(n, 200 + lev, 0)
+        du, df = g.upload(u, lev), g.upload(f, lev)
+        assert rel(g.apply(lev, du).numpy(), o.apply(lev, u)) < 1e-12
+        assert rel(g.residual(lev, du, df).numpy(), o.residual(lev, u, f)) < 1e-12
+        assert rel(g.block_solve(lev, df).numpy(), o.block_solve(lev, f)) < 1e-11
+        us = g.block_jacobi_step(lev, g.upload(u, lev), df, 0.5, 1).numpy()
+        assert rel(us, o.smooth(lev, u, f, 0.5, 1)) < 1e-11
+        assert rel(g.forward_substitution_solve(lev, df).numpy(),
+                   o.forward_substitution(lev, f)) < 1e-10
+        if o.levels[lev].coarsen_to_next:
+            mode = o.levels[lev].coarsen_to_next
+            rc = g.restrict(lev, du, mode).numpy()
+            assert rel(rc, o.restrict(lev, u, mode)) < 1e-13
+            dc = g.coarse_vector(lev, mode).copy_from(rc)
+            assert rel(g.prolong(lev, dc, mode).numpy(), o.prolong(lev, rc, mode)) < 1e-13
+    f = O.fill_uniform(o.levels[0].size, 7, 0)
+    u_o, rep_o = o.solve(f, eps=1e-8)
+    du = g.vector(0)
+    rep = g.solve(g.upload(f), du, S.CycleConfig(nu1=1, nu2=1), 1e-8)  # spectral request -> physical
+    assert rep.converged and rep.iterations == rep_o["iterations"]
+    assert rel(du.numpy(), u_o) < 1e-9
+    with pytest.raises(ValueError):
+        g.solve(g.upload(f), g.vector(0), S.CycleConfig(nu1=1, nu2=1, block_solver="vcycle"), 1e-8)
