@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libstmg_b200.so")
-SOURCES = ["stmg_kernels.cu", "stmg_spatial.cu", "stmg_capi.cu", "stmg_setup.cpp", "stmg_lfa.cpp"]
+SOURCES = ["stmg_kernels.cu", "stmg_apply.cu", "stmg_spatial.cu", "stmg_capi.cu", "stmg_setup.cpp", "stmg_lfa.cpp"]
 HEADERS = [os.path.join(CSRC, h) for h in ("stmg_launch.hpp", "stmg_modal.cuh", "stmg_setup.hpp", "stmg_lfa.hpp")] + [
     os.path.join(ROOT, "include", "stmg_b200.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -785,28 +785,6 @@ struct TmaShape {
   static constexpr size_t smem = size_t(kTmaStages) * STAGE * sizeof(double);
 };
 
-__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes,
-                                         unsigned bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
 __device__ __forceinline__ void cp_async16cg(unsigned dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
 }
@@ -3757,6 +3735,16 @@ cudaError_t launch_apply(const LevelView& L, const double* u, const double* f, d
           u, f, y, L.tc, L.sp.n1, L.sp.nx, L.sp.h, L.n_t, residual ? 1 : 0);
     });
     return cudaGetLastError();
+  }
+  // row-band kernels (stmg_apply.cu: TMA bulk row staging, rolling windows);
+  // STMG_APPLY_ROWS=0 keeps the tile kernels below
+  static const bool rows = [] {
+    const char* e = std::getenv("STMG_APPLY_ROWS");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (rows) {
+    const cudaError_t e = launch_apply_rows(L, u, f, y, residual, ab, st);
+    if (e != cudaErrorNotSupported) return e;
   }
   // register-blocked kernel: measured faster in 3D (27-point stencil), slower
   // in 2D (profiles/r01_v8_residual_ab.txt); STMG_APPLY_RB=0/1 forces either

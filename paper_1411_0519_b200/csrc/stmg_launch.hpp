@@ -48,6 +48,10 @@ struct LevelView {
 // ab: device array [a_0..a_{kMaxNL}), [b_0..) with N_tau = a b^T.
 cudaError_t launch_apply(const LevelView& L, const double* u, const double* f,
                          double* y, bool residual, const double* ab, cudaStream_t st);
+// Row-band variant (stmg_apply.cu); cudaErrorNotSupported when the level's
+// shape has no such kernel (launch_apply falls through to the tile kernels).
+cudaError_t launch_apply_rows(const LevelView& L, const double* u, const double* f,
+                              double* y, bool residual, const double* ab, cudaStream_t st);
 cudaError_t launch_restrict(const LevelView& F, int mode, int64_t n1c,
                             const double* fine, double* coarse, cudaStream_t st);
 cudaError_t launch_prolong(const LevelView& F, int mode, int64_t n1c,

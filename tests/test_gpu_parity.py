@@ -470,3 +470,21 @@ def test_high_degree_matches_oracle(S, case):
     assert rel(du.numpy(), u_o) < 1e-9
     with pytest.raises(ValueError):
         g.solve(g.upload(f), g.vector(0), S.CycleConfig(nu1=1, nu2=1, block_solver="vcycle"), 1e-8)
+
+
+@pytest.mark.parametrize("case", [
+    (0, 2, 6, 3), (1, 2, 6, 6), (2, 2, 6, 4), (3, 2, 6, 2), (2, 2, 7, 3), (1, 2, 8, 2),
+    (1, 3, 5, 4), (2, 3, 5, 2), (0, 3, 5, 3), (3, 3, 5, 1), (1, 3, 6, 1),
+])
+def test_row_band_residual_matches_oracle(S, case):
+    """apply / residual on grids wide enough for the row-band kernels
+    (csrc/stmg_apply.cu: 127 .. 511 nodes per axis in 2D, 63 / 127 in 3D),
+    several time chunks per CTA column, partial last band."""
+    p, dim, sl, tl = case
+    g, o = pair(S, p, dim, sl, tl, 1.0)
+    n = o.levels[0].size
+    u = O.fill_uniform(n, 300 + sl, 0)
+    f = O.fill_uniform(n, 400 + sl, 0)
+    du, df = g.upload(u, 0), g.upload(f, 0)
+    assert rel(g.apply(0, du).numpy(), o.apply(0, u)) < 1e-12
+    assert rel(g.residual(0, du, df).numpy(), o.residual(0, u, f)) < 1e-12
