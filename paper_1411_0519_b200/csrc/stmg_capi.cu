@@ -497,14 +497,32 @@ void dst_all(stmg_ctx* c, Level& L, const double* in, double* out, bool accumula
 void block_solve(stmg_ctx* c, Level& L, const double* b, double* x, double* acc_into = nullptr,
                  double alpha = 1.0) {
   const int dim = L.spec.dim;
-  CK(stmg::launch_dst_axis(L.view, 0, b, x, false, 1.0, L.d_twiddle, c->stream));
-  count(c);
-  for (int a = 1; a < dim; ++a) {
-    CK(stmg::launch_dst_axis(L.view, a, x, x, false, 1.0, L.d_twiddle, c->stream));
+  // forward transform: one-pass cluster kernel where the shape has one (2D,
+  // 127-node slabs), else one pass per axis
+  cudaError_t e2 = dim == 2 ? stmg::launch_dst2d(L.view, b, x, false, 1.0, L.d_twiddle, c->stream)
+                            : cudaErrorNotSupported;
+  if (e2 != cudaErrorNotSupported) {
+    CK(e2);
     count(c);
+  } else {
+    CK(stmg::launch_dst_axis(L.view, 0, b, x, false, 1.0, L.d_twiddle, c->stream));
+    count(c);
+    for (int a = 1; a < dim; ++a) {
+      CK(stmg::launch_dst_axis(L.view, a, x, x, false, 1.0, L.d_twiddle, c->stream));
+      count(c);
+    }
   }
   CK(stmg::launch_modal_solve(L.view, x, c->stream));
   count(c);
+  double* out = acc_into ? acc_into : x;
+  e2 = dim == 2 ? stmg::launch_dst2d(L.view, x, out, acc_into != nullptr, alpha, L.d_twiddle,
+                                     c->stream)
+                : cudaErrorNotSupported;
+  if (e2 != cudaErrorNotSupported) {
+    CK(e2);
+    count(c);
+    return;
+  }
   for (int a = 0; a < dim; ++a) {
     const bool last = a + 1 == dim;
     if (last && acc_into) {
