@@ -339,6 +339,64 @@ def updown_profile(h, step):
     return prof, dev
 
 
+def operator_record(h, f, u, reps=6):
+    """Reference-API operators on level 0 of an open single-GPU context:
+    the physical Q1 residual (stmg_residual, 24 B per dof) and one damped
+    block-Jacobi sweep through stmg_smooth (exact blocks).  Residual: CUDA
+    events on the library stream around each launch (profile slot 3), L2
+    evicted before every launch when the vectors are smaller than L2;
+    smoother: events around each whole sweep (profile slot 5: residual +
+    transforms + modal solve + update launches)."""
+    import ctypes as C
+    from paper_1411_0519_b200 import _capi as A
+    peak, kind = peaks()
+    n0 = h.size(0)
+    r = h.vector(0)
+    flush = None
+    if 3 * n0 * 8 < (512 << 20):
+        flush = C.c_void_p()
+        A.check(A.lib().stmg_device_alloc(h._ctx, L2_FLUSH_BYTES, C.byref(flush)))
+
+    def evict():
+        if flush is not None:
+            A.check(A.lib().stmg_memset_zero(h._ctx, flush, L2_FLUSH_BYTES))
+
+    h.residual(0, u, f, r)  # warm-up
+    h.synchronize()
+    h.profile(True)
+    h.profile_reset()
+    for _ in range(reps):
+        evict()
+        h.residual(0, u, f, r)
+    ms, n, b = h.profile_read(3)
+    h.profile(False)
+    res = b / ((ms / n) * 1e-3) / 1e9
+    h.block_jacobi_step(0, r, f, 0.5, 1)  # warm-up (r as the iterate: u stays intact)
+    h.synchronize()
+    h.profile(True)
+    h.profile_reset()
+    for _ in range(reps):
+        evict()
+        h.block_jacobi_step(0, r, f, 0.5, 1)
+    sms, sn, _ = h.profile_read(5)
+    h.profile(False)
+    sm = sms / sn
+    if flush is not None:
+        A.lib().stmg_device_free(h._ctx, flush)
+    del r
+    return {
+        "residual": {"kernel": "k_apply_rows (stmg_residual)", "ms_per_launch": ms / n,
+                     "achieved": res, "unit": "GB/s", "peak": peak, "peak_kind": kind,
+                     "frac": res / peak, "algorithmic_bytes_per_dof": 24},
+        "smoother_reference_api": {
+            "api": "stmg_smooth, one sweep: residual + forward sine transform + modal block "
+                   "solve + inverse transform with u += omega x",
+            "ms_per_sweep": sm, "achieved": 24.0 * n0 / (sm * 1e-3) / 1e9, "unit": "GB/s",
+            "frac": 24.0 * n0 / (sm * 1e-3) / 1e9 / peak, "algorithmic_bytes_per_dof": 24,
+            "bound": "shared-memory pipe of the FFT passes, not HBM (DESIGN.md 5)"},
+    }
+
+
 def scaling_record(stmg, name, base, weak, world, rank, local, dist, steps, warmup):
     """Sub-record of one scaling curve at this N (the driver's per-N runs give
     the curve; efficiencies are computed by the reader, not here)."""
@@ -381,6 +439,9 @@ def scaling_record(stmg, name, base, weak, world, rank, local, dist, steps, warm
         "updown_gbs_per_rank": gather_obj(dist, gbs),
         "updown_ms_per_launch_rank0": (ms / nl) if nl else None,
     }
+    if world == 1:
+        h.fill_uniform(u, SEED + 1, 0)
+        rec["operators"] = operator_record(h, f, u, reps=3)
     del f, u, h
     gc.collect()
     return rec
@@ -529,6 +590,10 @@ def run_ours(args, cfgname):
             "measured": "CUDA events on the library stream around every launch, in a replay of "
                         "the K timed steps right after the timed region",
             "transform_ms_per_solve": prof[2][0] / max(len(prof_dev), 1)}
+    ops = None
+    if world == 1:
+        h.fill_uniform(u, SEED + 1, 0)
+        ops = {cfgname: operator_record(h, f, u)}
     del f, u
     A.lib().stmg_device_free(h._ctx, flush)
     h.close()
@@ -541,6 +606,21 @@ def run_ours(args, cfgname):
                                            dist, args.scaling_steps, 1)
         subs["C5_weak"] = scaling_record(stmg, "C5_weak", "C5", True, world, rank, local, dist,
                                          args.scaling_steps, 1)
+        if world == 1:
+            # configs[3] (3D): operators only (its solve is a parity-test case)
+            c4 = CONFIGS["C4"]
+            h4 = stmg.Hierarchy(c4["p_t"], c4["dim"], c4["space_level"], c4["time_level"],
+                                c4["t_final"], device=local)
+            f4, u4 = h4.vector(0), h4.vector(0)
+            h4.fill_uniform(f4, SEED, 0)
+            h4.fill_uniform(u4, SEED + 1, 0)
+            ops["C4"] = operator_record(h4, f4, u4, reps=3)
+            del f4, u4
+            h4.close()
+            del h4
+            gc.collect()
+            for k_ in ("C3_strong", "C5_weak"):
+                ops[k_[:2]] = subs[k_].pop("operators")
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -575,6 +655,7 @@ def run_ours(args, cfgname):
                                        "serialised with the solve"}},
         "gpu_launches": int(launches),
         "roofline": roof,
+        "operators": ops,
         "clocks": clk,
         "scaling_runs": subs,
     }

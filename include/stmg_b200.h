@@ -246,7 +246,10 @@ int stmg_local_steps(const stmg_ctx* ctx, int64_t* first_step,
  *             1 = fused prolong+correct+post-smooth+residual-norm (finest),
  *             2 = basis transform pass, 3 = physical residual,
  *             4 = coarse part of a fused V(1,1) cycle (levels >= 1, all
- *                 kernels between two finest-level passes; bytes = 0). */
+ *                 kernels between two finest-level passes; bytes = 0),
+ *             5 = one damped block-Jacobi sweep of the physical smoother
+ *                 (stmg_smooth, exact blocks: residual + transforms + modal
+ *                 solve + update; bytes = 24 per dof, the reference's unit). */
 int stmg_profile_enable(stmg_ctx* ctx, int on);
 int stmg_profile_read(stmg_ctx* ctx, int kernel_id, double* total_ms,
                       int64_t* launches, double* bytes_per_launch);

@@ -545,9 +545,16 @@ cudaError_t launch_rows2_t(const LevelView& L, const double* u, const double* f,
   // rounded so that the grid is a whole number of waves of resident CTAs
   // (the C2 residual is a 40 us kernel of ~1 wave: a ragged last wave costs
   // up to half of it)
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_rows2<NL, RES, TYS, YS, XW>,
-                                                XW * YS * 32 + 32, smem);
+  static std::atomic<long long> occ_cache{-1};  // (smem << 8) | occ of the last query
+  long long oc = occ_cache.load();
+  if (oc < 0 || size_t(oc >> 8) != smem) {
+    int o = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_apply_rows2<NL, RES, TYS, YS, XW>,
+                                                  XW * YS * 32 + 32, smem);
+    oc = (static_cast<long long>(smem) << 8) | (o & 255);
+    occ_cache.store(oc);
+  }
+  const int occ = int(oc & 255);
   static const int sms = [] {
     int d = 0, n = 148;
     cudaGetDevice(&d);
@@ -625,12 +632,22 @@ cudaError_t launch_rows3_t(const LevelView& L, const double* u, const double* f,
   if (attr.first_use())
     cudaFuncSetAttribute(k_apply_rows3<NL, RES, TYS, YS, TZ, XW>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_rows3<NL, RES, TYS, YS, TZ, XW>,
-                                                XW * YS * 32 + 32, smem);
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static std::atomic<long long> occ_cache{-1};  // (smem << 8) | occ of the last query
+  long long oc = occ_cache.load();
+  if (oc < 0 || size_t(oc >> 8) != smem) {
+    int o = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_apply_rows3<NL, RES, TYS, YS, TZ, XW>,
+                                                  XW * YS * 32 + 32, smem);
+    oc = (static_cast<long long>(smem) << 8) | (o & 255);
+    occ_cache.store(oc);
+  }
+  const int occ = int(oc & 255);
+  static const int sms = [] {
+    int d = 0, n = 148;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    return n;
+  }();
   const i64 slots = i64(std::max(occ, 1)) * sms;
   i64 nch;
   if (c_env > 0) {

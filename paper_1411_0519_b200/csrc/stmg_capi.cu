@@ -181,7 +181,7 @@ struct stmg_ctx {
   std::vector<int> cur;  // current U buffer per level
   // profiling
   bool profile = false;
-  ProfSlot prof[5];
+  ProfSlot prof[6];
   i64 launches = 0;
   bool capturing = false;
   i64 captured_kernels = 0;
@@ -554,8 +554,10 @@ void smooth_phys(stmg_ctx* c, int level, double* u, const double* f, double omeg
   Level& L = c->levels[level];
   ensure(L.R, L.view.size());
   for (int s = 0; s < nu; ++s) {
+    prof_begin(c, 5);
     residual(c, L, u, f, L.R.base);
     block_solve(c, L, L.R.base, L.R.base, u, omega);
+    prof_end(c, 5, 24.0 * double(L.view.size()));  // the reference's unit: read u, f; write u
   }
 }
 
@@ -2946,7 +2948,7 @@ int stmg_profile_read(stmg_ctx* c, int id, double* total_ms, int64_t* launches,
                       double* bytes_per_launch) {
   return cguard(c, [&] {
     require(c != nullptr, "null context");
-    require(id >= 0 && id < 5, "kernel id out of range");
+    require(id >= 0 && id < 6, "kernel id out of range");
     CK(cudaStreamSynchronize(c->stream));
     prof_collect(c);
     if (total_ms) *total_ms = c->prof[id].total_ms;

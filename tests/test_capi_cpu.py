@@ -78,7 +78,7 @@ def test_host_setup_rejects_bad_arguments(capi):
     with pytest.raises(ValueError):
         stmg.Hierarchy(1, 4, 3, 3)
     with pytest.raises(ValueError):
-        stmg.Hierarchy(4, 1, 3, 3)  # p_t > 3 not on the GPU path
+        stmg.Hierarchy(11, 1, 3, 3)  # p_t > kMaxTimeDegree = 10 (dg_time.hpp:10)
     with pytest.raises(ValueError):
         stmg.Hierarchy(1, 1, 0, 2, two_grid=2)
 
