@@ -46,7 +46,8 @@ def _worker(rank, world, port, out):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import torch
-    p, lev, n_t, tau = 1, 3, 8, 0.05
+    p, lev, tl = 1, 3, 3
+    n_t, tau = 2 ** tl, 0.05
     K, M, N = dense.dg_block(p, tau)
     Mh, Kh = dense.space_mats(1, lev)
     nx, nl = Mh.shape[0], p + 1
@@ -54,7 +55,11 @@ def _worker(rank, world, port, out):
     rng = np.random.default_rng(7)
     u = rng.uniform(-1, 1, n_t * slab)
     f = rng.uniform(-1, 1, n_t * slab)
-    n_loc = n_t // world
+    # slab split from the library's own host-side plan (stmg_shard_plan, the
+    # function stmg_create_distributed uses), not re-derived here
+    from paper_1411_0519_b200 import stmg
+    gather_level, n_loc = stmg.shard_plan(p, 1, lev, tl, world)
+    assert n_loc * world == n_t and gather_level >= 1
     lo, hi = rank * n_loc * slab, (rank + 1) * n_loc * slab
     u_loc, f_loc = u[lo:hi].copy(), f[lo:hi].copy()
     # trace halo: last slab of rank g goes to rank g+1
