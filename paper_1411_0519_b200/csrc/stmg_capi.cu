@@ -1180,11 +1180,11 @@ void ensure_hist(stmg_ctx* c, int n) {
 }
 
 // Residual norm of the spectral iterate at level 0 (synchronising).
-double spectral_resnorm(stmg_ctx* c, int level) {
+double spectral_resnorm(stmg_ctx* c, int level, bool u_zero = false) {
   Level& L = c->levels[level];
   stmg::ModalArgs a = modal_args(L, nullptr, 0.5, false);
   CK(stmg::launch_resnorm(L.view, a, L.U[c->cur[level]].base, L.F.base, c->partials.base,
-                          c->stream));
+                          c->stream, u_zero));
   CK(stmg::launch_norm_final(c->partials.base, a.n_partials, c->d_norm, nullptr, 0, c->stream));
   count(c, 2);
   tiny(c, {to_host(c->h_norm, c->d_norm, 8)});
@@ -1512,13 +1512,18 @@ void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config
     tiny(c, {to_host(c->h_flag, c->d_flag, 4)});
     dst_all(c, L0, f, L0.F.base);
     CK(cudaStreamSynchronize(c->stream));
-    if (*c->h_flag) dst_all(c, L0, u, L0.U[0].base);
-    else CK(cudaMemsetAsync(L0.U[0].base, 0, size_t(L0.view.size()) * sizeof(double), c->stream));
-    const double r0 = spectral_resnorm(c, 0);
+    const bool u_zero = !*c->h_flag;
+    if (!u_zero) dst_all(c, L0, u, L0.U[0].base);
+    // zero guess: r0 = ||f|| from F alone (bitwise the general kernel's value)
+    const double r0 = spectral_resnorm(c, 0, u_zero);
     r.r0 = r.r_final = r0;
     push(r0);
     if (r0 == 0.0) r.converged = 1;
     const bool fused = fused_eligible(c, cfg) && !r.converged && max_iter > 0;
+    // the fused schedule's zero-guess prefix never reads U[0]; every other
+    // path (and the immediate return when f == 0) needs the zero iterate there
+    if (u_zero && !fused)
+      CK(cudaMemsetAsync(L0.U[0].base, 0, size_t(L0.view.size()) * sizeof(double), c->stream));
     if (fused) run_fused(c, cfg, eps, max_iter, history, history_cap, &nh, r, !*c->h_flag);
     // the device-side loop needs the finest iterate back in its buffer after
     // a cycle; the per-cycle graph (kept for profiling) reports where it ends

@@ -1852,7 +1852,10 @@ __global__ void __launch_bounds__(128) k_smooth(const double* __restrict__ f,
 }
 
 // Residual sum-of-squares partials of f - L u per (chunk, block).
-template <int DIM, int NL>
+// ZERO: u == 0 is known (zero initial guess): only f is read; every term that
+// involves u is an exact zero, so the partials are bitwise those of the
+// general kernel on a zero vector.
+template <int DIM, int NL, bool ZERO>
 __global__ void __launch_bounds__(128) k_resnorm(const double* __restrict__ u,
                                                  const double* __restrict__ f,
                                                  double* __restrict__ partials, const TM<NL> t,
@@ -1871,10 +1874,15 @@ __global__ void __launch_bounds__(128) k_resnorm(const double* __restrict__ u,
     double up[NL];
 #pragma unroll
     for (int l = 0; l < NL; ++l) up[l] = 0.0;
-    if (n0 > 0 || !first_global) load_nl<NL>(u + (n0 - 1) * slab + r, nx, up);
+    if (!ZERO && (n0 > 0 || !first_global)) load_nl<NL>(u + (n0 - 1) * slab + r, nx, up);
     for (i64 m = n0; m < nend; ++m) {
       double uv[NL], fv[NL], au[NL], np[NL];
-      load_nl<NL>(u + m * slab + r, nx, uv);
+      if (ZERO) {
+#pragma unroll
+        for (int l = 0; l < NL; ++l) uv[l] = 0.0;
+      } else {
+        load_nl<NL>(u + m * slab + r, nx, uv);
+      }
       load_nl<NL>(f + m * slab + r, nx, fv);
       apply_mode<NL>(t, Mj, Kj, uv, au);
       matvec<NL>(t.N, up, np);
@@ -2986,175 +2994,11 @@ __device__ __forceinline__ void dst_passes(double2* X, const int tt,
 #ifndef STMG_DST_MINB
 #define STMG_DST_MINB 5  // A/B vs 4 and 6: profiles/r01_v17_dst_minb_ab.txt
 #endif
-template <int LOG2N>
-__global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK, (LOG2N >= 4 ? STMG_DST_MINB : 1)) k_dst_lines_v1(
-    const double* __restrict__ in, double* __restrict__ out, const i64 n_lines, const i64 stride,
-    const double scale, const double alpha, const int accumulate,
-    const double2* __restrict__ tw) {
-  using S = DSTShape<LOG2N>;
-  constexpr int F = S::F, TL = S::TL, n1 = S::n1, N = S::N, BUF = S::BUF;
-  constexpr int TS = S::TS, KB = S::KB;
-  constexpr int BLK = S::BLOCK;
-  extern __shared__ double2 sm[];
-  double2* wsum = sm + F * BUF;  // per-thread scan totals
-  __shared__ i64 lbase[TL];      // global offset of element 0 of each tile line
-
-  const i64 line0 = i64(blockIdx.x) * TL;
-  const int nt = int(min(i64(TL), n_lines - line0));
-  for (int li = threadIdx.x; li < TL; li += BLK) {
-    const i64 line = line0 + min(li, nt - 1);
-    const i64 o = line / stride;
-    lbase[li] = o * stride * n1 + (line - o * stride);
-  }
-  for (int f = threadIdx.x; f < F; f += BLK) sm[f * BUF + dst_pad(0)] = make_double2(0.0, 0.0);
-  __syncthreads();
-  // ---- load fused with the pre-processing: items (line pair f, j = 1..N/2)
-  // load z_j = (a, b)_{j-1} and its mirror z_{N-j}, write
-  //   X_j = sin(j pi/N)(z_j + z_{N-j}) + (z_j - z_{N-j})/2,  X_{N-j} = ... - ...
-  // (one shared-memory store per value; the middle j = N/2 is its own mirror)
-  constexpr int H = N / 2;
-  constexpr int ITEMS_ALL = F * H;
-  constexpr int ITEMS = (ITEMS_ALL + BLK - 1) / BLK;
-  double2 lo[ITEMS], hi[ITEMS];
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int e = threadIdx.x + i * BLK;
-    int f, jj;
-    if (stride == 1) {
-      f = e / H;
-      jj = e - f * H;
-    } else {
-      jj = e / F;
-      f = e - jj * F;
-    }
-    double al = 0.0, bl = 0.0, ah = 0.0, bh = 0.0;
-    if (e < ITEMS_ALL) {
-      const i64 pl = i64(jj) * stride, ph = i64(N - 2 - jj) * stride;  // j - 1, N - j - 1
-      if (2 * f < nt) {
-        al = __ldcs(in + lbase[2 * f] + pl);
-        ah = __ldcs(in + lbase[2 * f] + ph);
-      }
-      if (2 * f + 1 < nt) {
-        bl = __ldcs(in + lbase[2 * f + 1] + pl);
-        bh = __ldcs(in + lbase[2 * f + 1] + ph);
-      }
-    }
-    lo[i] = make_double2(al, bl);
-    hi[i] = make_double2(ah, bh);
-  }
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int e = threadIdx.x + i * BLK;
-    if (e >= ITEMS_ALL) continue;
-    int f, jj;
-    if (stride == 1) {
-      f = e / H;
-      jj = e - f * H;
-    } else {
-      jj = e / F;
-      f = e - jj * F;
-    }
-    const int j = jj + 1;
-    double2* X = sm + f * BUF;
-    const double sj = -__ldg(tw + j).y;  // sin(j pi / N)
-    const double2 sum = make_double2(lo[i].x + hi[i].x, lo[i].y + hi[i].y);
-    const double2 dif = make_double2(0.5 * (lo[i].x - hi[i].x), 0.5 * (lo[i].y - hi[i].y));
-    X[dst_pad(j)] = make_double2(sj * sum.x + dif.x, sj * sum.y + dif.y);
-    if (j != H) X[dst_pad(N - j)] = make_double2(sj * sum.x - dif.x, sj * sum.y - dif.y);
-  }
-  __syncthreads();
-  // ---- FFT of length N per pair
-  const int team = threadIdx.x / TS, tt = threadIdx.x % TS;
-#ifndef STMG_DST_SKIP_FFT
-  dst_passes<LOG2N, 0, 1>(sm + team * BUF, tt, tw);
-#endif
-  __syncthreads();
-  // ---- post-processing: split a/b, X_{2k} = I_k, X_{2k+1} = prefix sum of R
-  double2* X = sm + team * BUF;
-  double2 Rv[KB], Iv[KB];
-  double2 run = make_double2(0.0, 0.0);
-#pragma unroll
-  for (int q = 0; q < KB; ++q) {
-    const int k = tt * KB + q;
-    double2 R = make_double2(0.0, 0.0), I = make_double2(0.0, 0.0);
-    if (k < N / 2) {
-      const double2 Y1 = X[dst_pad(k)], Y2 = X[dst_pad((N - k) & (N - 1))];
-      R = make_double2(0.5 * (Y1.x + Y2.x), 0.5 * (Y1.y + Y2.y));  // (Ra, Rb)
-      I = make_double2(0.5 * (Y2.y - Y1.y), 0.5 * (Y1.x - Y2.x));  // (Ia, Ib)
-      if (k == 0) R = make_double2(0.5 * R.x, 0.5 * R.y);
-    }
-    run = make_double2(run.x + R.x, run.y + R.y);
-    Rv[q] = run;  // inclusive prefix within the thread's block
-    Iv[q] = I;
-  }
-  // team-wide exclusive scan of the block totals
-  double2 off = make_double2(0.0, 0.0);
-  {
-    constexpr int W = TS < 32 ? TS : 32;
-    const int lane = threadIdx.x & 31;
-    double2 inc = run;
-#pragma unroll
-    for (int d = 1; d < W; d <<= 1) {
-      const double ux = __shfl_up_sync(0xffffffffu, inc.x, d, W);
-      const double uy = __shfl_up_sync(0xffffffffu, inc.y, d, W);
-      if ((lane % W) >= d) {
-        inc.x += ux;
-        inc.y += uy;
-      }
-    }
-    off = make_double2(inc.x - run.x, inc.y - run.y);
-    if (TS > 32) {  // combine the warps of a team
-      wsum[threadIdx.x] = inc;
-      __syncthreads();
-      const int w0 = (threadIdx.x / 32) * 32;  // first thread of this warp
-      for (int w = team * TS + 31; w < w0; w += 32) {
-        off.x += wsum[w].x;
-        off.y += wsum[w].y;
-      }
-    }
-  }
-  __syncthreads();  // every Y read is done; X is reused for the outputs
-#pragma unroll
-  for (int q = 0; q < KB; ++q) {
-    const int k = tt * KB + q;
-    if (k >= N / 2) continue;
-    if (k >= 1) X[dst_pad(2 * k)] = Iv[q];                               // X_{2k}
-    X[dst_pad(2 * k + 1)] = make_double2(off.x + Rv[q].x, off.y + Rv[q].y);  // X_{2k+1}
-  }
-  __syncthreads();
-
-  // ---- store: X_{j+1} of both lines of the pair
-  constexpr int OUT_ALL = F * n1;
-#pragma unroll 4
-  for (int e = threadIdx.x; e < OUT_ALL; e += BLK) {
-    int f, j;
-    if (stride == 1) {
-      f = e / n1;
-      j = e - f * n1;
-    } else {
-      j = e / F;
-      f = e - j * F;
-    }
-    const double2 Z = sm[f * BUF + dst_pad(j + 1)];
-    const double va = Z.x * scale, vb = Z.y * scale;
-    if (2 * f < nt) {
-      const i64 addr = lbase[2 * f] + i64(j) * stride;
-      if (accumulate) out[addr] += alpha * va;
-      else __stcs(out + addr, va);
-    }
-    if (2 * f + 1 < nt) {
-      const i64 addr = lbase[2 * f + 1] + i64(j) * stride;
-      if (accumulate) out[addr] += alpha * vb;
-      else __stcs(out + addr, vb);
-    }
-  }
-}
-
 // STRIDED: lines along y / z (element stride = `stride`, the F line pairs of a
 // CTA are 2F adjacent x columns); ACC: out += alpha * DST(in).  Both are
 // template parameters and every (pair, index) decomposition below is written
 // out for the thread (no per-item divisions, 64-bit multiplies or line-base
-// reloads): the v1 kernel spent 40 % of its instructions in the store loop
+// reloads): the round-1 kernel spent 40 % of its instructions in the store loop
 // and 18 % in the load loop on index arithmetic (ncu source view, C3).
 template <int LOG2N, bool STRIDED, bool ACC>
 __global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK, (LOG2N >= 4 ? STMG_DST_MINB : 1)) k_dst_lines(
@@ -4094,10 +3938,6 @@ cudaError_t launch_dst_axis(const LevelView& L, int axis, const double* in, doub
       k_dst_dense64<true><<<g, 128, 0, st>>>(in, out, n_lines, stride, alpha, accumulate ? 1 : 0);
     return cudaGetLastError();
   }
-  static const bool v1 = [] {  // A/B: the round-1 kernel
-    const char* e = std::getenv("STMG_DST_V1");
-    return e && std::atoi(e) != 0;
-  }();
   switch (log2n) {
 #define STMG_DST_LAUNCH(K, STR, AC)                                                         \
   {                                                                                        \
@@ -4112,14 +3952,7 @@ cudaError_t launch_dst_axis(const LevelView& L, int axis, const double* in, doub
   case K: {                                                                                \
     using SH = DSTShape<K>;                                                                \
     const unsigned grid = unsigned((n_lines + SH::TL - 1) / SH::TL);                       \
-    if (v1) {                                                                              \
-      static PerDevice attr_set;                                                           \
-      if (attr_set.first_use())                                                            \
-        cudaFuncSetAttribute(k_dst_lines_v1<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             int(SH::smem));                                               \
-      k_dst_lines_v1<K><<<grid, SH::BLOCK, SH::smem, st>>>(in, out, n_lines, stride, scale,  \
-                                                         alpha, accumulate ? 1 : 0, tw);   \
-    } else if (stride == 1) {                                                              \
+    if (stride == 1) {                                                                     \
       if (accumulate) STMG_DST_LAUNCH(K, false, true) else STMG_DST_LAUNCH(K, false, false) \
     } else {                                                                               \
       if (accumulate) STMG_DST_LAUNCH(K, true, true) else STMG_DST_LAUNCH(K, true, false)  \
@@ -4597,13 +4430,17 @@ cudaError_t launch_smooth(const LevelView& L, ModalArgs& a, bool zero_guess, con
 }
 
 cudaError_t launch_resnorm(const LevelView& L, ModalArgs& a, const double* u, const double* f,
-                           double* partials, cudaStream_t st) {
+                           double* partials, cudaStream_t st, bool u_zero) {
   const SP s = make_sp(L.sp);
   const dim3 grid(grid1(L.sp.nx, 128), unsigned((L.n_t + a.chunk - 1) / a.chunk));
   a.n_partials = i64(grid.x) * grid.y;
   STMG_DISPATCH(L.sp.dim, L.tc.nl, {
-    PDLK(k_resnorm<DIM, NL>, grid, 128, 0, st, u, f, partials, make_tm<NL>(L.tc), s, L.n_t, a.chunk,
-                                            L.first_global);
+    if (u_zero)
+      PDLK(k_resnorm<DIM, NL, true>, grid, 128, 0, st, u, f, partials, make_tm<NL>(L.tc), s, L.n_t,
+                                                    a.chunk, L.first_global);
+    else
+      PDLK(k_resnorm<DIM, NL, false>, grid, 128, 0, st, u, f, partials, make_tm<NL>(L.tc), s, L.n_t,
+                                                     a.chunk, L.first_global);
   });
   return cudaGetLastError();
 }

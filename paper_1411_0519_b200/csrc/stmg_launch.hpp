@@ -124,8 +124,10 @@ cudaError_t launch_updown(const LevelView& L, ModalArgs& a, const double* ec,
                           double* const* tbl, const int* par, const double* f, double* fc,
                           double* partials, cudaStream_t st, int64_t s0 = 0);
 // Residual sum-of-squares partials of f - L u.
+// u_zero: the iterate is known to be zero (u is not read; same partials).
 cudaError_t launch_resnorm(const LevelView& L, ModalArgs& a, const double* u,
-                           const double* f, double* partials, cudaStream_t st);
+                           const double* f, double* partials, cudaStream_t st,
+                           bool u_zero = false);
 
 // Chunk length heuristic for the modal kernels at a level.
 int pick_chunk(const LevelView& L, bool grouped);
