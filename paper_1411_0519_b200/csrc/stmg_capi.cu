@@ -186,6 +186,7 @@ struct stmg_ctx {
   bool capturing = false;
   i64 captured_kernels = 0;
   cudaEvent_t ev_solve[2] = {nullptr, nullptr};
+  cudaEvent_t ev_host = nullptr;  // host waits for a mapped word, not for the whole stream
   // single-CTA coarse tail (levels >= tail_start), built on first solve
   void* tail_table = nullptr;
   void* tail_host = nullptr;
@@ -1180,7 +1181,8 @@ void ensure_hist(stmg_ctx* c, int n) {
 }
 
 // Residual norm of the spectral iterate at level 0 (synchronising).
-double spectral_resnorm(stmg_ctx* c, int level, bool u_zero = false) {
+// Enqueue only: the norm lands in d_norm and (mapped) h_norm; ev_host marks it.
+void spectral_resnorm_async(stmg_ctx* c, int level, bool u_zero) {
   Level& L = c->levels[level];
   stmg::ModalArgs a = modal_args(L, nullptr, 0.5, false);
   CK(stmg::launch_resnorm(L.view, a, L.U[c->cur[level]].base, L.F.base, c->partials.base,
@@ -1188,7 +1190,12 @@ double spectral_resnorm(stmg_ctx* c, int level, bool u_zero = false) {
   CK(stmg::launch_norm_final(c->partials.base, a.n_partials, c->d_norm, nullptr, 0, c->stream));
   count(c, 2);
   tiny(c, {to_host(c->h_norm, c->d_norm, 8)});
-  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaEventRecord(c->ev_host, c->stream));
+}
+
+double spectral_resnorm(stmg_ctx* c, int level, bool u_zero = false) {
+  spectral_resnorm_async(c, level, u_zero);
+  CK(cudaEventSynchronize(c->ev_host));
   return *c->h_norm;
 }
 
@@ -1371,19 +1378,23 @@ void fused_body(stmg_ctx* c, const stmg_cycle_config& cfg, i64* np, bool defer_n
 
 // Runs the cycles of a solve whose finest iterate is in U0[0] (r0 known and
 // > 0); leaves the result in U0[c->cur[0]].  Fills r and history.
+// prefix of the fused schedule: pre-smooth + restriction of cycle 1 into U0[1], F1
+void fused_prefix(stmg_ctx* c, const stmg_cycle_config& cfg, bool u_zero) {
+  Level& L = c->levels[0];
+  Level& C = c->levels[1];
+  stmg::ModalArgs a = modal_args(L, &C, cfg.omega_t, true);
+  CK(stmg::launch_down(L.view, a, u_zero, L.F.base, L.U[0].base, L.U[1].base, C.F.base,
+                       c->stream));
+  count(c);
+}
+
 void run_fused(stmg_ctx* c, const stmg_cycle_config& cfg, double eps, int max_iter,
                double* history, int history_cap, int* nh, stmg_solve_report& r,
-               bool u_zero) {
+               bool u_zero, bool prefix_done = false) {
   Level& L = c->levels[0];
   Level& C = c->levels[1];
   ensure_hist(c, max_iter + 1);
-  // prefix: pre-smooth + restriction of cycle 1 into U0[1], F1
-  {
-    stmg::ModalArgs a = modal_args(L, &C, cfg.omega_t, true);
-    CK(stmg::launch_down(L.view, a, u_zero, L.F.base, L.U[0].base, L.U[1].base, C.F.base,
-                         c->stream));
-    count(c);
-  }
+  if (!prefix_done) fused_prefix(c, cfg, u_zero);
   tiny(c, {set8(c->d_pp, reinterpret_cast<unsigned long long>(L.U[0].base)),
            set8(c->d_pp + 1, reinterpret_cast<unsigned long long>(L.U[1].base)),
            set4(c->d_par, 1u), copy(c->d_r0, c->d_norm, 8), copy(c->d_hist, c->d_norm, 8),
@@ -1510,21 +1521,30 @@ void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config
     CK(stmg::launch_nonzero(u, L0.view.size(), c->d_flag, c->stream));
     count(c);
     tiny(c, {to_host(c->h_flag, c->d_flag, 4)});
+    CK(cudaEventRecord(c->ev_host, c->stream));
     dst_all(c, L0, f, L0.F.base);
-    CK(cudaStreamSynchronize(c->stream));
+    // the host reads the flag while the transform of f runs: no stream-wide
+    // synchronisation (and no idle GPU) before the next kernels are enqueued
+    CK(cudaEventSynchronize(c->ev_host));
     const bool u_zero = !*c->h_flag;
     if (!u_zero) dst_all(c, L0, u, L0.U[0].base);
     // zero guess: r0 = ||f|| from F alone (bitwise the general kernel's value)
-    const double r0 = spectral_resnorm(c, 0, u_zero);
+    spectral_resnorm_async(c, 0, u_zero);
+    // the fused schedule's prefix does not depend on r0: enqueue it before the
+    // host waits for r0 (if r0 turns out to be 0 its output is simply unused)
+    const bool may_fuse = fused_eligible(c, cfg) && max_iter > 0;
+    if (may_fuse) fused_prefix(c, cfg, u_zero);
+    CK(cudaEventSynchronize(c->ev_host));
+    const double r0 = *c->h_norm;
     r.r0 = r.r_final = r0;
     push(r0);
     if (r0 == 0.0) r.converged = 1;
-    const bool fused = fused_eligible(c, cfg) && !r.converged && max_iter > 0;
+    const bool fused = may_fuse && !r.converged;
     // the fused schedule's zero-guess prefix never reads U[0]; every other
     // path (and the immediate return when f == 0) needs the zero iterate there
     if (u_zero && !fused)
       CK(cudaMemsetAsync(L0.U[0].base, 0, size_t(L0.view.size()) * sizeof(double), c->stream));
-    if (fused) run_fused(c, cfg, eps, max_iter, history, history_cap, &nh, r, !*c->h_flag);
+    if (fused) run_fused(c, cfg, eps, max_iter, history, history_cap, &nh, r, u_zero, true);
     // the device-side loop needs the finest iterate back in its buffer after
     // a cycle; the per-cycle graph (kept for profiling) reports where it ends
     bool loop_ok = false;
@@ -2340,6 +2360,7 @@ int stmg_create(const stmg_hierarchy_params* p, stmg_ctx** out) {
     CK(cudaMallocHost(&c->h_iter, sizeof(int)));
     CK(cudaEventCreate(&c->ev_solve[0]));
     CK(cudaEventCreate(&c->ev_solve[1]));
+    CK(cudaEventCreateWithFlags(&c->ev_host, cudaEventDisableTiming));
     for (auto& s : c->prof) {
       CK(cudaEventCreate(&s.ga));
       CK(cudaEventCreate(&s.gb));
@@ -2402,6 +2423,7 @@ int stmg_destroy(stmg_ctx* c) {
     }
     cudaEventDestroy(c->ev_solve[0]);
     cudaEventDestroy(c->ev_solve[1]);
+    if (c->ev_host) cudaEventDestroy(c->ev_host);
     cudaFree(c->d_norm);
     cudaFree(c->d_hist);
     cudaFree(c->d_flag);

@@ -1875,22 +1875,36 @@ __global__ void __launch_bounds__(128) k_resnorm(const double* __restrict__ u,
 #pragma unroll
     for (int l = 0; l < NL; ++l) up[l] = 0.0;
     if (!ZERO && (n0 > 0 || !first_global)) load_nl<NL>(u + (n0 - 1) * slab + r, nx, up);
-    for (i64 m = n0; m < nend; ++m) {
-      double uv[NL], fv[NL], au[NL], np[NL];
-      if (ZERO) {
+    // UB steps per batch: all loads of a batch are issued before the first use
+    // (one load pair in flight per thread left this kernel latency bound:
+    // 67 us for the 66 MB of C2); the accumulation order is unchanged
+    constexpr int UB = NL <= 2 ? 8 : 4;
+    for (i64 m0 = n0; m0 < nend; m0 += UB) {
+      double uv[UB][NL], fv[UB][NL];
 #pragma unroll
-        for (int l = 0; l < NL; ++l) uv[l] = 0.0;
-      } else {
-        load_nl<NL>(u + m * slab + r, nx, uv);
+      for (int j = 0; j < UB; ++j) {
+        if (m0 + j < nend) {
+          if (!ZERO) load_nl<NL>(u + (m0 + j) * slab + r, nx, uv[j]);
+          load_nl<NL>(f + (m0 + j) * slab + r, nx, fv[j]);
+        }
       }
-      load_nl<NL>(f + m * slab + r, nx, fv);
-      apply_mode<NL>(t, Mj, Kj, uv, au);
-      matvec<NL>(t.N, up, np);
 #pragma unroll
-      for (int l = 0; l < NL; ++l) {
-        const double res = fv[l] - au[l] + Mj * np[l];
-        sumsq += res * res;
-        up[l] = uv[l];
+      for (int j = 0; j < UB; ++j) {
+        if (m0 + j < nend) {
+          double au[NL], np[NL];
+          if (ZERO) {
+#pragma unroll
+            for (int l = 0; l < NL; ++l) uv[j][l] = 0.0;
+          }
+          apply_mode<NL>(t, Mj, Kj, uv[j], au);
+          matvec<NL>(t.N, up, np);
+#pragma unroll
+          for (int l = 0; l < NL; ++l) {
+            const double res = fv[j][l] - au[l] + Mj * np[l];
+            sumsq += res * res;
+            up[l] = uv[j][l];
+          }
+        }
       }
     }
   }
@@ -2919,7 +2933,13 @@ struct DSTShape {
   static constexpr int L = N;
   static constexpr int V = L >= 16 ? 16 : L;
   static constexpr int TS = L / V;  // threads per FFT (team)
-  static constexpr int BLOCK = TS > 128 ? TS : 128;
+#ifndef STMG_DST_BLOCK9
+#define STMG_DST_BLOCK9 256  // A/B vs 128: C5 transform 11.9-12.8 -> 11.5-11.9 ms (profiles/r02_v4_dst_lines_ab.txt)
+#endif
+  // N = 512: a 128-thread block holds only 4 line pairs = 8 adjacent columns
+  // (64 B per row) in a strided pass; STMG_DST_BLOCK9 = 256 doubles that
+  static constexpr int BLOCK0 = LOG2N == 9 ? STMG_DST_BLOCK9 : 128;
+  static constexpr int BLOCK = TS > BLOCK0 ? TS : BLOCK0;
   static constexpr int F = BLOCK / TS;  // FFTs (= line pairs) per block
   static constexpr int TL = 2 * F;      // lines per block
   // padded FFT buffer.  STMG_DST_BUFPAD = 1 makes BUF odd in 16-byte units
@@ -3001,7 +3021,7 @@ __device__ __forceinline__ void dst_passes(double2* X, const int tt,
 // reloads): the round-1 kernel spent 40 % of its instructions in the store loop
 // and 18 % in the load loop on index arithmetic (ncu source view, C3).
 template <int LOG2N, bool STRIDED, bool ACC>
-__global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK, (LOG2N >= 4 ? STMG_DST_MINB : 1)) k_dst_lines(
+__global__ void __launch_bounds__(DSTShape<LOG2N>::BLOCK, (LOG2N >= 4 ? (DSTShape<LOG2N>::BLOCK > 128 ? STMG_DST_MINB / 2 : STMG_DST_MINB) : 1)) k_dst_lines(
     const double* __restrict__ in, double* __restrict__ out, const i64 n_lines, const i64 stride,
     const double scale, const double alpha, const double2* __restrict__ tw) {
   using S = DSTShape<LOG2N>;
