@@ -1390,7 +1390,11 @@ void fused_prefix(stmg_ctx* c, const stmg_cycle_config& cfg, bool u_zero) {
 
 void run_fused(stmg_ctx* c, const stmg_cycle_config& cfg, double eps, int max_iter,
                double* history, int history_cap, int* nh, stmg_solve_report& r,
-               bool u_zero, bool prefix_done = false) {
+               bool u_zero, bool prefix_done = false, bool r0_deferred = false) {
+  // r0_deferred (zero guess, device loop): the host has not read r0; it comes
+  // back as history[0] with the loop's results, so the whole solve is enqueued
+  // without a host round trip.  r0 == 0 then means f == 0: the one cycle the
+  // loop ran worked on zeros and the report is the reference's (0 iterations).
   Level& L = c->levels[0];
   Level& C = c->levels[1];
   ensure_hist(c, max_iter + 1);
@@ -1459,13 +1463,19 @@ void run_fused(stmg_ctx* c, const stmg_cycle_config& cfg, double eps, int max_it
     CK(cudaStreamSynchronize(c->stream));
   }
   const std::vector<double> h(c->h_hist, c->h_hist + iters + 1);
+  if (r0_deferred) {
+    r.r0 = r.r_final = h[0];
+    if (history && *nh < history_cap) history[*nh] = h[0];
+    ++*nh;
+    if (h[0] == 0.0) iters = 0;
+  }
   for (int k = 1; k <= iters; ++k) {
     if (history && *nh < history_cap) history[*nh] = h[k];
     ++*nh;
   }
   r.iterations = iters;
   r.r_final = iters > 0 ? h[iters] : r.r0;
-  r.converged = (iters > 0 && h[iters] <= eps * r.r0) ? 1 : 0;
+  r.converged = ((iters > 0 && h[iters] <= eps * r.r0) || (r0_deferred && r.r0 == 0.0)) ? 1 : 0;
   // suffix: the last cycle's post-smooth from its (intact) inputs; after an
   // even number of cycles the last input A is U0[1], after an odd number U0[0]
   const int a_last = (iters % 2 == 1) ? 1 : 0;
@@ -1478,8 +1488,11 @@ void run_fused(stmg_ctx* c, const stmg_cycle_config& cfg, double eps, int max_it
   c->cur[0] = 1 - a_last;
 }
 
+// known_zero: the caller guarantees u == 0 on the device (it zeroed the buffer
+// itself): no k_nonzero pass and no flag round trip.
 void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config& cfg, double eps,
-                int max_iter, double* history, int history_cap, stmg_solve_report* rep) {
+                int max_iter, double* history, int history_cap, stmg_solve_report* rep,
+                bool known_zero = false) {
   require(eps > 0.0, "eps_mg must be positive");
   require(f != nullptr && u != nullptr, "null vector");
   require(max_iter >= 0, "max_iter must be >= 0");
@@ -1517,16 +1530,21 @@ void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config
     ensure_svc(c, cfg);
     c->cur[0] = 0;
     // a zero initial guess (the usual case) needs no transform
-    tiny(c, {set4(c->d_flag, 0u)});
-    CK(stmg::launch_nonzero(u, L0.view.size(), c->d_flag, c->stream));
-    count(c);
-    tiny(c, {to_host(c->h_flag, c->d_flag, 4)});
-    CK(cudaEventRecord(c->ev_host, c->stream));
-    dst_all(c, L0, f, L0.F.base);
-    // the host reads the flag while the transform of f runs: no stream-wide
-    // synchronisation (and no idle GPU) before the next kernels are enqueued
-    CK(cudaEventSynchronize(c->ev_host));
-    const bool u_zero = !*c->h_flag;
+    bool u_zero = true;
+    if (known_zero) {
+      dst_all(c, L0, f, L0.F.base);
+    } else {
+      tiny(c, {set4(c->d_flag, 0u)});
+      CK(stmg::launch_nonzero(u, L0.view.size(), c->d_flag, c->stream));
+      count(c);
+      tiny(c, {to_host(c->h_flag, c->d_flag, 4)});
+      CK(cudaEventRecord(c->ev_host, c->stream));
+      dst_all(c, L0, f, L0.F.base);
+      // the host reads the flag while the transform of f runs: no stream-wide
+      // synchronisation (and no idle GPU) before the next kernels are enqueued
+      CK(cudaEventSynchronize(c->ev_host));
+      u_zero = !*c->h_flag;
+    }
     if (!u_zero) dst_all(c, L0, u, L0.U[0].base);
     // zero guess: r0 = ||f|| from F alone (bitwise the general kernel's value)
     spectral_resnorm_async(c, 0, u_zero);
@@ -1534,17 +1552,22 @@ void solve_impl(stmg_ctx* c, const double* f, double* u, const stmg_cycle_config
     // host waits for r0 (if r0 turns out to be 0 its output is simply unused)
     const bool may_fuse = fused_eligible(c, cfg) && max_iter > 0;
     if (may_fuse) fused_prefix(c, cfg, u_zero);
-    CK(cudaEventSynchronize(c->ev_host));
-    const double r0 = *c->h_norm;
-    r.r0 = r.r_final = r0;
-    push(r0);
-    if (r0 == 0.0) r.converged = 1;
+    // zero guess + device loop: r0 is not needed on the host before the loop
+    const bool defer = may_fuse && u_zero && c->use_device_loop && !c->profile;
+    double r0 = 0.0;
+    if (!defer) {
+      CK(cudaEventSynchronize(c->ev_host));
+      r0 = *c->h_norm;
+      r.r0 = r.r_final = r0;
+      push(r0);
+      if (r0 == 0.0) r.converged = 1;
+    }
     const bool fused = may_fuse && !r.converged;
     // the fused schedule's zero-guess prefix never reads U[0]; every other
     // path (and the immediate return when f == 0) needs the zero iterate there
     if (u_zero && !fused)
       CK(cudaMemsetAsync(L0.U[0].base, 0, size_t(L0.view.size()) * sizeof(double), c->stream));
-    if (fused) run_fused(c, cfg, eps, max_iter, history, history_cap, &nh, r, u_zero, true);
+    if (fused) run_fused(c, cfg, eps, max_iter, history, history_cap, &nh, r, u_zero, true, defer);
     // the device-side loop needs the finest iterate back in its buffer after
     // a cycle; the per-cycle graph (kept for profiling) reports where it ends
     bool loop_ok = false;
@@ -2858,7 +2881,8 @@ int stmg_solve_host_batch(stmg_ctx* c, int count, const double* const* f_host,
       if (c->shards)
         solve_sharded(c, F[s]->base, U[s]->base, *cfg, eps, max_iter, nullptr, 0, &r);
       else
-        solve_impl(c, F[s]->base, U[s]->base, *cfg, eps, max_iter, nullptr, 0, &r);
+        solve_impl(c, F[s]->base, U[s]->base, *cfg, eps, max_iter, nullptr, 0, &r,
+                   /*known_zero=*/(u0_host ? u0_host[i] : u_host[i]) == nullptr);
       CK(cudaEventRecord(c->ev_done, c->stream));
       tmark(i, 3, c->stream);
       CK(cudaStreamWaitEvent(c->s_out, c->ev_done, 0));

@@ -12,6 +12,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1411_0519_b200 import _capi as A, stmg  # noqa: E402
 
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+zero = len(sys.argv) > 2 and sys.argv[2] == "zero"  # zero initial guess: nothing uploaded for u
 h = stmg.Hierarchy(1, 2, 6, 8)
 n = h.size(0)
 bufs = []
@@ -29,7 +30,7 @@ for rep in range(2):
     h.synchronize()
     t0 = time.perf_counter()
     reps = h.solve_host_batch([bufs[0][1]] * k, [outs[i % 3] for i in range(k)], cfg, 1e-8,
-                              u0s=[bufs[1][1]] * k)
+                              u0s=[None if zero else bufs[1][1]] * k)
     dt = time.perf_counter() - t0
     print(f"rep {rep}: {k} solves, {1e3 * dt / k:.3f} ms per solve, iterations "
           f"{[r.iterations for r in reps]}", file=sys.stderr, flush=True)
