@@ -698,6 +698,10 @@ cudaError_t launch_apply_rows(const LevelView& L, const double* u, const double*
   if (L.tc.nl > kFastNL || L.sp.dim < 2) return cudaErrorNotSupported;
   if (L.sp.n1 < (L.sp.dim == 2 ? 96 : 48)) return cudaErrorNotSupported;
   if ((reinterpret_cast<uintptr_t>(u) & 15) != 0) return cudaErrorNotSupported;
+  // the 16-byte rounded copy of the vector's last run would read one double
+  // past the end when the vector has an odd number of entries (n_t = 1 with an
+  // odd number of DG components): leave those to the tile kernels
+  if ((L.size() & 1) != 0) return cudaErrorNotSupported;
   if (residual && (reinterpret_cast<uintptr_t>(f) & 15) != 0) return cudaErrorNotSupported;
 #define STMG_ROWS_CASE(D, Q, R)                                           \
   case (D) * 16 + (Q) * 2 + (R):                                          \
