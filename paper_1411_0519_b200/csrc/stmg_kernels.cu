@@ -2499,8 +2499,13 @@ __global__ void __launch_bounds__(256) k_restrict(const double* __restrict__ fin
   }
 }
 
-// prolong_semi / prolong_full (transfer.cpp:87-96, 151-158): one thread per
-// fine (step, node); linear interpolation per axis, U_2n = C_n R1, U_2n+1 = C_n R2.
+// prolong_semi / prolong_full (transfer.cpp:87-96, 151-158): linear
+// interpolation per axis, U_2n = C_n R1, U_2n+1 = C_n R2.  One thread per fine
+// node and COARSE step: it gathers the interpolated coarse value once and
+// writes both fine steps (the round-1 kernel gathered per fine step through
+// divergent neighbour loops: 0.8-1.3 TB/s).  The 2^DIM neighbour slots are
+// uniform -- an absent neighbour is a clamped index with weight 0 -- and are
+// visited in the old (z, y, x) order, so the sums are unchanged.
 template <int DIM, int NL, int CO>
 __global__ void __launch_bounds__(256) k_prolong(const double* __restrict__ coarse,
                                                  double* __restrict__ fine, const TM<NL> t,
@@ -2510,63 +2515,68 @@ __global__ void __launch_bounds__(256) k_prolong(const double* __restrict__ coar
   if (r >= nx) return;
   int c[3];
   coords<DIM>(r, unsigned(n1), c);
-  for (i64 n = blockIdx.y; n < n_t; n += gridDim.y) {
-  const i64 nc = n >> 1;
-  double cv[NL];
+  // per axis: two coarse slots (index, weight)
+  int j[3][2];
+  double w[3][2];
 #pragma unroll
-  for (int l = 0; l < NL; ++l) cv[l] = 0.0;
-  const double* src = coarse + nc * NL * nxc;
-  if (CO == 1) {
+  for (int a = 0; a < 3; ++a) {
+    j[a][0] = j[a][1] = 0;
+    w[a][0] = 1.0;
+    w[a][1] = 0.0;
+    if (a >= DIM || CO == 1) continue;
+    const int i = c[a], jj = i / 2;
+    if (i % 2 == 1) {
+      j[a][0] = jj;
+    } else {  // between coarse nodes jj - 1 and jj (either may be the boundary)
+      j[a][0] = jj > 0 ? jj - 1 : 0;
+      w[a][0] = jj > 0 ? 0.5 : 0.0;
+      j[a][1] = jj < n1c ? jj : int(n1c) - 1;
+      w[a][1] = jj < n1c ? 0.5 : 0.0;
+    }
+  }
+  i64 rc[1 << DIM];
+  double ww[1 << DIM];
 #pragma unroll
-    for (int k = 0; k < NL; ++k) cv[k] = __ldg(src + k * nxc + r);
-  } else {
-    // per axis: up to two coarse neighbours with weights
-    int j[3][2];
-    double w[3][2];
-    int cnt[3];
+  for (int q = 0; q < (1 << DIM); ++q) {
+    const int ix = q & 1, iy = DIM > 1 ? (q >> 1) & 1 : 0, iz = DIM > 2 ? (q >> 2) & 1 : 0;
+    ww[q] = w[0][ix] * w[1][iy] * w[2][iz];
+    rc[q] = (i64(j[2][iz]) * n1c + j[1][iy]) * n1c + j[0][ix];
+  }
+  // a thread keeps its slots for a run of coarse steps (the index arithmetic
+  // above costs more than one step's gathers)
+  const i64 ntc = n_t >> 1;
+  const i64 per = (ntc + gridDim.y - 1) / gridDim.y;
+  const i64 nc0 = i64(blockIdx.y) * per, nc1 = min(nc0 + per, ntc);
+#pragma unroll 2
+  for (i64 nc = nc0; nc < nc1; ++nc) {
+    double cv[NL];
+    const double* src = coarse + nc * NL * nxc;
+    if (CO == 1) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      cnt[a] = 1;
-      j[a][0] = 0;
-      w[a][0] = 1.0;
-      j[a][1] = 0;
-      w[a][1] = 0.0;
-      if (a >= DIM) continue;
-      const int i = c[a];
-      if (i % 2 == 1) {
-        j[a][0] = i / 2;
-      } else {
-        const int jj = i / 2;
-        cnt[a] = 0;
-        if (jj > 0) {
-          j[a][cnt[a]] = jj - 1;
-          w[a][cnt[a]] = 0.5;
-          ++cnt[a];
-        }
-        if (jj < n1c) {
-          j[a][cnt[a]] = jj;
-          w[a][cnt[a]] = 0.5;
-          ++cnt[a];
+      for (int k = 0; k < NL; ++k) cv[k] = __ldg(src + k * nxc + r);
+    } else {
+#pragma unroll
+      for (int k = 0; k < NL; ++k) cv[k] = 0.0;
+      // a zero-weight slot is skipped like the absent neighbour it stands for
+      // (w is exactly 0 or 0.5^m: the test is exact)
+#pragma unroll
+      for (int q = 0; q < (1 << DIM); ++q) {
+        if (ww[q] != 0.0) {
+#pragma unroll
+          for (int k = 0; k < NL; ++k) cv[k] += ww[q] * __ldg(src + k * nxc + rc[q]);
         }
       }
     }
-    for (int iz = 0; iz < cnt[2]; ++iz)
-      for (int iy = 0; iy < cnt[1]; ++iy)
-        for (int ix = 0; ix < cnt[0]; ++ix) {
-          const double ww = w[0][ix] * w[1][iy] * w[2][iz];
-          const i64 rc = (i64(j[2][iz]) * n1c + j[1][iy]) * n1c + j[0][ix];
+    double* o = fine + (2 * nc) * NL * nx + r;
 #pragma unroll
-          for (int k = 0; k < NL; ++k) cv[k] += ww * __ldg(src + k * nxc + rc);
-        }
-  }
-  double* o = fine + n * NL * nx + r;
+    for (int e = 0; e < 2; ++e)
 #pragma unroll
-  for (int l = 0; l < NL; ++l) {
-    double s = 0.0;
+      for (int l = 0; l < NL; ++l) {
+        double sacc = 0.0;
 #pragma unroll
-    for (int k = 0; k < NL; ++k) s += cv[k] * ((n & 1) ? t.R2[k][l] : t.R1[k][l]);
-    o[l * nx] = s;
-  }
+        for (int k = 0; k < NL; ++k) sacc += cv[k] * (e ? t.R2[k][l] : t.R1[k][l]);
+        __stcs(o + (e * NL + l) * nx, sacc);
+      }
   }
 }
 
@@ -3907,7 +3917,12 @@ cudaError_t launch_prolong(const LevelView& F, int mode, int64_t n1c, const doub
     });
     return cudaGetLastError();
   }
-  const dim3 g = grid2(F.sp.nx, F.n_t, 256);
+  // one thread per fine node and run of coarse steps: ~8 steps per thread, but
+  // at least ~16 CTAs per SM in the grid
+  const i64 ntc = F.n_t / 2, bx = grid1(F.sp.nx, 256);
+  i64 gy = std::max<i64>((ntc + 7) / 8, std::min<i64>(ntc, (148 * 16 + bx - 1) / bx));
+  gy = std::max<i64>(1, std::min<i64>(gy, 65535));
+  const dim3 g{unsigned(bx), unsigned(gy), 1u};
   STMG_DISPATCH(F.sp.dim, F.tc.nl, {
     const TM<NL> t = make_tm<NL>(F.tc);
     if (mode == 2)
