@@ -34,6 +34,31 @@ for name in (sys.argv[1:] or ["C2"]):
         dt = (time.perf_counter() - t0) / 5
         out[nm] = {"ms": dt * 1e3, "alg_GBps": 8.0 * (n0 + c.n) / dt / 1e9}
     del c, fine
+    # semi-coarsening variants (time only), norm, forward substitution
+    c1 = h.coarse_vector(0, 1)
+    fine = h.vector(0)
+
+    def timed(fn, reps=5):
+        fn()
+        h.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        h.synchronize()
+        return (time.perf_counter() - t0) / reps
+
+    dt = timed(lambda: A.check(A.lib().stmg_restrict(h._ctx, 0, 1, f.ptr, c1.ptr)))
+    out["restrict_semi"] = {"ms": dt * 1e3, "alg_GBps": 8.0 * (n0 + c1.n) / dt / 1e9}
+    dt = timed(lambda: A.check(A.lib().stmg_prolong(h._ctx, 0, 1, c1.ptr, fine.ptr)))
+    out["prolong_semi"] = {"ms": dt * 1e3, "alg_GBps": 8.0 * (n0 + c1.n) / dt / 1e9}
+    dt = timed(lambda: h.norm(0, f))
+    out["norm"] = {"ms": dt * 1e3, "alg_GBps": 8.0 * n0 / dt / 1e9}
+    last = len(h.levels) - 1
+    fl = h.vector(last)
+    h.fill_uniform(fl, SEED, 3)
+    dt = timed(lambda: h.forward_substitution_solve(last, fl))
+    out["forward_substitution_coarsest"] = {"ms": dt * 1e3, "dofs": fl.n}
+    del c1, fine, fl
     if name == "C2":
         u = h.vector(0)
         for path in ("spectral", "physical"):
