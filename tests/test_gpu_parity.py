@@ -493,3 +493,32 @@ def test_row_band_residual_matches_oracle(S, case):
     du, df = g.upload(u, 0), g.upload(f, 0)
     assert rel(g.apply(0, du).numpy(), o.apply(0, u)) < 1e-12
     assert rel(g.residual(0, du, df).numpy(), o.residual(0, u, f)) < 1e-12
+    # transfers at the same sizes (k_restrict / the round-2 k_prolong)
+    if o.levels[0].coarsen_to_next:
+        for mode in (1, 2):
+            rc = g.restrict(0, du, mode).numpy()
+            assert rel(rc, o.restrict(0, u, mode)) < 1e-13
+            c = O.fill_uniform(rc.size, 500 + sl, 0)
+            dc = g.coarse_vector(0, mode).copy_from(c)
+            assert rel(g.prolong(0, dc, mode).numpy(), o.prolong(0, c, mode)) < 1e-13
+
+
+@pytest.mark.parametrize("case", [(1, 2, 6, 3), (2, 2, 6, 2), (1, 3, 5, 2)])
+def test_physical_path_cycle_on_row_band_sizes(S, case):
+    """Two V-cycles through the reference call structure (physical path:
+    residual, exact block solves, transfers as separate operators) on grids
+    where level 0 runs the row-band residual and the one-pass / dense
+    transforms; 1e-10 per cycle against the oracle."""
+    p, dim, sl, tl = case
+    g, o = pair(S, p, dim, sl, tl, 1.0)
+    f = O.fill_uniform(o.levels[0].size, 11, 0)
+    df = g.upload(f)
+    u = np.zeros_like(f)
+    du = g.upload(u)
+    cfg = S.CycleConfig(nu1=1, nu2=1, gamma=1, omega_t=0.5, path="physical")
+    for k in range(2):
+        u = o.mg_cycle(0, u, f, 1, 1, 1, 0.5)
+        g.mg_cycle(0, du, df, cfg)
+        assert rel(du.numpy(), u) < 1e-10, k
+    us = g.block_jacobi_step(0, g.upload(u), df, 0.5, 1).numpy()
+    assert rel(us, o.smooth(0, u, f, 0.5, 1)) < 1e-11
