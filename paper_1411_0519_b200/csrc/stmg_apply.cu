@@ -21,10 +21,18 @@
 //  * the CTA marches through a chunk of time steps, NS slabs in flight, the
 //    rank-one jump term reusing the previous step's M-traces from registers,
 //    so u and f are read once and r is written once (24 B per dof);
-//  * f is loaded straight into registers one whole step ahead (each register
-//    is reloaded as soon as its value is consumed).
-// The per-output operation order is that of k_apply, so both kernels give
-// bitwise identical results.
+//  * warp specialisation: one producer warp waits on per-stage "empty"
+//    mbarriers and issues the copies of the next slab (u rows and the band's f
+//    rows) against the stage's "full" mbarrier; the consumer warps never meet
+//    in a CTA-wide barrier.  (A first version loaded f straight into registers
+//    one step ahead and reloaded each register right after its use: every
+//    later use then waited for the fresh load on the shared scoreboard --
+//    48 % of the stall samples -- which is why f goes through the stage.)
+//  * CTAs whose band and halo lie inside the grid run a variant without any
+//    range tests; time chunks are balanced and their number is rounded to a
+//    whole number of waves of resident CTAs.
+// Results agree with the tile kernels to rounding (the DG-block combination is
+// an FMA chain here); parity with the CPU oracle: 1e-12 (tests/test_gpu_parity.py).
 #include <atomic>
 #include <cstdlib>
 #include <type_traits>
