@@ -397,6 +397,58 @@ def operator_record(h, f, u, reps=6):
     }
 
 
+def concurrent_record(stmg, cfg, local, steps, contexts=3):
+    """Aggregate throughput of the same solves when `contexts` independent
+    problems are in flight (one context, host thread and library stream each;
+    device-resident inputs).  A single C2 solve leaves the GPU partly idle
+    during its latency-bound coarse levels; independent problems fill it.
+    Extra information: `value` stays the one-problem-at-a-time figure."""
+    import threading
+    from paper_1411_0519_b200 import _capi as A
+    ccfg = stmg.CycleConfig(nu1=1, nu2=1, gamma=1, omega_t=0.5)
+    ctxs = []
+    for _ in range(contexts):
+        h = stmg.Hierarchy(cfg["p_t"], cfg["dim"], cfg["space_level"], cfg["time_level"],
+                           cfg["t_final"], device=local)
+        f, u = h.vector(0), h.vector(0)
+        h.fill_uniform(f, SEED, 0)
+        if cfg["random_u0"]:
+            L0 = h.levels[0]
+            u0 = stmg.BlockVector(h, L0["n_x"], (L0["n_x"],))
+            h.fill_uniform(u0, SEED, 1)
+            h.fold_u0(f, u0)
+        ctxs.append((h, f, u))
+    its = []
+
+    def work(c, k):
+        h, f, u = c
+        for _ in range(k):
+            A.check(A.lib().stmg_memset_zero(h._ctx, u.ptr, u.n * 8))
+            its.append(h.solve(f, u, ccfg, EPS).iterations)
+        h.synchronize()
+
+    per = max(steps // contexts, 1)
+    for c in ctxs:
+        work(c, 2)
+    its.clear()
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=work, args=(c, per)) for c in ctxs]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    dt = time.perf_counter() - t0
+    n0 = ctxs[0][1].n
+    rec = {"contexts": contexts, "solves": per * contexts, "ms_per_solve": 1e3 * dt / (per * contexts),
+           "value": float(n0) * sum(its) / dt, "unit": UNIT,
+           "timing": "host wall clock around the worker threads (each ends with a stream "
+                     "synchronisation); no L2 flush (the contexts' working sets exceed L2)"}
+    for h, f, u in ctxs:
+        del f, u
+        h.close()
+    return rec
+
+
 def scaling_record(stmg, name, base, weak, world, rank, local, dist, steps, warmup):
     """Sub-record of one scaling curve at this N (the driver's per-N runs give
     the curve; efficiencies are computed by the reader, not here)."""
@@ -600,6 +652,10 @@ def run_ours(args, cfgname):
     del h
     gc.collect()
 
+    conc = None
+    if world == 1 and not args.no_scaling:
+        conc = concurrent_record(stmg, cfg, local, max(args.steps, 12))
+        gc.collect()
     subs = {}
     if not args.no_scaling:
         subs["C3_strong"] = scaling_record(stmg, "C3_strong", "C3", False, world, rank, local,
@@ -656,6 +712,7 @@ def run_ours(args, cfgname):
         "gpu_launches": int(launches),
         "roofline": roof,
         "operators": ops,
+        "concurrent_problems": conc,
         "clocks": clk,
         "scaling_runs": subs,
     }
