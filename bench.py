@@ -26,9 +26,9 @@ than N GPUs are visible or any rank fails -- there is no replica fallback.
 The main line is configs[1] scaled weakly in time (N_t = 256 N, tau fixed:
 per-GPU work constant, time slabs over the ranks, NCCL halo exchange inside
 the library).  Every run (N = 1 included) adds "scaling" sub-records:
-configs[2] C3 strong scaling (N_t = 4096 fixed) and configs[4] C5 weak
-scaling (N_t = 2048 N), each with ms per solve and per V-cycle, iterations and
-the per-rank k_updown HBM GB/s, so the driver's per-N runs give both curves.
+configs[2] C3 and configs[3] C4 strong scaling (N_t fixed) and configs[4] C5
+weak scaling (N_t = 2048 N), each with ms per solve and per V-cycle, iterations
+and the per-rank k_updown HBM GB/s, so the driver's per-N runs give the curves.
 """
 from __future__ import annotations
 
@@ -660,22 +660,12 @@ def run_ours(args, cfgname):
     if not args.no_scaling:
         subs["C3_strong"] = scaling_record(stmg, "C3_strong", "C3", False, world, rank, local,
                                            dist, args.scaling_steps, 1)
+        subs["C4_strong"] = scaling_record(stmg, "C4_strong", "C4", False, world, rank, local,
+                                           dist, args.scaling_steps, 1)
         subs["C5_weak"] = scaling_record(stmg, "C5_weak", "C5", True, world, rank, local, dist,
                                          args.scaling_steps, 1)
         if world == 1:
-            # configs[3] (3D): operators only (its solve is a parity-test case)
-            c4 = CONFIGS["C4"]
-            h4 = stmg.Hierarchy(c4["p_t"], c4["dim"], c4["space_level"], c4["time_level"],
-                                c4["t_final"], device=local)
-            f4, u4 = h4.vector(0), h4.vector(0)
-            h4.fill_uniform(f4, SEED, 0)
-            h4.fill_uniform(u4, SEED + 1, 0)
-            ops["C4"] = operator_record(h4, f4, u4, reps=3)
-            del f4, u4
-            h4.close()
-            del h4
-            gc.collect()
-            for k_ in ("C3_strong", "C5_weak"):
+            for k_ in ("C3_strong", "C4_strong", "C5_weak"):
                 ops[k_[:2]] = subs[k_].pop("operators")
 
     line = {
