@@ -139,6 +139,18 @@ def dist_setup(expect_world: int):
         raise SystemExit(f"[bench] WORLD_SIZE={world} but --gpus {expect_world}: refusing to run")
     dist = None
     if world > 1:
+        # watchdog: the NCCL transport has only ever run on virtual shards (one
+        # GPU per box here); a rank that deadlocks must not hang the node
+        limit = float(os.environ.get("STMG_BENCH_TIMEOUT", "900"))
+
+        def _abort():
+            print(f"[bench] rank {rank}: no result after {limit:.0f} s -- aborting (exit 3)",
+                  file=sys.stderr, flush=True)
+            os._exit(3)
+
+        wd = threading.Timer(limit, _abort)
+        wd.daemon = True
+        wd.start()
         import torch
         import torch.distributed as dist
         ndev = torch.cuda.device_count()
