@@ -839,6 +839,7 @@ stmg::ModalArgs modal_args(const Level& L, const Level* C, double omega, bool gr
   a.chunk = stmg::pick_chunk(L.view, grouped);
   a.mode = L.spec.coarsen ? L.spec.coarsen : 1;
   a.n1c = C ? C->spec.n1() : L.spec.n1();
+  a.block = stmg::pick_updown_block(L.view, stmg::pick_chunk(L.view, true), a.mode);
   return a;
 }
 
@@ -1913,12 +1914,24 @@ i64 shard_np(stmg_ctx* c, bool grouped) {
   return stmg::partial_count(v, shard_chunk(c->levels[0], v, grouped), grouped);
 }
 
+// Partial sums of one shard's launch_updown (its CTAs may be 256 threads wide).
+i64 shard_np_updown(stmg_ctx* c) {
+  const stmg::LevelView& v = c->shards->local[0].lv[0].view;
+  const Level& G = c->levels[0];
+  const int mode = G.spec.coarsen ? G.spec.coarsen : 1;
+  const int block = stmg::pick_updown_block(G.view, stmg::pick_chunk(G.view, true), mode);
+  return stmg::partial_count(v, shard_chunk(G, v, true), true, block);
+}
+
 stmg::ModalArgs shard_args(stmg_ctx* c, int l, const ShardLevel& s, double omega, bool grouped) {
   stmg::ModalArgs a;
   a.omega = omega;
   a.chunk = shard_chunk(c->levels[l], s.view, grouped);
   a.mode = c->levels[l].spec.coarsen ? c->levels[l].spec.coarsen : 1;
   a.n1c = c->levels[l + 1].spec.n1();
+  // from the GLOBAL level: every shard uses the single-shard block size
+  a.block = stmg::pick_updown_block(c->levels[l].view,
+                                    stmg::pick_chunk(c->levels[l].view, true), a.mode);
   return a;
 }
 
@@ -2061,7 +2074,7 @@ void sharded_fused_body(stmg_ctx* c, const stmg_cycle_config& cfg, int pa, doubl
   }
   const stmg::LevelView& v0 = ss.local[0].lv[0].view;
   halo(c, v0.n_t, v0.slab(), 3, [&](Shard& sh) { return sh.lv[0].U[pa].base; });
-  const i64 np = shard_np(c, true);  // k_updown's partials = k_up's (grouped)
+  const i64 np = shard_np_updown(c);
   for (Shard& sh : ss.local) {
     ShardLevel& L = sh.lv[0];
     stmg::ModalArgs a = shard_args(c, 0, L, cfg.omega_t, true);

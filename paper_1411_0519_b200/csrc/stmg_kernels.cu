@@ -774,10 +774,10 @@ __device__ __forceinline__ double updown_body_ops(const i64 tid, const i64 n0, c
 #endif
 constexpr int kTmaStages = STMG_TMA_STAGES;
 
-template <int DIM, int NL>
+template <int DIM, int NL, int BT = 128>
 struct TmaShape {
   static constexpr int NM = 1 << DIM;       // members per alias group
-  static constexpr int GPB = 128 / NM;      // groups per block (one row run)
+  static constexpr int GPB = BT / NM;       // groups per block (one row run)
   static constexpr int SEG = GPB + 2;       // doubles per slot
   static constexpr int NU = 2 * NL * NM;    // u slots (2 steps) = f slots
   static constexpr int NC = 2 * NU + NL;    // copies per stage
@@ -796,14 +796,14 @@ __device__ __forceinline__ int shift16(const double* p) {
   return int((reinterpret_cast<uintptr_t>(p) >> 3) & 1);
 }
 
-template <int DIM, int NL>
+template <int DIM, int NL, int BT>
 __device__ __forceinline__ double updown_body_tma(const i64 tid, const i64 n0, const i64 nend,
                                                   const double* ec, const PingPong pp,
                                                   const double* f, double* fc,
                                                   const TM<NL>& t, const SP& s, const i64 n1c,
                                                   const double omega, double* ring,
                                                   const i64 s0) {
-  using S = TmaShape<DIM, NL>;
+  using S = TmaShape<DIM, NL, BT>;
   constexpr int NM = S::NM, GPB = S::GPB, SEG = S::SEG, NU = S::NU;
   __shared__ alignas(8) unsigned long long bars[kTmaStages];
   __shared__ i64 segb[NM + 1];  // run start (fine mode) per member; coarse run start
@@ -868,16 +868,16 @@ __device__ __forceinline__ double updown_body_tma(const i64 tid, const i64 n0, c
   };
   // CG (STMG_UPDOWN_TMA == 2): the same runs, copied by all threads in
   // 16-byte cp.async.cg chunks (L2 -> shared, no L1 allocation); chunk
-  // k = threadIdx.x + 128 i of a stage.  Fine-run sources at n = 0 are
+  // k = threadIdx.x + BT i of a stage.  Fine-run sources at n = 0 are
   // precomputed (n is even, so n * slab keeps the 16-byte alignment).
   constexpr bool CG = STMG_UPDOWN_TMA == 2;
-  constexpr int HC = SEG / 2, NCH = S::NC * HC, KPT = (NCH + 127) / 128;
+  constexpr int HC = SEG / 2, NCH = S::NC * HC, KPT = (NCH + BT - 1) / BT;
   const double* csrc[KPT];
   unsigned cdst[KPT];
   if (CG) {
 #pragma unroll
     for (int i = 0; i < KPT; ++i) {
-      const int k = int(threadIdx.x) + 128 * i;
+      const int k = int(threadIdx.x) + BT * i;
       const int c = k / HC, j = k - c * HC;
       cdst[i] = unsigned(c * SEG + 2 * j) * 8u;
       csrc[i] = nullptr;
@@ -892,7 +892,7 @@ __device__ __forceinline__ double updown_body_tma(const i64 tid, const i64 n0, c
     const unsigned base = ring_s + unsigned(st * S::STAGE) * 8u;
 #pragma unroll
     for (int i = 0; i < KPT; ++i) {
-      const int k = int(threadIdx.x) + 128 * i;
+      const int k = int(threadIdx.x) + BT * i;
       if (k >= NCH) break;
       const int c = k / HC;
       const double* src;
@@ -1045,15 +1045,18 @@ __device__ __forceinline__ double updown_body_tma(const i64 tid, const i64 n0, c
 #define STMG_UPDOWN_MINB2 4  // p_t <= 1: 4 CTAs/SM (v16 A/B vs 5 and 3: C2 1.691 -> 1.669 ms,
                              // C4/C5 -1.5 %; profiles/r01_v16_minb_ab.txt)
 #endif
-template <int DIM, int NL>
-__global__ void __launch_bounds__(128, (NL <= 2 ? STMG_UPDOWN_MINB2 : NL == 3 ? STMG_UPDOWN_MINB3 : 1)) k_updown_tma(const double* __restrict__ ec,
-                                                    const PingPong pp,
-                                                    const double* __restrict__ f,
-                                                    double* __restrict__ fc,
-                                                    double* __restrict__ partials, const TM<NL> t,
-                                                    const SP s, const i64 n_t, const int C,
-                                                    const i64 n1c, const double omega,
-                                                    const i64 s0) {
+// BT threads per CTA: 128, or 256 (p_t <= 1) where the level is large: twice
+// the alias groups per CTA double the length of every staged run (2D: 66
+// instead of 34 doubles, 3D: 34 instead of 18 -- the 2-double alignment slack
+// and the per-copy issue cost halve).  The choice is made on the host from the
+// GLOBAL level (pick_updown_block), so time-slab shards keep the single-shard
+// partial-sum layout.
+template <int DIM, int NL, int BT>
+__global__ void __launch_bounds__(BT, (BT == 128 ? (NL <= 2 ? STMG_UPDOWN_MINB2 : NL == 3 ? STMG_UPDOWN_MINB3 : 1)
+                                                  : STMG_UPDOWN_MINB2 / 2))
+k_updown_tma(const double* __restrict__ ec, const PingPong pp, const double* __restrict__ f,
+             double* __restrict__ fc, double* __restrict__ partials, const TM<NL> t, const SP s,
+             const i64 n_t, const int C, const i64 n1c, const double omega, const i64 s0) {
   __shared__ double sh[32];
   extern __shared__ __align__(16) double ring[];
   const unsigned bx = blockIdx.x, by = blockIdx.y;
@@ -1061,7 +1064,7 @@ __global__ void __launch_bounds__(128, (NL <= 2 ? STMG_UPDOWN_MINB2 : NL == 3 ? 
   const i64 n0 = i64(by) * C;
   const i64 nend = min(n0 + i64(C), n_t);
   const double sumsq =
-      updown_body_tma<DIM, NL>(tid, n0, nend, ec, pp, f, fc, t, s, n1c, omega, ring, s0);
+      updown_body_tma<DIM, NL, BT>(tid, n0, nend, ec, pp, f, fc, t, s, n1c, omega, ring, s0);
   pdl_trigger();
   const double tot = block_sum(sumsq, sh);
   if (threadIdx.x == 0) partials[i64(by) * gridDim.x + bx] = tot;
@@ -4162,7 +4165,9 @@ cudaError_t launch_updown(const LevelView& L, ModalArgs& a, const double* ec,
                           double* partials, cudaStream_t st, int64_t s0) {
   const SP s = make_sp(L.sp);
   const i64 lanes = ipow(s.G, L.sp.dim) << L.sp.dim;
-  const dim3 grid(grid1(lanes, 128), unsigned((L.n_t + a.chunk - 1) / a.chunk));
+  const bool tma = a.mode == 2 && STMG_UPDOWN_TMA;
+  const int bt = (tma && a.block == 256) ? 256 : 128;
+  const dim3 grid(grid1(lanes, bt), unsigned((L.n_t + a.chunk - 1) / a.chunk));
   a.n_partials = i64(grid.x) * grid.y;
   const PingPong pp{tbl, par};
   STMG_DISPATCH(L.sp.dim, L.tc.nl, {
@@ -4173,8 +4178,21 @@ cudaError_t launch_updown(const LevelView& L, ModalArgs& a, const double* ec,
     cudaFuncSetAttribute(k_updown<DIM, NL, 1>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          STMG_UPDOWN_CARVEOUT);
 #endif
-    if (a.mode == 2 && STMG_UPDOWN_TMA && s.G % TmaShape<DIM, NL>::GPB == 0)
-      PDLK(k_updown_tma<DIM, NL>, grid, 128, TmaShape<DIM, NL>::smem, st, ec, pp, f, fc,
+    if (bt == 256) {
+      if constexpr (DIM >= 2 && NL <= 2) {
+        if (s.G % TmaShape<DIM, NL, 256>::GPB != 0) return cudaErrorInvalidValue;
+        static PerDevice attr;
+        if (attr.first_use())
+          cudaFuncSetAttribute(k_updown_tma<DIM, NL, 256>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(TmaShape<DIM, NL, 256>::smem));
+        PDLK(k_updown_tma<DIM, NL, 256>, grid, 256, TmaShape<DIM, NL, 256>::smem, st, ec, pp, f,
+             fc, partials, t, s, L.n_t, a.chunk, a.n1c, a.omega, i64(s0));
+      } else {
+        return cudaErrorInvalidValue;  // pick_updown_block never asks for this
+      }
+    } else if (tma && s.G % TmaShape<DIM, NL>::GPB == 0)
+      PDLK(k_updown_tma<DIM, NL, 128>, grid, 128, TmaShape<DIM, NL>::smem, st, ec, pp, f, fc,
            partials, t, s, L.n_t, a.chunk, a.n1c, a.omega, i64(s0));
     else if (a.mode == 2)
       PDLK(k_updown<DIM, NL, 2>, grid, 128, updown_smem(NL), st, ec, pp, f, fc, partials, t,
@@ -4345,15 +4363,43 @@ void free_csub(CsubPlan* plan) {
   plan->n_ctas = plan->trees = 0;
 }
 
-int64_t partial_count(const LevelView& L, int chunk, bool grouped) {
+int64_t partial_count(const LevelView& L, int chunk, bool grouped, int block) {
   const i64 G = (L.sp.n1 + 1) / 2;
   const i64 units = grouped ? (ipow(G, L.sp.dim) << L.sp.dim) : L.sp.nx;
-  return i64(grid1(units, 128)) * ((L.n_t + chunk - 1) / chunk);
+  return i64(grid1(units, block)) * ((L.n_t + chunk - 1) / chunk);
+}
+
+#ifndef STMG_UPDOWN_BLOCK256_WAVES
+#define STMG_UPDOWN_BLOCK256_WAVES 0  // A/B: 256 wins on C2 (-1.1 %), C4 (-2.2 %), C5 (-1 %): profiles/r02_v8_updown_block256_ab.txt
+#endif
+// Threads per CTA of the fused level-0 kernel (launch_updown) for the level
+// `G` (the GLOBAL level: the result must not depend on the time-slab split).
+int pick_updown_block(const LevelView& G, int chunk, int mode) {
+  static const int forced = [] {
+    const char* e = std::getenv("STMG_UPDOWN_BLOCK");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (!(mode == 2 && STMG_UPDOWN_TMA == 2 && G.sp.dim >= 2 && G.tc.nl <= 2)) return 128;
+  const i64 g = (G.sp.n1 + 1) / 2;
+  const int nm = 1 << G.sp.dim;
+  if (g % (256 / nm) != 0) return 128;
+  if (forced == 128 || forced == 256) return forced;
+  static const int sms = [] {
+    int d = 0, n = 148;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    return n;
+  }();
+  const i64 lanes = ipow(g, G.sp.dim) << G.sp.dim;
+  const i64 chunks = (G.n_t + chunk - 1) / chunk;
+  // (a minimum number of waves of 256-thread CTAs can be required; measured: none needed)
+  return i64(grid1(lanes, 256)) * chunks >= i64(sms) * 2 * STMG_UPDOWN_BLOCK256_WAVES ? 256 : 128;
 }
 
 #ifndef STMG_CHUNK_TARGET
 #define STMG_CHUNK_TARGET (148 * 256)
 #endif
+
 // levels below STMG_CHUNK_BIG dofs (latency-bound coarse levels) may use
 // their own target (A/B: 148*64 ... 148*1024 for them are all slower on C2
 // than the common 148*256; profiles/r01_v17_chunk_small_ab.txt)

@@ -103,6 +103,7 @@ struct ModalArgs {
   int64_t n1c = 0;       // coarse nodes per axis (full coarsening)
   int mode = 1;          // 1 semi, 2 full (coarsening to the next level)
   int64_t n_partials = 0;  // out: number of partial sums written
+  int block = 128;         // threads per CTA of launch_updown (pick_updown_block)
 };
 // Pre-smooth (one damped block-Jacobi sweep) + residual + restriction.
 // zero_guess: u_in == 0 (coarse levels).  Writes u_out and fc.
@@ -131,8 +132,11 @@ cudaError_t launch_resnorm(const LevelView& L, ModalArgs& a, const double* u,
 
 // Chunk length heuristic for the modal kernels at a level.
 int pick_chunk(const LevelView& L, bool grouped);
-// Number of partial sums written by launch_up (grouped) / launch_resnorm.
-int64_t partial_count(const LevelView& L, int chunk, bool grouped);
+// Number of partial sums written by launch_up (grouped) / launch_resnorm
+// (block = 128) or launch_updown (block = pick_updown_block).
+int64_t partial_count(const LevelView& L, int chunk, bool grouped, int block = 128);
+// Threads per CTA of launch_updown for the GLOBAL level G (128 or 256).
+int pick_updown_block(const LevelView& G, int chunk, int mode);
 
 // Single-CTA coarse tail (levels[0..nlev) = the small levels down to the
 // coarsest).  The device table is built once (outside graph capture).
